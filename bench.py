@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark of the SRP-map hot path (BASELINE.json metric) on B200.
+
+Workload (config.workload): BASELINE configs[1] "C2" -- UCA M=8 (P=28 pairs),
+fs=16 kHz, frame length 1024 (512 bins), 10 s scene -> F=311 frames,
+J=50,000 candidates (50x50x20 over 5x5x2 m), N_aux=4 for the approximate
+path.  A step = one pass of the hot path over the 311-frame batch:
+GCC-PHAT -> lattice IDFT -> sinc interpolation (maps + fused argmax) for the
+headline ``value`` (Nyquist-approximate path), and GCC-PHAT -> conventional
+map (+ fused argmax) reported under ``conventional``.
+
+Timing: W untimed warm-ups, then K timed steps, each bracketed by CUDA
+events on the launching stream; L2 (126 MB) is flushed before every timed
+step by writing a 256 MiB buffer (outside the events).  Multi-GPU
+(torchrun): one process per GPU, every rank runs its own seeded scene (weak
+scaling, frames are independent -- no data-path collective); barrier +
+synchronize around the timed region and the max over ranks of the device
+time.  ``--impl reference`` times the reference's CPU algorithm (the oracle
+port in ``oracle/``) on the host cores, on bounded frame samples.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SRP frames·candidates/sec (conv & Nyquist-approx), % of HBM/tensor roofline"
+UNIT = "frames*candidates/s"
+FS = 16000.0
+T = 1.0 / FS
+N_AUX = 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-frames", type=int, default=6, help="frames in the CPU sample")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- workload
+def workload(rank=0):
+    from paper_2012_09499_b200 import scenes
+    from oracle import srp_oracle as O  # geometry helpers only (host constants)
+
+    scene = scenes.make_c2(scene_index=rank)
+    pairs = O.canonical_pairs(8)
+    pm = np.array([m for m, _ in pairs], np.int32)
+    pmp = np.array([mp for _, mp in pairs], np.int32)
+    bounds = np.array([np.linalg.norm(scene.mic_pos[m] - scene.mic_pos[mp]) / 343.0
+                       for m, mp in pairs])
+    tdoa = O.tdoa_table_nearfield(scene.mic_pos, scene.grid, pairs, 343.0)
+    omega = 2.0 * np.pi * np.arange(512) * FS / 1024
+    return scene, pm, pmp, bounds, tdoa, omega
+
+
+def config_dict(F, J, P, Kb, total_samples):
+    return {
+        "workload": "C2 (BASELINE configs[1]): UCA M=8 r=0.1 m, fs=16 kHz, frame 1024/hop 512, "
+                    "10 s white source + 6 image sources + diffuse noise 5 dB, 50x50x20 grid",
+        "frames": F, "candidates": J, "pairs": P, "bins": Kb, "n_aux": N_AUX,
+        "lattice_samples": total_samples, "value_path": "approx (GCC-PHAT + lattice + interp "
+        "+ argmax)", "l2": "flushed before every timed step (256 MiB write)",
+        "parallelism": "frame-parallel replicas (one seeded scene per rank)",
+    }
+
+
+# -------------------------------------------------------------- clocks probe
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- CPU baseline
+def cpu_sample(scene, pm, pmp, bounds, tdoa, omega, n_frames, conv_frames):
+    """Time the reference algorithm (oracle port) on host cores.
+
+    approx: cross_spectrum + build_gcc_lattice + srp_approx + argmax per frame
+    (sinc table precomputed and excluded, as the reference does,
+    experiment.py:339-344); conventional: cross_spectrum +
+    srp_conventional_frames + argmax (phase generation included, srp.py:421).
+    Returns f.c/s for both paths.
+    """
+    from oracle import srp_oracle as O
+
+    J = tdoa.shape[0]
+    Y = scene.Y.astype(np.complex128)
+    _, w = O.sinc_table(tdoa, bounds, T, N_AUX)  # untimed precompute
+    t0 = time.perf_counter()
+    for f in range(n_frames):
+        psi, _ = O.cross_spectrum(Y[f], pm, pmp)
+        _, rows = O.gcc_lattice(psi, omega, bounds, T, N_AUX)
+        O.argmax(O.approx_map(w, rows))
+    t_approx = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    psis = np.stack([O.cross_spectrum(Y[f], pm, pmp)[0] for f in range(conv_frames)])
+    maps = O.conventional_frames(psis, omega, tdoa, candidate_chunk=8192)
+    [O.argmax(m) for m in maps]
+    t_conv = time.perf_counter() - t0
+    return n_frames * J / t_approx, conv_frames * J / t_conv, t_approx, t_conv
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # the reference arm runs on rank 0 only
+    scene, pm, pmp, bounds, tdoa, omega = workload(0)
+    nf, cf = args.cpu_frames, 1
+    for _ in range(args.warmup):
+        cpu_sample(scene, pm, pmp, bounds, tdoa, omega, 1, 1)
+    vals, convs, ts = [], [], []
+    for _ in range(args.steps):
+        a, c, ta, tc = cpu_sample(scene, pm, pmp, bounds, tdoa, omega, nf, cf)
+        vals.append(a)
+        convs.append(c)
+        ts.append(ta)
+    value = float(np.median(vals))
+    cores = os.cpu_count()
+    sample = (f"{nf} C2 frames x {tdoa.shape[0]} candidates per step (approx); {cf} frame "
+              "per step (conventional); numpy/OpenBLAS, all host threads")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * float(np.median(ts)), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(311, tdoa.shape[0], 28, 512, None),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "conventional": {"value": float(np.median(convs)), "unit": UNIT},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2012_09499_b200 import _native
+    from paper_2012_09499_b200.plan import SrpPlan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    scene, pm, pmp, bounds, tdoa, omega = workload(rank)
+    plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=N_AUX, weights="stored",
+                   device=dev)
+    F, J, P, Kb = scene.Y.shape[0], plan.J, plan.P, plan.Kb
+    Y_host = torch.from_numpy(scene.Y).pin_memory()
+    Y = Y_host.to(dev)
+    maps_host = torch.empty((F, J), dtype=torch.float32).pin_memory()
+    am_host = torch.empty((F,), dtype=torch.int32).pin_memory()
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > L2
+    stream = torch.cuda.current_stream(dev)
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    def step(path, timers=None):
+        psi, _ = plan.cross_spectra(Y)
+        if path == "approx":
+            xi = plan.lattice(psi)
+            if timers:
+                timers[0].record(stream)
+            out = plan.approx(xi)
+            if timers:
+                timers[1].record(stream)
+        else:
+            if timers:
+                timers[0].record(stream)
+            out = plan.conventional(psi)
+            if timers:
+                timers[1].record(stream)
+        return out
+
+    def e2e_step(path):
+        Y.copy_(Y_host, non_blocking=True)
+        maps, am = step(path)
+        maps_host.copy_(maps, non_blocking=True)
+        am_host.copy_(am, non_blocking=True)
+
+    def timed(fn, path, kernel_timers=False):
+        for _ in range(args.warmup):
+            fn(path)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        tot, ktot = 0.0, 0.0
+        launches0 = _native.launch_count()
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = ev(), ev()
+            kt = (ev(), ev()) if kernel_timers else None
+            a.record(stream)
+            if kernel_timers:
+                fn(path, kt)
+            else:
+                fn(path)
+            b.record(stream)
+            b.synchronize()
+            tot += a.elapsed_time(b)
+            if kernel_timers:
+                ktot += kt[0].elapsed_time(kt[1])
+        torch.cuda.synchronize()
+        launches = _native.launch_count() - launches0
+        ms = tot / args.steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms, ktot / args.steps, launches
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms_a, k_a, launches_a = timed(step, "approx", kernel_timers=True)
+    ms_c, k_c, launches_c = timed(step, "conventional", kernel_timers=True)
+    clk = clocks.stop()
+    e2e_a, _, _ = timed(lambda p: e2e_step(p), "approx")
+    e2e_c, _, _ = timed(lambda p: e2e_step(p), "conventional")
+
+    units = F * J * world
+    value = units / (ms_a * 1e-3)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # TFLOP/s nominal FP32 SIMT
+    # dominant kernel of the approx step: K4 interpolation, 2 T_pad flops / (f.c)
+    k4_flops = 2.0 * plan.total_samples * F * J
+    k2_flops = 4.0 * P * Kb * F * J
+    roof_a = {"kernel": "srpb_interp (K4)", "bound": "fp32", "achieved": k4_flops / (k_a * 1e-3) / 1e12,
+              "peak": fp32_peak, "unit": "TFLOP/s", "traffic": None,
+              "peak_source": "nominal FP32 SIMT 148 SM x 128 lanes x 2 x 1.965 GHz (no measured "
+                             "FP32 peak in MEASURED_PEAKS.json)",
+              "flops_per_unit": 2.0 * plan.total_samples, "units_per_launch": F * J,
+              "kernel_ms": k_a}
+    roof_a["frac"] = roof_a["achieved"] / roof_a["peak"]
+    roof_c = {"kernel": "srpb_conventional (K2)", "bound": "fp32",
+              "achieved": k2_flops / (k_c * 1e-3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
+              "traffic": None, "flops_per_unit": 4.0 * P * Kb, "units_per_launch": F * J,
+              "kernel_ms": k_c}
+    roof_c["frac"] = roof_c["achieved"] / roof_c["peak"]
+    h2d = F * scene.Y.shape[1] * Kb * 8
+    d2h = F * J * 4 + F * 4
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_a, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (seeded C2 scenes, one per rank; reference publishes no dataset)",
+        "config": config_dict(F, J, P, Kb, plan.total_samples),
+        "e2e": {"value": units / (e2e_a * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_a,
+                "api": "SrpPlan.run on pinned host Y -> pinned host maps + argmax"},
+        "gpu_launches": launches_a // max(args.steps, 1) * args.steps,
+        "roofline": roof_a,
+        "conventional": {"value": units / (ms_c * 1e-3), "unit": UNIT, "ms_per_step": ms_c,
+                         "e2e": {"value": units / (e2e_c * 1e-3), "unit": UNIT,
+                                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                                 "ms_per_step": e2e_c},
+                         "gpu_launches": launches_c, "roofline": roof_c},
+        "clocks": clk,
+        "peaks_used": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained")},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        a, c, ta, tc = cpu_sample(scene, pm, pmp, bounds, tdoa, omega, args.cpu_frames, 1)
+        out["cpu_baseline"] = {
+            "value": a, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{args.cpu_frames} C2 frames x {J} candidates (approx path, oracle port "
+                      f"of the reference, {ta:.2f} s); conventional 1 frame: {c:.3e} f.c/s "
+                      f"({tc:.2f} s)",
+            "conventional_value": c,
+        }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,164 @@
+/*
+ * srpb.h -- C ABI of the B200-native SRP-map hot path (libsrpb.so).
+ *
+ * The reference (srpfast, arXiv 2012.09499) is pure Python/numpy; it has no
+ * FFI of its own.  Its drop-in boundary is the Python function API of
+ * srpfast.spectral / srpfast.srp (re-exported at pkg/src/srpfast/__init__.py
+ * :43-66).  These entry points are what that API binds, one per numpy
+ * "kernel" of the reference.  The Python mirror of the
+ * reference API (paper_2012_09499_b200/spectral.py, srp.py) calls them via
+ * ctypes; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - every pointer argument is a DEVICE pointer unless stated otherwise;
+ *    complex data is interleaved (re, im) float pairs ("complex64");
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *  - calls are asynchronous and stream ordered; nothing is allocated or
+ *    freed, no global mutable state is kept (re-entrant);
+ *  - return 0 on success, <0 invalid argument (nothing launched),
+ *    >0 a cudaError_t from the launch; srpb_last_error() gives a
+ *    thread-local message for the last failing call on this thread.
+ *
+ * Shapes: F frames, M channels, Kb one-sided bins (DC kept, Nyquist dropped,
+ * spectral.py:70-73), P pairs in canonical order (geometry.py:141-176),
+ * J candidates, T_pad = padded total lattice samples (multiple of 32).
+ */
+#ifndef SRPB_H
+#define SRPB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRPB_WEIGHT_PHAT 0
+#define SRPB_WEIGHT_IDENTITY 1
+
+/* Version of this ABI (bumped on any signature change). */
+int srpb_abi_version(void);
+
+/* Message of the last failing call on the calling thread ("" if none). */
+const char* srpb_last_error(void);
+
+/*
+ * K1 GCC-PHAT cross-spectra for F frames.
+ * Replaces spectral.cross_spectrum (pkg/src/srpfast/spectral.py:218-285),
+ * batched over frames.
+ *   Y        [F, M, Kb] complex64 STFT frames
+ *   pair_m, pair_mp [P] int32 channel indices (index_m, index_m_prime)
+ *   weighting SRPB_WEIGHT_PHAT or SRPB_WEIGHT_IDENTITY
+ *   floor_rel adaptive floor factor (DEFAULT_PHAT_FLOOR_REL = 1e-12,
+ *             spectral.py:31-32) used when abs_floor <= 0
+ *   abs_floor explicit floor (> 0) or <= 0 for the adaptive floor
+ *   Psi      [F, P, Kb] complex64 out: psi = raw / max(|raw|, floor), 0 where
+ *            raw == 0 (phat) or psi = raw (identity)
+ *   floor_out [F] float64 out (may be NULL): the floor applied per frame
+ *            (0 under identity weighting)
+ */
+int srpb_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                  const int32_t* pair_mp, int P, int weighting, double floor_rel,
+                  double abs_floor, float* Psi, double* floor_out, void* stream);
+
+/*
+ * K2 conventional SRP maps (harmonic bins w_k = k w_1).
+ * Replaces srp.srp_conventional_frames (srp.py:391-429) incl. the steering
+ * phases of srp._phase_matrix (srp.py:350-373), generated on the fly:
+ *   SRP[f, j] = sum_p 2 Re sum_k psi[f,p,k] e^{j k w_1 tau[j,p]}
+ * with w_1 tau[j,p] / 2pi = (tau_i[p,j] + tau_f[p,j]) / period.
+ *   Psi      [F, P, Kb] complex64
+ *   tau_i    [P, J] int32, tau_f [P, J] float32 (|tau_f| <= 1/2): host split
+ *            of x = w_1 tau period / 2pi (fp64) into rint + fraction
+ *   period   integer period of the phase (the frame length N = 2 Kb)
+ *   maps     [F, J] float32 out, or NULL (argmax only)
+ *   keys     [F] uint64 in/out, or NULL: running packed argmax keys
+ *            (srpb_argmax_keys_reset first); see srpb_keys_to_index
+ */
+int srpb_conventional(const float* Psi, int F, int P, int Kb, int period,
+                      const int32_t* tau_i, const float* tau_f, int J, float* maps,
+                      unsigned long long* keys, void* stream);
+
+/*
+ * K2g conventional SRP maps for arbitrary (non-harmonic) bins: the dense
+ * exp branch of srp._phase_matrix (srp.py:366-367), phases in fp64.
+ *   omega [Kb] float64 rad/s, tau [J, P] float64 seconds
+ */
+int srpb_conventional_general(const float* Psi, int F, int P, int Kb,
+                              const double* omega, const double* tau, int J,
+                              float* maps, unsigned long long* keys, void* stream);
+
+/*
+ * Lattice twiddles e^{j w_k n T} for n in [-L, L], fp64 phases rounded to fp32.
+ * Signal-independent table of srp.build_gcc_lattice (srp.py:235-236).
+ *   omega [Kb] float64, tw [2L+1, Kb] complex64 out (row 0 = lag -L)
+ */
+int srpb_lattice_twiddles(const double* omega, int Kb, double sample_period, int L,
+                          float* tw, void* stream);
+
+/*
+ * K3 lattice GCC samples for F frames.
+ * Replaces srp.build_gcc_lattice (srp.py:201-247):
+ *   Xi[f, off[p] + n + reach[p]] = 2 Re sum_k psi[f,p,k] tw[L + n, k]
+ *   for n in [-reach[p], reach[p]], reach[p] = N_p + n_aux.
+ *   off [P+1] int32 prefix sums of 2 reach + 1; pad columns [off[P], T_pad)
+ *   are written as 0.
+ *   Xi [F, T_pad] float32 out
+ */
+int srpb_lattice(const float* Psi, int F, int P, int Kb, const float* tw, int L,
+                 const int32_t* off, const int32_t* reach, int T_pad, float* Xi,
+                 void* stream);
+
+/*
+ * Sinc interpolation table W[j, off[p] + n + reach[p]] = sinc(x[j,p] - n),
+ * exact 1/0 at integer arguments (srp._sinc_kernel srp.py:250-261,
+ * srp.precompute_sinc_table srp.py:287-317), x = tau / T split on the host in
+ * fp64 into sx_i [P, J] int32 = rint(x) and sx_f [P, J] float32 = x - rint(x).
+ *   W [J, T_pad] float32 out (pad columns 0)
+ */
+int srpb_sinc_table(const int32_t* sx_i, const float* sx_f, int J, int P,
+                    const int32_t* off, const int32_t* reach, int T_pad, float* W,
+                    void* stream);
+
+/*
+ * K4 approximate SRP maps from lattice samples: maps = Xi W^T.
+ * Replaces srp.srp_approx (srp.py:320-347), batched over frames.
+ *   W [J, T_pad] float32 (srpb_sinc_table), Xi [F, T_pad] float32
+ *   maps [F, J] float32 out or NULL; keys [F] as in srpb_conventional
+ */
+int srpb_interp(const float* W, const float* Xi, int F, int J, int T_pad, float* maps,
+                unsigned long long* keys, void* stream);
+
+/*
+ * K4f approximate maps with the sinc weights generated on the fly from the
+ * split TDOAs (no stored W; the only option when J x T_pad does not fit,
+ * e.g. C4's 361 GB table).  Same arithmetic as srpb_sinc_table + srpb_interp.
+ */
+int srpb_interp_onthefly(const int32_t* sx_i, const float* sx_f, int P,
+                         const int32_t* off, const int32_t* reach, const float* Xi,
+                         int F, int J, int T_pad, float* maps, unsigned long long* keys,
+                         void* stream);
+
+/*
+ * K5 per-frame argmax, lowest index on ties (srp.argmax_candidate,
+ * srp.py:107-109) over stored maps [F, J]: folds into keys [F].
+ */
+int srpb_argmax(const float* maps, int F, int J, unsigned long long* keys, void* stream);
+
+/*
+ * K5d argmax over float64 maps [F, J] (maps built on the host, e.g. an
+ * SrpMap whose values came from numpy): idx[f] int32 = first maximum,
+ * exactly numpy.argmax (srp.py:109).
+ */
+int srpb_argmax_f64(const double* maps, int F, int J, int32_t* idx, void* stream);
+
+/* keys[f] = 0 for f < F (the identity of the packed-key max). */
+int srpb_argmax_keys_reset(unsigned long long* keys, int F, void* stream);
+
+/* idx[f] = candidate index held by keys[f] (int32). */
+int srpb_keys_to_index(const unsigned long long* keys, int F, int32_t* idx, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SRPB_H */

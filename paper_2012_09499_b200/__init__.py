@@ -1,0 +1,66 @@
+"""B200-native SRP-map hot path of arXiv 2012.09499 (drop-in for ``srpfast``).
+
+GCC-PHAT cross-spectra -> {conventional SRP | Nyquist lattice IDFT + sinc
+interpolation} -> per-frame argmax, as hand-written sm_100a CUDA kernels in
+``libsrpb.so`` (C ABI: ``include/srpb.h``) driven from PyTorch host code.
+
+The public names mirror the reference's hot-path API
+(``pkg/src/srpfast/__init__.py:13-66``: geometry inputs, spectral and srp
+functions and types); :class:`SrpPlan` is the batched device-resident entry.
+There is no CPU fallback: without the library and a CUDA device the compute
+functions raise.
+"""
+
+from .geometry import (
+    CandidateGrid,
+    MicArray,
+    MicPair,
+    build_tdoa_table,
+    circular_array,
+    enumerate_pairs,
+    tdoa_farfield,
+    tdoa_nearfield,
+)
+from .plan import SrpPlan, lattice_layout, standalone_argmax
+from .spectral import (
+    DEFAULT_PHAT_FLOOR_REL,
+    CrossSpectra,
+    FrameSpec,
+    SpectralFrame,
+    cross_spectrum,
+    cross_spectrum_frames,
+    stft_analyze,
+)
+from .srp import (
+    ComplexityReport,
+    GccLattice,
+    MultCounter,
+    SincTable,
+    SrpMap,
+    argmax_candidate,
+    build_gcc_lattice,
+    build_gcc_lattice_frames,
+    complexity_report,
+    gcc_at_lag,
+    lattice_half_counts,
+    precompute_sinc_table,
+    srp_approx,
+    srp_approx_frames,
+    srp_conventional,
+    srp_conventional_frames,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CandidateGrid", "MicArray", "MicPair", "build_tdoa_table", "circular_array",
+    "enumerate_pairs", "tdoa_farfield", "tdoa_nearfield",
+    "SrpPlan", "lattice_layout", "standalone_argmax",
+    "DEFAULT_PHAT_FLOOR_REL", "CrossSpectra", "FrameSpec", "SpectralFrame", "cross_spectrum",
+    "cross_spectrum_frames", "stft_analyze",
+    "ComplexityReport", "GccLattice", "MultCounter", "SincTable", "SrpMap",
+    "argmax_candidate", "build_gcc_lattice", "build_gcc_lattice_frames", "complexity_report",
+    "gcc_at_lag", "lattice_half_counts", "precompute_sinc_table", "srp_approx",
+    "srp_approx_frames", "srp_conventional", "srp_conventional_frames",
+    "__version__",
+]

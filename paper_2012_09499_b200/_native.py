@@ -1,0 +1,128 @@
+"""ctypes binding of ``libsrpb.so`` (the C ABI declared in ``include/srpb.h``).
+
+There is deliberately no CPU fallback: if the library is missing or no CUDA
+device is present, every hot-path call raises.  Tensors are passed as raw
+device pointers (``tensor.data_ptr()``) and the current torch CUDA stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsrpb.so")
+_lib = None
+
+c_int, c_double, c_void_p = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+
+# name -> argtypes (restype int unless listed in _RESTYPES)
+_SIGNATURES = {
+    "srpb_abi_version": [],
+    "srpb_last_error": [],
+    "srpb_gcc_phat": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
+                      c_double, c_double, c_void_p, c_void_p, c_void_p],
+    "srpb_conventional": [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
+                          c_void_p, c_void_p, c_void_p],
+    "srpb_conventional_general": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
+                                  c_void_p, c_void_p, c_void_p],
+    "srpb_lattice_twiddles": [c_void_p, c_int, c_double, c_int, c_void_p, c_void_p],
+    "srpb_lattice": [c_void_p, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_void_p, c_int,
+                     c_void_p, c_void_p],
+    "srpb_sinc_table": [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p,
+                        c_void_p],
+    "srpb_interp": [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],
+    "srpb_interp_onthefly": [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int,
+                             c_int, c_int, c_void_p, c_void_p, c_void_p],
+    "srpb_argmax": [c_void_p, c_int, c_int, c_void_p, c_void_p],
+    "srpb_argmax_f64": [c_void_p, c_int, c_int, c_void_p, c_void_p],
+    "srpb_argmax_keys_reset": [c_void_p, c_int, c_void_p],
+    "srpb_keys_to_index": [c_void_p, c_int, c_void_p, c_void_p],
+}
+_RESTYPES = {"srpb_last_error": ctypes.c_char_p}
+
+
+class NativeError(RuntimeError):
+    """A CUDA launch or runtime failure reported by libsrpb."""
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load(path: str | None = None):
+    """Load and type the library (idempotent).  Raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or _LIB_PATH
+    if not os.path.exists(path):
+        raise ImportError(
+            f"libsrpb.so not found at {path}; build it with `make` or "
+            "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
+        )
+    lib = ctypes.CDLL(path)
+    for name, argtypes in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = _RESTYPES.get(name, c_int)
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    return tuple(_SIGNATURES)
+
+
+def ptr(t):
+    """Device pointer of a tensor (or 0 for None)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("hot-path tensors must live on a CUDA device")
+    return t.data_ptr()
+
+
+def stream_handle(device=None):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+_LAUNCHING = {n for n in _SIGNATURES if n not in ("srpb_abi_version", "srpb_last_error")}
+_launches = 0
+
+
+def launch_count() -> int:
+    """Kernel launches issued through the C ABI by this process so far."""
+    return _launches
+
+
+def call(name, *args):
+    """Invoke ``name`` and translate its status code.
+
+    <0 -> ValueError (invalid argument, nothing launched);
+    >0 -> NativeError (CUDA error from the launch).
+    """
+    global _launches
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if name in _LAUNCHING:
+        _launches += 1
+    if rc != 0:
+        msg = lib.srpb_last_error().decode(errors="replace")
+        if rc < 0:
+            raise ValueError(msg)
+        raise NativeError(msg)
+    return rc
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_2012_09499_b200 needs a CUDA device (B200); there is no CPU fallback"
+        )
+    load()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {dev}")
+    return dev

@@ -1,0 +1,173 @@
+// C ABI of libsrpb.so (declared in include/srpb.h): argument validation,
+// thread-local error messages, and stream-ordered launches.
+#include <cstdarg>
+#include <cstdio>
+
+#include "../../include/srpb.h"
+#include "common.cuh"
+
+namespace srpb {
+cudaError_t launch_gcc_phat(const float*, int, int, int, const int32_t*, const int32_t*, int, int,
+                            double, double, float*, double*, cudaStream_t);
+cudaError_t launch_conventional(const float*, int, int, int, int, const int32_t*, const float*,
+                                int, float*, unsigned long long*, cudaStream_t);
+cudaError_t launch_conventional_general(const float*, int, int, int, const double*,
+                                        const double*, int, float*, unsigned long long*,
+                                        cudaStream_t);
+cudaError_t launch_lattice_twiddles(const double*, int, double, int, float*, cudaStream_t);
+cudaError_t launch_lattice(const float*, int, int, int, const float*, int, const int32_t*,
+                           const int32_t*, int, int, float*, cudaStream_t);
+cudaError_t launch_sinc_table(const int32_t*, const float*, int, int, const int32_t*,
+                              const int32_t*, int, float*, cudaStream_t);
+cudaError_t launch_interp(const float*, const float*, int, int, int, float*,
+                          unsigned long long*, cudaStream_t);
+cudaError_t launch_interp_onthefly(const int32_t*, const float*, int, const int32_t*,
+                                   const int32_t*, const float*, int, int, int, float*,
+                                   unsigned long long*, cudaStream_t);
+cudaError_t launch_argmax(const float*, int, int, unsigned long long*, cudaStream_t);
+cudaError_t launch_argmax_f64(const double*, int, int, int32_t*, cudaStream_t);
+cudaError_t launch_keys_reset(unsigned long long*, int, cudaStream_t);
+cudaError_t launch_keys_to_index(const unsigned long long*, int, int32_t*, cudaStream_t);
+}  // namespace srpb
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return -1;
+}
+
+int status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return 0;
+  snprintf(g_err, sizeof(g_err), "%s: CUDA error %d (%s)", what, static_cast<int>(e),
+           cudaGetErrorString(e));
+  return static_cast<int>(e);
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+#define REQUIRE(cond, ...) \
+  do {                     \
+    if (!(cond)) return fail(__VA_ARGS__); \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+int srpb_abi_version(void) { return 1; }
+
+const char* srpb_last_error(void) { return g_err; }
+
+int srpb_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                  const int32_t* pair_mp, int P, int weighting, double floor_rel,
+                  double abs_floor, float* Psi, double* floor_out, void* stream) {
+  REQUIRE(F >= 0 && M >= 1 && Kb >= 1 && P >= 1, "srpb_gcc_phat: bad shape F=%d M=%d Kb=%d P=%d",
+          F, M, Kb, P);
+  REQUIRE(M <= 64, "srpb_gcc_phat: at most 64 channels supported, got %d", M);
+  REQUIRE(weighting == SRPB_WEIGHT_PHAT || weighting == SRPB_WEIGHT_IDENTITY,
+          "srpb_gcc_phat: unknown weighting %d", weighting);
+  REQUIRE(F == 0 || (Y && Psi && pair_m && pair_mp), "srpb_gcc_phat: null pointer");
+  return status(srpb::launch_gcc_phat(Y, F, M, Kb, pair_m, pair_mp, P, weighting, floor_rel,
+                                      abs_floor, Psi, floor_out, S(stream)),
+                "srpb_gcc_phat");
+}
+
+int srpb_conventional(const float* Psi, int F, int P, int Kb, int period, const int32_t* tau_i,
+                      const float* tau_f, int J, float* maps, unsigned long long* keys,
+                      void* stream) {
+  REQUIRE(F >= 0 && P >= 1 && Kb >= 1 && J >= 0, "srpb_conventional: bad shape");
+  REQUIRE(period >= 1 && period <= 46340, "srpb_conventional: period %d out of range", period);
+  REQUIRE(F == 0 || J == 0 || (Psi && tau_i && tau_f), "srpb_conventional: null pointer");
+  REQUIRE(maps || keys, "srpb_conventional: need maps and/or keys output");
+  return status(srpb::launch_conventional(Psi, F, P, Kb, period, tau_i, tau_f, J, maps, keys,
+                                          S(stream)),
+                "srpb_conventional");
+}
+
+int srpb_conventional_general(const float* Psi, int F, int P, int Kb, const double* omega,
+                              const double* tau, int J, float* maps, unsigned long long* keys,
+                              void* stream) {
+  REQUIRE(F >= 0 && P >= 1 && Kb >= 1 && J >= 0, "srpb_conventional_general: bad shape");
+  REQUIRE(F == 0 || J == 0 || (Psi && omega && tau), "srpb_conventional_general: null pointer");
+  REQUIRE(maps || keys, "srpb_conventional_general: need maps and/or keys output");
+  return status(srpb::launch_conventional_general(Psi, F, P, Kb, omega, tau, J, maps, keys,
+                                                  S(stream)),
+                "srpb_conventional_general");
+}
+
+int srpb_lattice_twiddles(const double* omega, int Kb, double sample_period, int L, float* tw,
+                          void* stream) {
+  REQUIRE(Kb >= 1 && L >= 0 && omega && tw, "srpb_lattice_twiddles: bad argument");
+  REQUIRE(sample_period > 0.0, "srpb_lattice_twiddles: sample_period must be positive");
+  return status(srpb::launch_lattice_twiddles(omega, Kb, sample_period, L, tw, S(stream)),
+                "srpb_lattice_twiddles");
+}
+
+int srpb_lattice(const float* Psi, int F, int P, int Kb, const float* tw, int L,
+                 const int32_t* off, const int32_t* reach, int T_pad, float* Xi, void* stream) {
+  REQUIRE(F >= 0 && P >= 1 && Kb >= 1 && L >= 0 && T_pad >= 1, "srpb_lattice: bad shape");
+  REQUIRE(F == 0 || (Psi && tw && off && reach && Xi), "srpb_lattice: null pointer");
+  return status(srpb::launch_lattice(Psi, F, P, Kb, tw, L, off, reach, 2 * L + 1, T_pad, Xi,
+                                     S(stream)),
+                "srpb_lattice");
+}
+
+int srpb_sinc_table(const int32_t* sx_i, const float* sx_f, int J, int P, const int32_t* off,
+                    const int32_t* reach, int T_pad, float* W, void* stream) {
+  REQUIRE(J >= 0 && P >= 1 && T_pad >= 1, "srpb_sinc_table: bad shape");
+  REQUIRE(J == 0 || (sx_i && sx_f && off && reach && W), "srpb_sinc_table: null pointer");
+  return status(srpb::launch_sinc_table(sx_i, sx_f, J, P, off, reach, T_pad, W, S(stream)),
+                "srpb_sinc_table");
+}
+
+int srpb_interp(const float* W, const float* Xi, int F, int J, int T_pad, float* maps,
+                unsigned long long* keys, void* stream) {
+  REQUIRE(F >= 0 && J >= 0 && T_pad >= 1, "srpb_interp: bad shape");
+  REQUIRE(T_pad % 32 == 0, "srpb_interp: T_pad must be a multiple of 32, got %d", T_pad);
+  REQUIRE(F == 0 || J == 0 || (W && Xi), "srpb_interp: null pointer");
+  REQUIRE(maps || keys, "srpb_interp: need maps and/or keys output");
+  return status(srpb::launch_interp(W, Xi, F, J, T_pad, maps, keys, S(stream)), "srpb_interp");
+}
+
+int srpb_interp_onthefly(const int32_t* sx_i, const float* sx_f, int P, const int32_t* off,
+                         const int32_t* reach, const float* Xi, int F, int J, int T_pad,
+                         float* maps, unsigned long long* keys, void* stream) {
+  REQUIRE(F >= 0 && J >= 0 && P >= 1 && T_pad >= 1, "srpb_interp_onthefly: bad shape");
+  REQUIRE(T_pad % 32 == 0, "srpb_interp_onthefly: T_pad must be a multiple of 32");
+  REQUIRE(F == 0 || J == 0 || (sx_i && sx_f && off && reach && Xi),
+          "srpb_interp_onthefly: null pointer");
+  REQUIRE(maps || keys, "srpb_interp_onthefly: need maps and/or keys output");
+  return status(srpb::launch_interp_onthefly(sx_i, sx_f, P, off, reach, Xi, F, J, T_pad, maps,
+                                             keys, S(stream)),
+                "srpb_interp_onthefly");
+}
+
+int srpb_argmax(const float* maps, int F, int J, unsigned long long* keys, void* stream) {
+  REQUIRE(F >= 0 && J >= 0, "srpb_argmax: bad shape");
+  REQUIRE(F == 0 || J == 0 || (maps && keys), "srpb_argmax: null pointer");
+  return status(srpb::launch_argmax(maps, F, J, keys, S(stream)), "srpb_argmax");
+}
+
+int srpb_argmax_f64(const double* maps, int F, int J, int32_t* idx, void* stream) {
+  REQUIRE(F >= 0 && J >= 0, "srpb_argmax_f64: bad shape");
+  REQUIRE(F == 0 || J == 0 || (maps && idx), "srpb_argmax_f64: null pointer");
+  return status(srpb::launch_argmax_f64(maps, F, J, idx, S(stream)), "srpb_argmax_f64");
+}
+
+int srpb_argmax_keys_reset(unsigned long long* keys, int F, void* stream) {
+  REQUIRE(F >= 0 && (F == 0 || keys), "srpb_argmax_keys_reset: bad argument");
+  return status(srpb::launch_keys_reset(keys, F, S(stream)), "srpb_argmax_keys_reset");
+}
+
+int srpb_keys_to_index(const unsigned long long* keys, int F, int32_t* idx, void* stream) {
+  REQUIRE(F >= 0 && (F == 0 || (keys && idx)), "srpb_keys_to_index: bad argument");
+  return status(srpb::launch_keys_to_index(keys, F, idx, S(stream)), "srpb_keys_to_index");
+}
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+// K2: conventional SRP maps with on-the-fly steering phases.
+//
+// Restates srp.srp_conventional_frames (pkg/src/srpfast/srp.py:391-429):
+//   SRP[f, j] = sum_p 2 Re( e^{j w_k tau[j,p]} . psi[f, p, :] )      (:420-422)
+// as one contraction over (pair, bin, re/im):
+//   A[j, (p,k,0)] = cos(theta_jpk), A[j, (p,k,1)] = -sin(theta_jpk)
+//   B[(p,k,c), f] = Psi[f, p, k].{re, im}   (the float view of Psi [F, P, Kb])
+//   maps = 2 * A B
+// The phase matrix (srp._phase_matrix, srp.py:350-373; a J x Kb complex128
+// table per pair in the reference, 491 GB fp32 at C3 for all pairs) is never
+// stored: every CTA generates its 128 x 16-bin A tile in shared memory and
+// reuses it across its 64 frames.
+//
+// Harmonic bins (w_k = k w_1): theta/2pi = k (i + f) / N with the integer
+// part reduced exactly (common.cuh).  Non-harmonic bins (the dense-exp branch,
+// srp.py:366-367): theta = w_k tau in fp64, reduced, then fp32 sincos.
+//
+// Roofline: FP32 pipe, 4 P Kb flops per frame.candidate.
+#include "simt_gemm.cuh"
+
+namespace srpb {
+
+constexpr int kBinsPerChunk = kTileK / 2;  // 16 bins -> 32 real K rows
+
+template <bool kHarmonic>
+__global__ void __launch_bounds__(kGemmThreads)
+conventional_simt_kernel(const float* __restrict__ Psi, int F, int P, int Kb, int period,
+                         int mask, const int32_t* __restrict__ tau_i,
+                         const float* __restrict__ tau_f, const double* __restrict__ omega,
+                         const double* __restrict__ tau, int J, float* __restrict__ maps,
+                         unsigned long long* __restrict__ keys) {
+  __shared__ __align__(16) SimtTiles s;
+  const int tid = threadIdx.x;
+  const int j0 = blockIdx.x * kTileJ;
+  const int f0 = blockIdx.y * kTileF;
+  const int tj = tid & 15, tf = tid >> 4;
+  const float inv_period = 1.0f / static_cast<float>(period);
+
+  // A-generation role: candidate jg, bins [half*8, half*8 + 8) of each chunk
+  const int jg_local = tid & (kTileJ - 1);
+  const int jg = j0 + jg_local;
+  const int half = tid >> 7;
+  // B-load role: frame fl, bins [q*4, q*4 + 4) of each chunk
+  const int fl = tid & (kTileF - 1);
+  const int q = tid >> 6;
+  const size_t row_stride = static_cast<size_t>(P) * Kb * 2;  // floats per frame
+
+  float acc[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0f;
+
+  for (int p = 0; p < P; ++p) {
+    int ti = 0;
+    float tfr = 0.0f;
+    double tau_jp = 0.0;
+    if (jg < J) {
+      if (kHarmonic) {
+        ti = tau_i[static_cast<size_t>(p) * J + jg];
+        tfr = tau_f[static_cast<size_t>(p) * J + jg];
+      } else {
+        tau_jp = tau[static_cast<size_t>(jg) * P + p];
+      }
+    }
+    for (int k0 = 0; k0 < Kb; k0 += kBinsPerChunk) {
+      // ---- A tile: steering phases of 128 candidates x 16 bins
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int kl = half * 8 + b;
+        const int k = k0 + kl;
+        float c = 0.0f, sn = 0.0f;
+        if (k < Kb) {
+          if (kHarmonic) {
+            harmonic_phase(k, ti, tfr, period, mask, inv_period, &c, &sn);
+          } else {
+            const double th = omega[k] * tau_jp;
+            double sd, cd;
+            sincos(th, &sd, &cd);
+            c = static_cast<float>(cd);
+            sn = static_cast<float>(sd);
+          }
+        }
+        s.A[2 * kl][jg_local] = c;
+        s.A[2 * kl + 1][jg_local] = -sn;
+      }
+      // ---- B tile: Psi[f, p, k0 .. k0+16) as 32 real rows
+      {
+        const int f = f0 + fl;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int kl = q * 4 + b;
+          const int k = k0 + kl;
+          float2 v = make_float2(0.0f, 0.0f);
+          if (f < F && k < Kb)
+            v = *reinterpret_cast<const float2*>(Psi + static_cast<size_t>(f) * row_stride +
+                                                 (static_cast<size_t>(p) * Kb + k) * 2);
+          s.B[2 * kl][fl] = v.x;
+          s.B[2 * kl + 1][fl] = v.y;
+        }
+      }
+      __syncthreads();
+      simt_mma_chunk(s, tj, tf, acc);
+      __syncthreads();
+    }
+  }
+  simt_epilogue(acc, 2.0f, j0, f0, J, F, tj, tf, maps, keys);
+}
+
+cudaError_t launch_conventional(const float* Psi, int F, int P, int Kb, int period,
+                                const int32_t* tau_i, const float* tau_f, int J, float* maps,
+                                unsigned long long* keys, cudaStream_t stream) {
+  if (F == 0 || J == 0) return cudaSuccess;
+  const int mask = (period & (period - 1)) == 0 ? period - 1 : 0;
+  dim3 grid((J + kTileJ - 1) / kTileJ, (F + kTileF - 1) / kTileF);
+  conventional_simt_kernel<true><<<grid, kGemmThreads, 0, stream>>>(
+      Psi, F, P, Kb, period, mask, tau_i, tau_f, nullptr, nullptr, J, maps, keys);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conventional_general(const float* Psi, int F, int P, int Kb,
+                                        const double* omega, const double* tau, int J,
+                                        float* maps, unsigned long long* keys,
+                                        cudaStream_t stream) {
+  if (F == 0 || J == 0) return cudaSuccess;
+  dim3 grid((J + kTileJ - 1) / kTileJ, (F + kTileF - 1) / kTileF);
+  conventional_simt_kernel<false><<<grid, kGemmThreads, 0, stream>>>(
+      Psi, F, P, Kb, 1, 0, nullptr, nullptr, omega, tau, J, maps, keys);
+  return cudaGetLastError();
+}
+
+}  // namespace srpb

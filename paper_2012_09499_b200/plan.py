@@ -1,0 +1,292 @@
+"""Device-resident SRP plan: the batched entry point of the hot path.
+
+One ``SrpPlan`` holds everything that depends only on geometry, bins and
+lattice parameters, uploaded/built once (SURVEY.md 8(b) "plan object caching
+device-resident geometry and W"):
+
+* pair index rows (``geometry.py:141-176`` canonical order),
+* the conventional steering split ``x = w_1 tau N / 2pi = i + f`` per
+  (pair, candidate) -- harmonic bins, ``srp.py:360-373`` -- or the raw fp64
+  ``tau``/``omega`` for non-harmonic bins (``srp.py:366-367``),
+* lattice layout ``N_p = floor(bound/T)`` (``srp.py:123-134``), reach
+  ``N_p + n_aux``, prefix offsets in ``np.concatenate`` order, the padded
+  width ``T_pad`` (multiple of 32), and the twiddles ``e^{j w_k n T}``,
+* the sinc split ``tau/T = i + f`` and, when it fits, the weight table
+  ``W [J, T_pad]`` built on the device (``srp.py:287-317``); otherwise the
+  interpolation kernel regenerates the weights on the fly.
+
+All per-frame work goes through ``libsrpb.so``; nothing here computes maps.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+DEFAULT_PHAT_FLOOR_REL = 1e-12  # spectral.py:31-32
+#: store W when it needs at most this many bytes (else generate on the fly)
+DEFAULT_MAX_WEIGHT_BYTES = 48 << 30
+
+
+def is_harmonic(omega: np.ndarray) -> bool:
+    """The reference's test for the recurrence branch (``srp.py:359-365``)."""
+    omega = np.asarray(omega, dtype=float)
+    return bool(
+        omega.size >= 2
+        and omega[0] == 0.0
+        and omega[1] > 0.0
+        and np.allclose(np.diff(omega), omega[1], rtol=1e-12, atol=0.0)
+    )
+
+
+def split_rint(x: np.ndarray):
+    """fp64 ``x`` -> (int64 rint(x), fp32 x - rint(x)), |fraction| <= 1/2."""
+    i = np.rint(x)
+    return i.astype(np.int64), (x - i).astype(np.float32)
+
+
+def lattice_layout(tdoa_bounds, sample_period, n_aux):
+    """Half counts, reach, prefix offsets, total and padded width."""
+    if not (sample_period > 0 and math.isfinite(sample_period)):
+        raise ValueError(f"sample_period must be positive, got {sample_period}")
+    if n_aux < 0 or int(n_aux) != n_aux:
+        raise ValueError(f"n_aux must be a non-negative integer, got {n_aux}")
+    halves = tuple(int(math.floor(b / sample_period)) for b in tdoa_bounds)
+    reach = np.array([h + int(n_aux) for h in halves], dtype=np.int32)
+    counts = 2 * reach + 1
+    off = np.zeros(len(halves) + 1, dtype=np.int32)
+    off[1:] = np.cumsum(counts)
+    total = int(off[-1])
+    t_pad = max(32, (total + 31) // 32 * 32)
+    return halves, reach, off, total, t_pad
+
+
+class SrpPlan:
+    """Geometry-dependent device state for conventional and approximate maps.
+
+    Parameters
+    ----------
+    tdoa_table : (J, P) float64 seconds, canonical pair order
+    pair_m, pair_mp : (P,) channel indices (``index_m``, ``index_m_prime``)
+    tdoa_bounds : (P,) seconds (``MicPair.tdoa_bound``)
+    bin_frequencies : (Kb,) rad/s
+    sample_period, n_aux : lattice spacing and guard samples (approximate
+        path); ``None`` builds the conventional path only
+    weights : ``"auto"`` | ``"stored"`` | ``"onthefly"``
+    """
+
+    def __init__(self, tdoa_table, pair_m, pair_mp, tdoa_bounds, bin_frequencies,
+                 sample_period=None, n_aux=None, weights="auto", device=None,
+                 max_weight_bytes=DEFAULT_MAX_WEIGHT_BYTES, conventional=True):
+        self.device = N.require_cuda(device)
+        table = np.asarray(tdoa_table, dtype=np.float64)
+        omega = np.asarray(bin_frequencies, dtype=np.float64)
+        if table.ndim != 2 or table.shape[0] == 0:
+            raise ValueError(f"tdoa_table must have shape (J, P), got {table.shape}")
+        self.J, self.P = table.shape
+        self.Kb = omega.size
+        if len(pair_m) != self.P or len(pair_mp) != self.P or len(tdoa_bounds) != self.P:
+            raise ValueError(f"grid table has {self.P} pair columns, expected {len(pair_m)}")
+        self.omega = omega
+        self.bounds = np.asarray(tdoa_bounds, dtype=np.float64)
+        dev = self.device
+        self.pair_m = torch.as_tensor(np.asarray(pair_m, dtype=np.int32), device=dev)
+        self.pair_mp = torch.as_tensor(np.asarray(pair_mp, dtype=np.int32), device=dev)
+        self.M = int(max(np.max(pair_m), np.max(pair_mp))) + 1
+        self.harmonic = is_harmonic(omega)
+        self.period = 2 * self.Kb
+
+        self._conv_ready = False
+        if conventional:
+            self._build_conventional(table)
+
+        self.sample_period = None
+        self.n_aux = None
+        self.W = None
+        if sample_period is not None:
+            self._build_lattice(table, float(sample_period), int(n_aux) if n_aux is not None else 0,
+                                weights, max_weight_bytes)
+
+    # ------------------------------------------------------------------ build
+    def _build_conventional(self, table):
+        dev = self.device
+        if self.harmonic:
+            # x = w_1 tau N / 2pi: theta_k / 2pi = k x / N (srp.py:370-372)
+            x = (self.omega[1] * table.T) * self.period / (2.0 * math.pi)
+            i, f = split_rint(x)
+            self.conv_ti = torch.as_tensor(np.mod(i, self.period).astype(np.int32), device=dev)
+            self.conv_tf = torch.as_tensor(np.ascontiguousarray(f), device=dev)
+            self._conv_x = x
+        else:
+            self.omega_dev = torch.as_tensor(self.omega, device=dev)
+            self.tau_dev = torch.as_tensor(np.ascontiguousarray(table), device=dev)
+        self._conv_ready = True
+
+    def _build_lattice(self, table, T, n_aux, weights, max_weight_bytes):
+        dev = self.device
+        halves, reach, off, total, t_pad = lattice_layout(self.bounds, T, n_aux)
+        self.sample_period, self.n_aux = T, n_aux
+        self.half_counts, self.total_samples, self.T_pad = halves, total, t_pad
+        self.reach_np, self.off_np = reach, off
+        self.reach = torch.as_tensor(reach, device=dev)
+        self.off = torch.as_tensor(off, device=dev)
+        self.L = int(reach.max())
+        self.omega_dev = torch.as_tensor(self.omega, device=dev)
+        self.twiddles = torch.empty((2 * self.L + 1, self.Kb, 2), dtype=torch.float32, device=dev)
+        s = N.stream_handle(dev)
+        N.call("srpb_lattice_twiddles", N.ptr(self.omega_dev), self.Kb, T, self.L,
+               N.ptr(self.twiddles), s)
+        # sinc split x = tau / T (srp.py:310)
+        xs = table.T / T
+        i, f = split_rint(xs)
+        if np.any(np.abs(i) > 2**30):
+            raise ValueError("tdoa / sample_period out of int32 range")
+        self.sx_i = torch.as_tensor(i.astype(np.int32), device=dev)
+        self.sx_f = torch.as_tensor(np.ascontiguousarray(f), device=dev)
+        need = self.J * t_pad * 4
+        if weights not in ("auto", "stored", "onthefly"):
+            raise ValueError(f"weights must be auto|stored|onthefly, got {weights!r}")
+        store = weights == "stored" or (weights == "auto" and need <= max_weight_bytes)
+        if store:
+            self.W = torch.empty((self.J, t_pad), dtype=torch.float32, device=dev)
+            N.call("srpb_sinc_table", N.ptr(self.sx_i), N.ptr(self.sx_f), self.J, self.P,
+                   N.ptr(self.off), N.ptr(self.reach), t_pad, N.ptr(self.W), s)
+        self.weight_mode = "stored" if store else "onthefly"
+
+    # ---------------------------------------------------------------- helpers
+    def _keys(self, F):
+        keys = torch.empty(F, dtype=torch.int64, device=self.device)
+        N.call("srpb_argmax_keys_reset", N.ptr(keys), F, N.stream_handle(self.device))
+        return keys
+
+    def keys_to_index(self, keys):
+        idx = torch.empty(keys.numel(), dtype=torch.int32, device=self.device)
+        N.call("srpb_keys_to_index", N.ptr(keys), keys.numel(), N.ptr(idx),
+               N.stream_handle(self.device))
+        return idx
+
+    def _check_frames(self, t, shape_tail, dtype, name):
+        if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if t.dtype != dtype or tuple(t.shape[1:]) != tuple(shape_tail) or not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous {dtype} [F, {shape_tail}], got "
+                             f"{t.dtype} {tuple(t.shape)}")
+
+    # -------------------------------------------------------------- hot path
+    def cross_spectra(self, Y, weighting="phat", phat_floor=None, out=None):
+        """K1: ``Y`` [F, M, Kb] complex64 -> (Psi [F, P, Kb] complex64,
+        applied floors [F] float64)."""
+        if weighting not in ("phat", "identity"):
+            raise ValueError(f"unknown weighting {weighting!r}")
+        if Y.dim() != 3 or Y.shape[2] != self.Kb:
+            raise ValueError(f"Y must be [F, M, {self.Kb}], got {tuple(Y.shape)}")
+        if Y.shape[1] < self.M:
+            raise ValueError(f"pair index {self.M - 1} out of range for {Y.shape[1]} channels")
+        self._check_frames(Y, (Y.shape[1], self.Kb), torch.complex64, "Y")
+        F = Y.shape[0]
+        abs_floor = -1.0
+        if weighting == "phat" and phat_floor is not None:
+            if not (phat_floor > 0 and math.isfinite(phat_floor)):
+                raise ValueError(f"phat_floor must be positive, got {phat_floor}")
+            abs_floor = float(phat_floor)
+        psi = out if out is not None else torch.empty((F, self.P, self.Kb), dtype=torch.complex64,
+                                                      device=self.device)
+        floors = torch.empty(F, dtype=torch.float64, device=self.device)
+        N.call("srpb_gcc_phat", N.ptr(Y), F, Y.shape[1], self.Kb, N.ptr(self.pair_m),
+               N.ptr(self.pair_mp), self.P, 0 if weighting == "phat" else 1,
+               DEFAULT_PHAT_FLOOR_REL, abs_floor, N.ptr(psi), N.ptr(floors),
+               N.stream_handle(self.device))
+        return psi, floors
+
+    def conventional(self, psi, maps=True, maps_out=None):
+        """K2 (+ fused K5): Psi [F, P, Kb] -> (maps [F, J] fp32 | None,
+        argmax [F] int32)."""
+        if not self._conv_ready:
+            raise ValueError("plan was built without the conventional path")
+        self._check_frames(psi, (self.P, self.Kb), torch.complex64, "psi")
+        F = psi.shape[0]
+        out = None
+        if maps:
+            out = maps_out if maps_out is not None else torch.empty(
+                (F, self.J), dtype=torch.float32, device=self.device)
+        keys = self._keys(F)
+        s = N.stream_handle(self.device)
+        if self.harmonic:
+            N.call("srpb_conventional", N.ptr(psi), F, self.P, self.Kb, self.period,
+                   N.ptr(self.conv_ti), N.ptr(self.conv_tf), self.J, N.ptr(out), N.ptr(keys), s)
+        else:
+            N.call("srpb_conventional_general", N.ptr(psi), F, self.P, self.Kb,
+                   N.ptr(self.omega_dev), N.ptr(self.tau_dev), self.J, N.ptr(out), N.ptr(keys), s)
+        return out, self.keys_to_index(keys)
+
+    def lattice(self, psi, out=None):
+        """K3: Psi [F, P, Kb] -> Xi [F, T_pad] fp32 (pad columns zero)."""
+        if self.sample_period is None:
+            raise ValueError("plan was built without a lattice (sample_period)")
+        self._check_frames(psi, (self.P, self.Kb), torch.complex64, "psi")
+        F = psi.shape[0]
+        xi = out if out is not None else torch.empty((F, self.T_pad), dtype=torch.float32,
+                                                     device=self.device)
+        N.call("srpb_lattice", N.ptr(psi), F, self.P, self.Kb, N.ptr(self.twiddles), self.L,
+               N.ptr(self.off), N.ptr(self.reach), self.T_pad, N.ptr(xi),
+               N.stream_handle(self.device))
+        return xi
+
+    def approx(self, xi, maps=True, maps_out=None):
+        """K4 (+ fused K5): Xi [F, T_pad] -> (maps [F, J] | None, argmax [F])."""
+        if self.sample_period is None:
+            raise ValueError("plan was built without a lattice (sample_period)")
+        self._check_frames(xi, (self.T_pad,), torch.float32, "xi")
+        F = xi.shape[0]
+        out = None
+        if maps:
+            out = maps_out if maps_out is not None else torch.empty(
+                (F, self.J), dtype=torch.float32, device=self.device)
+        keys = self._keys(F)
+        s = N.stream_handle(self.device)
+        if self.W is not None:
+            N.call("srpb_interp", N.ptr(self.W), N.ptr(xi), F, self.J, self.T_pad, N.ptr(out),
+                   N.ptr(keys), s)
+        else:
+            N.call("srpb_interp_onthefly", N.ptr(self.sx_i), N.ptr(self.sx_f), self.P,
+                   N.ptr(self.off), N.ptr(self.reach), N.ptr(xi), F, self.J, self.T_pad,
+                   N.ptr(out), N.ptr(keys), s)
+        return out, self.keys_to_index(keys)
+
+    def argmax(self, maps):
+        """K5 standalone over stored maps [F, J] fp32."""
+        if maps.dim() != 2 or maps.dtype != torch.float32 or not maps.is_contiguous():
+            raise ValueError("maps must be contiguous float32 [F, J]")
+        F, J = maps.shape
+        keys = self._keys(F)
+        N.call("srpb_argmax", N.ptr(maps), F, J, N.ptr(keys), N.stream_handle(self.device))
+        return self.keys_to_index(keys)
+
+    def run(self, Y, path="approx", maps=True, weighting="phat", phat_floor=None):
+        """Y [F, M, Kb] complex64 -> (maps | None, argmax) along ``path``."""
+        psi, _ = self.cross_spectra(Y, weighting, phat_floor)
+        if path == "conventional":
+            return self.conventional(psi, maps)
+        if path == "approx":
+            return self.approx(self.lattice(psi), maps)
+        raise ValueError(f"unknown path {path!r}")
+
+
+def standalone_argmax(maps: torch.Tensor) -> torch.Tensor:
+    """K5 over any [F, J] fp32 CUDA tensor (no plan needed)."""
+    N.require_cuda(maps.device)
+    if maps.dim() == 1:
+        maps = maps[None, :]
+    maps = maps.contiguous()
+    F, J = maps.shape
+    s = N.stream_handle(maps.device)
+    keys = torch.empty(F, dtype=torch.int64, device=maps.device)
+    N.call("srpb_argmax_keys_reset", N.ptr(keys), F, s)
+    N.call("srpb_argmax", N.ptr(maps), F, J, N.ptr(keys), s)
+    idx = torch.empty(F, dtype=torch.int32, device=maps.device)
+    N.call("srpb_keys_to_index", N.ptr(keys), F, N.ptr(idx), s)
+    return idx

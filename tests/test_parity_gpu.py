@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA path (through libsrpb.so's C ABI) vs the reference.
+
+Golden vectors come from running the unmodified reference
+(``tests/golden/make_golden.py``); larger seeded cases compare against the
+pinned oracle.  Tolerance (BASELINE.json north_star): per-frame relative L2
+map error <= 1e-5 for the fp32 path, identical argmax.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2012_09499_b200 as B
+from paper_2012_09499_b200 import scenes
+from paper_2012_09499_b200.plan import SrpPlan
+from oracle import srp_oracle as O
+from conftest import load_golden
+from helpers import REL_L2_TOL, assert_maps_match, rel_l2
+
+pytestmark = pytest.mark.gpu
+T = 1.0 / 16000.0
+
+
+def plan_from_golden(g, n_aux=None, weights="auto"):
+    return SrpPlan(g["tdoa"], g["pair_m"], g["pair_mp"], g["bounds"], g["omega"],
+                   sample_period=None if n_aux is None else T, n_aux=n_aux, weights=weights)
+
+
+def dev(x):
+    return torch.as_tensor(np.ascontiguousarray(x)).cuda()
+
+
+# --------------------------------------------------------------------- K1
+@pytest.mark.parametrize("name", ["c1", "c2_subset", "random_small", "on_lattice"])
+def test_gcc_phat_matches_reference(name):
+    g = load_golden(name)
+    plan = plan_from_golden(g)
+    psi, floors = plan.cross_spectra(dev(g["Y"]))
+    psi = psi.cpu().numpy()
+    assert np.max(np.abs(psi - g["psi"])) < 2e-6
+    np.testing.assert_allclose(floors.cpu().numpy(), g["floors"], rtol=1e-12)
+
+
+def test_gcc_phat_edge_cases():
+    g = load_golden("cross_edges")
+    pm, pmp = g["pair_m"], g["pair_mp"]
+    from paper_2012_09499_b200.spectral import gcc_phat_batch
+
+    for key in ("rand", "scaled", "zero_bin"):
+        psi, fl = gcc_phat_batch(dev(g[f"y_{key}"][None]), pm, pmp)
+        assert np.max(np.abs(psi[0].cpu().numpy() - g[f"psi_{key}"])) < 2e-6
+        assert fl.item() == pytest.approx(float(g[f"floor_{key}"]), rel=1e-12)
+    psi, _ = gcc_phat_batch(dev(g["y_zero_bin"][None]), pm, pmp)
+    assert torch.all(psi[0, :, 10] == 0)
+    raw, fl = gcc_phat_batch(dev(g["y_rand"][None]), pm, pmp, weighting="identity")
+    np.testing.assert_allclose(raw[0].cpu().numpy(), g["raw_rand"], rtol=1e-6, atol=1e-6)
+    psi, fl = gcc_phat_batch(dev(np.zeros((1, 4, 64), np.complex64)), pm, pmp)
+    assert torch.all(psi == 0) and fl.item() == 0.0
+    tiny = np.full((1, 2, 64), 1e-8 + 0j, dtype=np.complex64)
+    psi, fl = gcc_phat_batch(dev(tiny), [1], [0], phat_floor=1.0)
+    np.testing.assert_allclose(psi[0].cpu().numpy(), g["psi_tiny_floor1"], rtol=1e-5)
+    assert fl.item() == 1.0
+
+
+# --------------------------------------------------------------------- K2
+@pytest.mark.parametrize("name", ["c1", "c2_subset", "random_small", "on_lattice"])
+def test_conventional_matches_reference(name):
+    g = load_golden(name)
+    plan = plan_from_golden(g)
+    maps, am = plan.conventional(dev(g["psi"].astype(np.complex64)))
+    assert_maps_match(maps.cpu().numpy(), g["conv"], am.cpu().numpy(), what=name)
+    if name in ("c1", "c2_subset"):  # real-source scenes: argmax must be identical
+        assert list(am.cpu().numpy()) == list(g["argmax_conv"])
+
+
+def test_conventional_nonharmonic_bins():
+    g = load_golden("nonharmonic")
+    plan = SrpPlan(g["tdoa"], g["pair_m"], g["pair_mp"], g["bounds"], g["omega"])
+    assert not plan.harmonic
+    maps, am = plan.conventional(dev(g["psi"].astype(np.complex64)))
+    assert_maps_match(maps.cpu().numpy(), g["conv"], am.cpu().numpy(), what="nonharmonic")
+
+
+# --------------------------------------------------------------------- K3
+@pytest.mark.parametrize("name", ["c1", "c2_subset", "random_small", "on_lattice"])
+def test_lattice_matches_reference(name):
+    g = load_golden(name)
+    psi = dev(g["psi"].astype(np.complex64))
+    for n_aux in g["n_aux"]:
+        plan = plan_from_golden(g, int(n_aux))
+        assert list(plan.half_counts) == list(g[f"half_counts_{n_aux}"])
+        xi = plan.lattice(psi).cpu().numpy()
+        total = plan.total_samples
+        assert np.all(xi[:, total:] == 0.0)
+        for f in range(xi.shape[0]):
+            assert rel_l2(xi[f, :total], g[f"lattice_{n_aux}"][f]) <= REL_L2_TOL
+
+
+# --------------------------------------------------------------------- W
+def test_sinc_table_matches_reference():
+    g = load_golden("random_small")
+    plan = plan_from_golden(g, 1, weights="stored")
+    W = plan.W.cpu().numpy()
+    ref = g["sinc_w_1"]
+    assert np.max(np.abs(W[:, : ref.shape[1]] - ref)) < 1e-6
+    assert np.all(W[:, ref.shape[1]:] == 0.0)
+
+
+def test_sinc_table_exact_indicator_rows():
+    g = load_golden("sinc_integer")
+    plan = SrpPlan(g["tdoa"], [1], [0], g["bounds"], np.array([0.0, 1.0]), sample_period=T,
+                   n_aux=0, weights="stored")
+    W = plan.W.cpu().numpy()[:, : g["weights"].shape[1]]
+    assert np.array_equal(W, g["weights"].astype(np.float32))
+
+
+# --------------------------------------------------------------------- K4
+@pytest.mark.parametrize("weights", ["stored", "onthefly"])
+@pytest.mark.parametrize("name", ["c1", "c2_subset", "random_small", "on_lattice"])
+def test_approx_matches_reference(name, weights):
+    g = load_golden(name)
+    psi = dev(g["psi"].astype(np.complex64))
+    for n_aux in g["n_aux"]:
+        plan = plan_from_golden(g, int(n_aux), weights=weights)
+        maps, am = plan.approx(plan.lattice(psi))
+        assert_maps_match(maps.cpu().numpy(), g[f"approx_{n_aux}"], am.cpu().numpy(),
+                          what=f"{name} n_aux={n_aux} {weights}")
+        if name in ("c1", "c2_subset"):
+            assert list(am.cpu().numpy()) == list(g[f"argmax_approx_{n_aux}"])
+
+
+def test_approx_exact_on_lattice():
+    """Acceptance criterion 4: on-lattice TDOAs reconstruct the exact map."""
+    g = load_golden("on_lattice")
+    psi = dev(g["psi"].astype(np.complex64))
+    plan = plan_from_golden(g, 0)
+    maps, _ = plan.approx(plan.lattice(psi))
+    conv, _ = plan_from_golden(g).conventional(psi)
+    for f in range(maps.shape[0]):
+        assert rel_l2(maps[f].cpu().numpy(), conv[f].cpu().numpy()) <= REL_L2_TOL
+
+
+# ------------------------------------------------------- end to end (Y -> maps)
+@pytest.mark.parametrize("path", ["conventional", "approx"])
+def test_end_to_end_from_stft(path):
+    g = load_golden("c1")
+    plan = plan_from_golden(g, 2)
+    maps, am = plan.run(dev(g["Y"]), path=path)
+    ref = g["conv"] if path == "conventional" else g["approx_2"]
+    refam = g["argmax_conv"] if path == "conventional" else g["argmax_approx_2"]
+    assert_maps_match(maps.cpu().numpy(), ref, am.cpu().numpy(), what=path)
+    assert list(am.cpu().numpy()) == list(refam)
+
+
+def test_argmax_only_mode_matches_maps_mode():
+    g = load_golden("c2_subset")
+    plan = plan_from_golden(g, 4)
+    Y = dev(g["Y"])
+    m1, a1 = plan.run(Y, "approx", maps=True)
+    m0, a0 = plan.run(Y, "approx", maps=False)
+    assert m0 is None and torch.equal(a0, a1)
+    assert torch.equal(B.standalone_argmax(m1), a1)
+
+
+# -------------------------------------------- larger seeded shapes vs oracle
+def _oracle_case(scene, J, F, n_aux, weights="auto"):
+    pairs = O.canonical_pairs(scene.mic_pos.shape[0])
+    pm = np.array([m for m, _ in pairs], np.int32)
+    pmp = np.array([mp for _, mp in pairs], np.int32)
+    c = scene.speed_of_sound
+    bounds = np.array([np.linalg.norm(scene.mic_pos[m] - scene.mic_pos[mp]) / c for m, mp in pairs])
+    grid = scene.grid[np.linspace(0, scene.grid.shape[0] - 1, J).astype(int)]
+    tdoa = O.tdoa_table_nearfield(scene.mic_pos, grid, pairs, c)
+    omega = O.bin_frequencies(16000.0, scene.frame_length)
+    Y = scene.Y[:F]
+    psi = np.stack([O.cross_spectrum(Y[f].astype(complex), pm, pmp)[0] for f in range(F)])
+    plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=n_aux, weights=weights)
+    return plan, psi, omega, tdoa, bounds, Y
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_config_shapes_vs_oracle(cfg):
+    if cfg == "c2":
+        scene, J, F, n_aux, w = scenes.make_c2(num_frames=6), 3000, 6, 4, "stored"
+    elif cfg == "c3":
+        scene, J, F, n_aux, w = scenes.make_c3(num_frames=3), 800, 3, 8, "stored"
+    else:
+        scene, J, F, n_aux, w = scenes.make_c4(num_frames=2), 300, 2, 2, "onthefly"
+    plan, psi, omega, tdoa, bounds, Y = _oracle_case(scene, J, F, n_aux, w)
+    psi_g, _ = plan.cross_spectra(dev(Y))
+    assert np.max(np.abs(psi_g.cpu().numpy() - psi)) < 2e-6
+    conv_ref = O.conventional_frames(psi, omega, tdoa, candidate_chunk=512)
+    conv, am = plan.conventional(psi_g)
+    assert_maps_match(conv.cpu().numpy(), conv_ref, am.cpu().numpy(), what=f"{cfg} conv")
+    _, wts = O.sinc_table(tdoa, bounds, T, n_aux)
+    approx_ref = np.stack([O.approx_map(wts, O.gcc_lattice(psi[f], omega, bounds, T, n_aux)[1])
+                           for f in range(F)])
+    maps, am = plan.approx(plan.lattice(psi_g))
+    assert_maps_match(maps.cpu().numpy(), approx_ref, am.cpu().numpy(), what=f"{cfg} approx")
+
+
+# ------------------------------------ size-independent properties at full C2
+def test_full_c2_frame_sharding_and_determinism():
+    """BASELINE config C2 at full size (J=50k, F=311): maps are independent
+    of how frames are batched (the sharding invariant), bitwise repeatable,
+    and the fused argmax equals the standalone K5 over the stored maps."""
+    scene = scenes.make_c2()
+    pairs = O.canonical_pairs(8)
+    pm = np.array([m for m, _ in pairs], np.int32)
+    pmp = np.array([mp for _, mp in pairs], np.int32)
+    bounds = np.array([np.linalg.norm(scene.mic_pos[m] - scene.mic_pos[mp]) / 343.0
+                       for m, mp in pairs])
+    tdoa = O.tdoa_table_nearfield(scene.mic_pos, scene.grid, pairs, 343.0)
+    omega = O.bin_frequencies(16000.0, 1024)
+    plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=4)
+    Y = dev(scene.Y)
+    assert Y.shape == (311, 8, 512) and plan.J == 50000
+    for path in ("approx", "conventional"):
+        full, am = plan.run(Y, path)
+        again, am2 = plan.run(Y, path)
+        assert torch.equal(full, again) and torch.equal(am, am2)
+        parts = [plan.run(Y[lo:lo + 100].contiguous(), path) for lo in range(0, 311, 100)]
+        assert torch.equal(torch.cat([p[0] for p in parts]), full)
+        assert torch.equal(torch.cat([p[1] for p in parts]), am)
+        assert torch.equal(B.standalone_argmax(full), am)
+    # spot-check two frames against the oracle at full J
+    sel = [0, 200]
+    psi = np.stack([O.cross_spectrum(scene.Y[f].astype(complex), pm, pmp)[0] for f in sel])
+    conv_ref = O.conventional_frames(psi, omega, tdoa, candidate_chunk=4096)
+    conv, _ = plan.run(Y, "conventional")
+    for i, f in enumerate(sel):
+        assert rel_l2(conv[f].cpu().numpy(), conv_ref[i]) <= REL_L2_TOL
+        assert int(np.argmax(conv_ref[i])) == int(torch.argmax(conv[f]).item())
