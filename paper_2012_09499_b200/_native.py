@@ -81,6 +81,8 @@ def ptr(t):
         return None
     if not t.is_cuda:
         raise ValueError("hot-path tensors must live on a CUDA device")
+    if not t.is_contiguous():
+        raise ValueError("hot-path tensors must be contiguous (row-major)")
     return t.data_ptr()
 
 

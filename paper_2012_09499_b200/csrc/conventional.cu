@@ -46,10 +46,14 @@ conventional_simt_kernel(const float* __restrict__ Psi, int F, int P, int Kb, in
   const size_t row_stride = static_cast<size_t>(P) * Kb * 2;  // floats per frame
 
   float acc[8][4];
+  double tot[8][4];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0f;
+    for (int c = 0; c < 4; ++c) {
+      acc[a][c] = 0.0f;
+      tot[a][c] = 0.0;
+    }
 
   for (int p = 0; p < P; ++p) {
     int ti = 0;
@@ -103,8 +107,9 @@ conventional_simt_kernel(const float* __restrict__ Psi, int F, int P, int Kb, in
       simt_mma_chunk(s, tj, tf, acc);
       __syncthreads();
     }
+    simt_fold(acc, tot);  // one pair done: fold into fp64
   }
-  simt_epilogue(acc, 2.0f, j0, f0, J, F, tj, tf, maps, keys);
+  simt_epilogue(tot, 2.0, j0, f0, J, F, tj, tf, maps, keys);
 }
 
 cudaError_t launch_conventional(const float* Psi, int F, int P, int Kb, int period,

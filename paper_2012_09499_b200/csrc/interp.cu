@@ -75,10 +75,14 @@ interp_simt_kernel(const float* __restrict__ W, const int32_t* __restrict__ sx_i
   float gf = 0.0f, gsp = 0.0f;
 
   float acc[8][4];
+  double tot[8][4];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0f;
+    for (int c = 0; c < 4; ++c) {
+      acc[a][c] = 0.0f;
+      tot[a][c] = 0.0;
+    }
 
   for (int t0 = 0; t0 < T_pad; t0 += kTileK) {
     if (kOnTheFly) {
@@ -129,8 +133,10 @@ interp_simt_kernel(const float* __restrict__ W, const int32_t* __restrict__ sx_i
     __syncthreads();
     simt_mma_chunk(s, tj, tf, acc);
     __syncthreads();
+    if (((t0 / kTileK) & 15) == 15) simt_fold(acc, tot);  // every 512 columns
   }
-  simt_epilogue(acc, 1.0f, j0, f0, J, F, tj, tf, maps, keys);
+  simt_fold(acc, tot);
+  simt_epilogue(tot, 1.0, j0, f0, J, F, tj, tf, maps, keys);
 }
 
 cudaError_t launch_sinc_table(const int32_t* sx_i, const float* sx_f, int J, int P,

@@ -40,9 +40,24 @@ __device__ __forceinline__ void simt_mma_chunk(const SimtTiles& s, int tj, int t
   }
 }
 
+// Fold the fp32 partial sums into the fp64 totals and restart them.  K2
+// folds once per pair, K4 every 512 lattice columns: the fp32 partials then
+// sum at most ~2K terms, and the long reduction over pairs (C4: 496 pairs x
+// 1024 terms) runs in fp64 like the reference's per-pair accumulation
+// (srp.py:422, srp.py:342).
+__device__ __forceinline__ void simt_fold(float (&acc)[8][4], double (&tot)[8][4]) {
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      tot[a][c] += static_cast<double>(acc[a][c]);
+      acc[a][c] = 0.0f;
+    }
+}
+
 // Epilogue: scale, store maps (row-major [F, J]) and fold the per-frame
 // argmax of this tile into keys[f] (lowest j on ties).
-__device__ __forceinline__ void simt_epilogue(const float (&acc)[8][4], float scale, int j0,
+__device__ __forceinline__ void simt_epilogue(const double (&acc)[8][4], double scale, int j0,
                                               int f0, int J, int F, int tj, int tf,
                                               float* __restrict__ maps,
                                               unsigned long long* __restrict__ keys) {
@@ -53,7 +68,7 @@ __device__ __forceinline__ void simt_epilogue(const float (&acc)[8][4], float sc
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
       const int j = j0 + tj * 8 + a;
-      const float v = acc[a][c] * scale;
+      const float v = static_cast<float>(acc[a][c] * scale);
       if (j < J && f < F) {
         if (maps) maps[static_cast<size_t>(f) * J + j] = v;
         best = key_max(best, make_key(v, static_cast<uint32_t>(j)));

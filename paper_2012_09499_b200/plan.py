@@ -116,11 +116,11 @@ class SrpPlan:
         dev = self.device
         if self.harmonic:
             # x = w_1 tau N / 2pi: theta_k / 2pi = k x / N (srp.py:370-372)
-            x = (self.omega[1] * table.T) * self.period / (2.0 * math.pi)
+            x = np.ascontiguousarray((self.omega[1] * table.T) * self.period / (2.0 * math.pi))
             i, f = split_rint(x)
-            self.conv_ti = torch.as_tensor(np.mod(i, self.period).astype(np.int32), device=dev)
+            self.conv_ti = torch.as_tensor(
+                np.ascontiguousarray(np.mod(i, self.period), dtype=np.int32), device=dev)
             self.conv_tf = torch.as_tensor(np.ascontiguousarray(f), device=dev)
-            self._conv_x = x
         else:
             self.omega_dev = torch.as_tensor(self.omega, device=dev)
             self.tau_dev = torch.as_tensor(np.ascontiguousarray(table), device=dev)
@@ -141,11 +141,11 @@ class SrpPlan:
         N.call("srpb_lattice_twiddles", N.ptr(self.omega_dev), self.Kb, T, self.L,
                N.ptr(self.twiddles), s)
         # sinc split x = tau / T (srp.py:310)
-        xs = table.T / T
+        xs = np.ascontiguousarray(table.T) / T
         i, f = split_rint(xs)
         if np.any(np.abs(i) > 2**30):
             raise ValueError("tdoa / sample_period out of int32 range")
-        self.sx_i = torch.as_tensor(i.astype(np.int32), device=dev)
+        self.sx_i = torch.as_tensor(np.ascontiguousarray(i, dtype=np.int32), device=dev)
         self.sx_f = torch.as_tensor(np.ascontiguousarray(f), device=dev)
         need = self.J * t_pad * 4
         if weights not in ("auto", "stored", "onthefly"):
