@@ -197,6 +197,42 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+# ------------------------------------------------------------------ roofline
+FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # SIMT FMA pipe, nominal
+
+
+def roofline_entry(kms, plan, F, J, P, Kb, peaks, path):
+    """Roofline of the dominant kernel of a step, from its CUDA-event time.
+
+    Algorithmic work per unit: K4 2*sum(T_p) flops and K2
+    4*P*Kb flops per frame.candidate; K3 4*sum(T_p)*Kb flops per frame.
+    Tensor-core kernels are rated against the 3xTF32 rate derived from the
+    measured bf16 peak (TF32 = bf16/2; 3 MMAs per fp32-accurate product).
+    """
+    bf16 = peaks.get("bf16_tflops") or 1590.0
+    tc_peak = bf16 / 2.0 / 3.0
+    names = {"approx": ("srpb_interp_tc", "srpb_interp", "srpb_interp_onthefly"),
+             "conventional": ("srpb_conventional_tc", "srpb_conventional",
+                              "srpb_conventional_general")}[path]
+    name = next((n for n in names if n in kms), None)
+    if name is None:
+        return None
+    per_unit = 2.0 * plan.total_samples if path == "approx" else 4.0 * P * Kb
+    achieved = per_unit * F * J / (kms[name] * 1e-3) / 1e12
+    tc = name.endswith("_tc")
+    entry = {
+        "kernel": name, "bound": "tensor" if tc else "fp32", "achieved": achieved,
+        "peak": tc_peak if tc else FP32_NOMINAL_TFLOPS, "unit": "TFLOP/s", "traffic": None,
+        "peak_source": ("measured bf16 burst %.1f TF/s (MEASURED_PEAKS.json) / 2 (TF32 rate) / 3 "
+                        "(3xTF32 passes)" % bf16) if tc else
+                       "nominal FP32 SIMT 148 SM x 128 lanes x 2 x 1.965 GHz (none measured)",
+        "flops_per_unit": per_unit, "units_per_launch": F * J, "kernel_ms": kms[name],
+        "kernels_ms": kms,
+    }
+    entry["frac"] = achieved / entry["peak"]
+    return entry
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import torch
@@ -227,22 +263,34 @@ def run_ours(args):
     def ev():
         return torch.cuda.Event(enable_timing=True)
 
-    def step(path, timers=None):
+    class KernelTimer:
+        """CUDA events around each main kernel launch (plan.kernel_timer hook),
+        recorded on the launching stream."""
+
+        def __init__(self):
+            self.pending, self.pairs = {}, []
+
+        def before(self, name):
+            e = ev()
+            e.record(stream)
+            self.pending[name] = e
+
+        def after(self, name):
+            e = ev()
+            e.record(stream)
+            self.pairs.append((name, self.pending.pop(name), e))
+
+        def totals(self):
+            out = {}
+            for name, a, b in self.pairs:
+                out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+            return out
+
+    def step(path):
         psi, _ = plan.cross_spectra(Y)
         if path == "approx":
-            xi = plan.lattice(psi)
-            if timers:
-                timers[0].record(stream)
-            out = plan.approx(xi)
-            if timers:
-                timers[1].record(stream)
-        else:
-            if timers:
-                timers[0].record(stream)
-            out = plan.conventional(psi)
-            if timers:
-                timers[1].record(stream)
-        return out
+            return plan.approx(plan.lattice(psi))
+        return plan.conventional(psi)
 
     def e2e_step(path):
         Y.copy_(Y_host, non_blocking=True)
@@ -250,29 +298,26 @@ def run_ours(args):
         maps_host.copy_(maps, non_blocking=True)
         am_host.copy_(am, non_blocking=True)
 
-    def timed(fn, path, kernel_timers=False):
+    def timed(fn, path, profile=False):
         for _ in range(args.warmup):
             fn(path)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        tot, ktot = 0.0, 0.0
+        tot = 0.0
+        kt = KernelTimer() if profile else None
+        plan.kernel_timer = kt
         launches0 = _native.launch_count()
         for _ in range(args.steps):
             flush.zero_()
             a, b = ev(), ev()
-            kt = (ev(), ev()) if kernel_timers else None
             a.record(stream)
-            if kernel_timers:
-                fn(path, kt)
-            else:
-                fn(path)
+            fn(path)
             b.record(stream)
             b.synchronize()
             tot += a.elapsed_time(b)
-            if kernel_timers:
-                ktot += kt[0].elapsed_time(kt[1])
         torch.cuda.synchronize()
+        plan.kernel_timer = None
         launches = _native.launch_count() - launches0
         ms = tot / args.steps
         if world > 1:
@@ -280,15 +325,16 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
             dist.barrier()
-        return ms, ktot / args.steps, launches
+        kms = {k: v / args.steps for k, v in kt.totals().items()} if kt else {}
+        return ms, kms, launches
 
     clocks = ClockSampler(local)
     clocks.start()
-    ms_a, k_a, launches_a = timed(step, "approx", kernel_timers=True)
-    ms_c, k_c, launches_c = timed(step, "conventional", kernel_timers=True)
+    ms_a, kms_a, launches_a = timed(step, "approx", profile=True)
+    ms_c, kms_c, launches_c = timed(step, "conventional", profile=True)
     clk = clocks.stop()
-    e2e_a, _, _ = timed(lambda p: e2e_step(p), "approx")
-    e2e_c, _, _ = timed(lambda p: e2e_step(p), "conventional")
+    e2e_a, _, _ = timed(e2e_step, "approx")
+    e2e_c, _, _ = timed(e2e_step, "conventional")
 
     units = F * J * world
     value = units / (ms_a * 1e-3)
@@ -298,22 +344,8 @@ def run_ours(args):
             peaks = json.load(fh)
     except OSError:
         pass
-    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # TFLOP/s nominal FP32 SIMT
-    # dominant kernel of the approx step: K4 interpolation, 2 T_pad flops / (f.c)
-    k4_flops = 2.0 * plan.total_samples * F * J
-    k2_flops = 4.0 * P * Kb * F * J
-    roof_a = {"kernel": "srpb_interp (K4)", "bound": "fp32", "achieved": k4_flops / (k_a * 1e-3) / 1e12,
-              "peak": fp32_peak, "unit": "TFLOP/s", "traffic": None,
-              "peak_source": "nominal FP32 SIMT 148 SM x 128 lanes x 2 x 1.965 GHz (no measured "
-                             "FP32 peak in MEASURED_PEAKS.json)",
-              "flops_per_unit": 2.0 * plan.total_samples, "units_per_launch": F * J,
-              "kernel_ms": k_a}
-    roof_a["frac"] = roof_a["achieved"] / roof_a["peak"]
-    roof_c = {"kernel": "srpb_conventional (K2)", "bound": "fp32",
-              "achieved": k2_flops / (k_c * 1e-3) / 1e12, "peak": fp32_peak, "unit": "TFLOP/s",
-              "traffic": None, "flops_per_unit": 4.0 * P * Kb, "units_per_launch": F * J,
-              "kernel_ms": k_c}
-    roof_c["frac"] = roof_c["achieved"] / roof_c["peak"]
+    roof_a = roofline_entry(kms_a, plan, F, J, P, Kb, peaks, "approx")
+    roof_c = roofline_entry(kms_c, plan, F, J, P, Kb, peaks, "conventional")
     h2d = F * scene.Y.shape[1] * Kb * 8
     d2h = F * J * 4 + F * 4
     out = {
@@ -325,7 +357,7 @@ def run_ours(args):
         "e2e": {"value": units / (e2e_a * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_a,
                 "api": "SrpPlan.run on pinned host Y -> pinned host maps + argmax"},
-        "gpu_launches": launches_a // max(args.steps, 1) * args.steps,
+        "gpu_launches": launches_a,
         "roofline": roof_a,
         "conventional": {"value": units / (ms_c * 1e-3), "unit": UNIT, "ms_per_step": ms_c,
                          "e2e": {"value": units / (e2e_c * 1e-3), "unit": UNIT,

@@ -26,6 +26,7 @@
 #ifndef SRPB_H
 #define SRPB_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -137,6 +138,36 @@ int srpb_interp_onthefly(const int32_t* sx_i, const float* sx_f, int P,
                          const int32_t* off, const int32_t* reach, const float* Xi,
                          int F, int J, int T_pad, float* maps, unsigned long long* keys,
                          void* stream);
+
+/*
+ * Operand split for the 3xTF32 tensor-core kernels: hi = tf32(x),
+ * lo = tf32(x - hi) (round to nearest), elementwise over n floats
+ * (n % 4 == 0, 16-byte aligned pointers).
+ */
+int srpb_tf32_split(const float* x, size_t n, float* hi, float* lo, void* stream);
+
+/*
+ * K2tc conventional maps on the tcgen05 tensor cores (kind::tf32, 3xTF32):
+ * same result as srpb_conventional (srp.py:391-429).  The steering phases
+ * are generated on the fly into shared memory; Psi enters pre-split
+ * (srpb_tf32_split of the float view of Psi [F, P, Kb]).  Requires
+ * Kb % 16 == 0.  kb_per_group = 32-element K blocks accumulated per TMEM
+ * buffer before folding into the fp32 totals (the tensor core's accumulation
+ * is not round-to-nearest; short groups bound its drift, default 4).
+ */
+int srpb_conventional_tc(const float* psi_hi, const float* psi_lo, int F, int P, int Kb,
+                         int period, const int32_t* tau_i, const float* tau_f, int J,
+                         float* maps, unsigned long long* keys, int kb_per_group,
+                         void* stream);
+
+/*
+ * K4tc approximate maps on the tensor cores (srp.py:320-347): TMA-fed
+ * W_hi/W_lo [J, T_pad] and Xi_hi/Xi_lo [F, T_pad] (srpb_tf32_split),
+ * kb_per_group = 32-column K blocks per TMEM buffer.
+ */
+int srpb_interp_tc(const float* w_hi, const float* w_lo, const float* xi_hi, const float* xi_lo,
+                   int F, int J, int T_pad, float* maps, unsigned long long* keys,
+                   int kb_per_group, void* stream);
 
 /*
  * K5 per-frame argmax, lowest index on ties (srp.argmax_candidate,

@@ -35,6 +35,11 @@ _SIGNATURES = {
     "srpb_interp": [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],
     "srpb_interp_onthefly": [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int,
                              c_int, c_int, c_void_p, c_void_p, c_void_p],
+    "srpb_tf32_split": [c_void_p, ctypes.c_size_t, c_void_p, c_void_p, c_void_p],
+    "srpb_conventional_tc": [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
+                             c_int, c_void_p, c_void_p, c_int, c_void_p],
+    "srpb_interp_tc": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p,
+                       c_void_p, c_int, c_void_p],
     "srpb_argmax": [c_void_p, c_int, c_int, c_void_p, c_void_p],
     "srpb_argmax_f64": [c_void_p, c_int, c_int, c_void_p, c_void_p],
     "srpb_argmax_keys_reset": [c_void_p, c_int, c_void_p],

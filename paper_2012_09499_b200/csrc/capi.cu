@@ -25,6 +25,12 @@ cudaError_t launch_interp_onthefly(const int32_t*, const float*, int, const int3
                                    const int32_t*, const float*, int, int, int, float*,
                                    unsigned long long*, cudaStream_t);
 cudaError_t launch_argmax(const float*, int, int, unsigned long long*, cudaStream_t);
+cudaError_t launch_conventional_tc(const float*, const float*, int, int, int, int, const int32_t*,
+                                   const float*, int, float*, unsigned long long*, int,
+                                   cudaStream_t);
+cudaError_t launch_interp_tc(const float*, const float*, const float*, const float*, int, int, int,
+                             float*, unsigned long long*, int, cudaStream_t);
+cudaError_t launch_tf32_split(const float*, size_t, float*, float*, cudaStream_t);
 cudaError_t launch_argmax_f64(const double*, int, int, int32_t*, cudaStream_t);
 cudaError_t launch_keys_reset(unsigned long long*, int, cudaStream_t);
 cudaError_t launch_keys_to_index(const unsigned long long*, int, int32_t*, cudaStream_t);
@@ -146,6 +152,42 @@ int srpb_interp_onthefly(const int32_t* sx_i, const float* sx_f, int P, const in
   return status(srpb::launch_interp_onthefly(sx_i, sx_f, P, off, reach, Xi, F, J, T_pad, maps,
                                              keys, S(stream)),
                 "srpb_interp_onthefly");
+}
+
+int srpb_tf32_split(const float* x, size_t n, float* hi, float* lo, void* stream) {
+  REQUIRE(n % 4 == 0, "srpb_tf32_split: n must be a multiple of 4, got %zu", n);
+  REQUIRE(n == 0 || (x && hi && lo), "srpb_tf32_split: null pointer");
+  REQUIRE((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(hi) |
+           reinterpret_cast<uintptr_t>(lo)) % 16 == 0, "srpb_tf32_split: pointers must be 16-byte aligned");
+  return status(srpb::launch_tf32_split(x, n, hi, lo, S(stream)), "srpb_tf32_split");
+}
+
+int srpb_conventional_tc(const float* psi_hi, const float* psi_lo, int F, int P, int Kb, int period,
+                         const int32_t* tau_i, const float* tau_f, int J, float* maps,
+                         unsigned long long* keys, int kb_per_group, void* stream) {
+  REQUIRE(F >= 0 && P >= 1 && Kb >= 16 && J >= 0, "srpb_conventional_tc: bad shape");
+  REQUIRE(Kb % 16 == 0, "srpb_conventional_tc: Kb must be a multiple of 16, got %d", Kb);
+  REQUIRE(period >= 1 && period <= 46340, "srpb_conventional_tc: period %d out of range", period);
+  REQUIRE(kb_per_group >= 1, "srpb_conventional_tc: kb_per_group must be >= 1");
+  REQUIRE(F == 0 || J == 0 || (psi_hi && psi_lo && tau_i && tau_f),
+          "srpb_conventional_tc: null pointer");
+  REQUIRE(maps || keys, "srpb_conventional_tc: need maps and/or keys output");
+  return status(srpb::launch_conventional_tc(psi_hi, psi_lo, F, P, Kb, period, tau_i, tau_f, J,
+                                             maps, keys, kb_per_group, S(stream)),
+                "srpb_conventional_tc");
+}
+
+int srpb_interp_tc(const float* w_hi, const float* w_lo, const float* xi_hi, const float* xi_lo,
+                   int F, int J, int T_pad, float* maps, unsigned long long* keys,
+                   int kb_per_group, void* stream) {
+  REQUIRE(F >= 0 && J >= 0 && T_pad >= 32, "srpb_interp_tc: bad shape");
+  REQUIRE(T_pad % 32 == 0, "srpb_interp_tc: T_pad must be a multiple of 32, got %d", T_pad);
+  REQUIRE(kb_per_group >= 1, "srpb_interp_tc: kb_per_group must be >= 1");
+  REQUIRE(F == 0 || J == 0 || (w_hi && w_lo && xi_hi && xi_lo), "srpb_interp_tc: null pointer");
+  REQUIRE(maps || keys, "srpb_interp_tc: need maps and/or keys output");
+  return status(srpb::launch_interp_tc(w_hi, w_lo, xi_hi, xi_lo, F, J, T_pad, maps, keys,
+                                       kb_per_group, S(stream)),
+                "srpb_interp_tc");
 }
 
 int srpb_argmax(const float* maps, int F, int J, unsigned long long* keys, void* stream) {

@@ -81,8 +81,14 @@ class SrpPlan:
 
     def __init__(self, tdoa_table, pair_m, pair_mp, tdoa_bounds, bin_frequencies,
                  sample_period=None, n_aux=None, weights="auto", device=None,
-                 max_weight_bytes=DEFAULT_MAX_WEIGHT_BYTES, conventional=True):
+                 max_weight_bytes=DEFAULT_MAX_WEIGHT_BYTES, conventional=True, backend="auto",
+                 kb_per_group=4):
         self.device = N.require_cuda(device)
+        if backend not in ("auto", "simt", "tc"):
+            raise ValueError(f"backend must be auto|simt|tc, got {backend!r}")
+        self.backend = backend
+        self.kb_per_group = int(kb_per_group)
+        self.W_hi = self.W_lo = None
         table = np.asarray(tdoa_table, dtype=np.float64)
         omega = np.asarray(bin_frequencies, dtype=np.float64)
         if table.ndim != 2 or table.shape[0] == 0:
@@ -202,6 +208,41 @@ class SrpPlan:
                N.stream_handle(self.device))
         return psi, floors
 
+    def _use_tc(self, F, kind):
+        """Size heuristic for the tensor-core kernels (not a backend switch:
+        both are this library's sm_100a kernels).  A tcgen05 tile is 128
+        candidates x >= 32 frames; below 32 frames the SIMT kernel wastes
+        less work."""
+        if self.backend == "simt":
+            return False
+        ok = (self.harmonic and self.Kb % 16 == 0) if kind == "conv" else (self.W is not None)
+        if self.backend == "tc":
+            if not ok:
+                raise ValueError(f"tensor-core {kind} path unavailable for this plan")
+            return True
+        return ok and F >= 32
+
+    #: optional profiler hook: an object with before(name) / after(name)
+    #: called around each main kernel launch (bench.py records CUDA events)
+    kernel_timer = None
+
+    def _main(self, name, *args):
+        t = self.kernel_timer
+        if t is not None:
+            t.before(name)
+        N.call(name, *args)
+        if t is not None:
+            t.after(name)
+
+    def split_tf32(self, x):
+        """(hi, lo) tf32 operand split of a float32/complex64 tensor."""
+        xf = torch.view_as_real(x) if x.is_complex() else x
+        hi = torch.empty(xf.shape, dtype=torch.float32, device=self.device)
+        lo = torch.empty_like(hi)
+        N.call("srpb_tf32_split", N.ptr(xf), xf.numel(), N.ptr(hi), N.ptr(lo),
+               N.stream_handle(self.device))
+        return hi, lo
+
     def conventional(self, psi, maps=True, maps_out=None):
         """K2 (+ fused K5): Psi [F, P, Kb] -> (maps [F, J] fp32 | None,
         argmax [F] int32)."""
@@ -215,11 +256,16 @@ class SrpPlan:
                 (F, self.J), dtype=torch.float32, device=self.device)
         keys = self._keys(F)
         s = N.stream_handle(self.device)
-        if self.harmonic:
-            N.call("srpb_conventional", N.ptr(psi), F, self.P, self.Kb, self.period,
+        if self._use_tc(F, "conv"):
+            hi, lo = self.split_tf32(psi)
+            self._main("srpb_conventional_tc", N.ptr(hi), N.ptr(lo), F, self.P, self.Kb, self.period,
+                   N.ptr(self.conv_ti), N.ptr(self.conv_tf), self.J, N.ptr(out), N.ptr(keys),
+                   self.kb_per_group, s)
+        elif self.harmonic:
+            self._main("srpb_conventional", N.ptr(psi), F, self.P, self.Kb, self.period,
                    N.ptr(self.conv_ti), N.ptr(self.conv_tf), self.J, N.ptr(out), N.ptr(keys), s)
         else:
-            N.call("srpb_conventional_general", N.ptr(psi), F, self.P, self.Kb,
+            self._main("srpb_conventional_general", N.ptr(psi), F, self.P, self.Kb,
                    N.ptr(self.omega_dev), N.ptr(self.tau_dev), self.J, N.ptr(out), N.ptr(keys), s)
         return out, self.keys_to_index(keys)
 
@@ -231,7 +277,7 @@ class SrpPlan:
         F = psi.shape[0]
         xi = out if out is not None else torch.empty((F, self.T_pad), dtype=torch.float32,
                                                      device=self.device)
-        N.call("srpb_lattice", N.ptr(psi), F, self.P, self.Kb, N.ptr(self.twiddles), self.L,
+        self._main("srpb_lattice", N.ptr(psi), F, self.P, self.Kb, N.ptr(self.twiddles), self.L,
                N.ptr(self.off), N.ptr(self.reach), self.T_pad, N.ptr(xi),
                N.stream_handle(self.device))
         return xi
@@ -248,11 +294,17 @@ class SrpPlan:
                 (F, self.J), dtype=torch.float32, device=self.device)
         keys = self._keys(F)
         s = N.stream_handle(self.device)
-        if self.W is not None:
-            N.call("srpb_interp", N.ptr(self.W), N.ptr(xi), F, self.J, self.T_pad, N.ptr(out),
+        if self._use_tc(F, "interp"):
+            if self.W_hi is None:
+                self.W_hi, self.W_lo = self.split_tf32(self.W)
+            xh, xl = self.split_tf32(xi)
+            self._main("srpb_interp_tc", N.ptr(self.W_hi), N.ptr(self.W_lo), N.ptr(xh), N.ptr(xl), F,
+                   self.J, self.T_pad, N.ptr(out), N.ptr(keys), self.kb_per_group, s)
+        elif self.W is not None:
+            self._main("srpb_interp", N.ptr(self.W), N.ptr(xi), F, self.J, self.T_pad, N.ptr(out),
                    N.ptr(keys), s)
         else:
-            N.call("srpb_interp_onthefly", N.ptr(self.sx_i), N.ptr(self.sx_f), self.P,
+            self._main("srpb_interp_onthefly", N.ptr(self.sx_i), N.ptr(self.sx_f), self.P,
                    N.ptr(self.off), N.ptr(self.reach), N.ptr(xi), F, self.J, self.T_pad,
                    N.ptr(out), N.ptr(keys), s)
         return out, self.keys_to_index(keys)

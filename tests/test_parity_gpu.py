@@ -21,9 +21,10 @@ pytestmark = pytest.mark.gpu
 T = 1.0 / 16000.0
 
 
-def plan_from_golden(g, n_aux=None, weights="auto"):
+def plan_from_golden(g, n_aux=None, weights="auto", backend="auto"):
     return SrpPlan(g["tdoa"], g["pair_m"], g["pair_mp"], g["bounds"], g["omega"],
-                   sample_period=None if n_aux is None else T, n_aux=n_aux, weights=weights)
+                   sample_period=None if n_aux is None else T, n_aux=n_aux, weights=weights,
+                   backend=backend)
 
 
 def dev(x):
@@ -63,10 +64,13 @@ def test_gcc_phat_edge_cases():
 
 
 # --------------------------------------------------------------------- K2
+@pytest.mark.parametrize("backend", ["simt", "tc"])
 @pytest.mark.parametrize("name", ["c1", "c2_subset", "random_small", "on_lattice"])
-def test_conventional_matches_reference(name):
+def test_conventional_matches_reference(name, backend):
     g = load_golden(name)
-    plan = plan_from_golden(g)
+    if backend == "tc" and g["omega"].size % 16:
+        pytest.skip("tensor-core conventional kernel needs Kb % 16 == 0")
+    plan = plan_from_golden(g, backend=backend)
     maps, am = plan.conventional(dev(g["psi"].astype(np.complex64)))
     assert_maps_match(maps.cpu().numpy(), g["conv"], am.cpu().numpy(), what=name)
     if name in ("c1", "c2_subset"):  # real-source scenes: argmax must be identical
@@ -115,13 +119,14 @@ def test_sinc_table_exact_indicator_rows():
 
 
 # --------------------------------------------------------------------- K4
-@pytest.mark.parametrize("weights", ["stored", "onthefly"])
+@pytest.mark.parametrize("weights", ["stored-simt", "stored-tc", "onthefly"])
 @pytest.mark.parametrize("name", ["c1", "c2_subset", "random_small", "on_lattice"])
 def test_approx_matches_reference(name, weights):
     g = load_golden(name)
     psi = dev(g["psi"].astype(np.complex64))
+    w, backend = (weights.split("-") + ["simt"])[:2]
     for n_aux in g["n_aux"]:
-        plan = plan_from_golden(g, int(n_aux), weights=weights)
+        plan = plan_from_golden(g, int(n_aux), weights=w, backend=backend)
         maps, am = plan.approx(plan.lattice(psi))
         assert_maps_match(maps.cpu().numpy(), g[f"approx_{n_aux}"], am.cpu().numpy(),
                           what=f"{name} n_aux={n_aux} {weights}")
@@ -178,15 +183,20 @@ def _oracle_case(scene, J, F, n_aux, weights="auto"):
     return plan, psi, omega, tdoa, bounds, Y
 
 
+@pytest.mark.parametrize("backend", ["simt", "tc"])
 @pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
-def test_config_shapes_vs_oracle(cfg):
+def test_config_shapes_vs_oracle(cfg, backend):
+    """Full-K contractions (all pairs, all bins) of every config on a
+    candidate/frame subset: accumulation error over C3/C4's long K."""
     if cfg == "c2":
         scene, J, F, n_aux, w = scenes.make_c2(num_frames=6), 3000, 6, 4, "stored"
     elif cfg == "c3":
         scene, J, F, n_aux, w = scenes.make_c3(num_frames=3), 800, 3, 8, "stored"
     else:
-        scene, J, F, n_aux, w = scenes.make_c4(num_frames=2), 300, 2, 2, "onthefly"
+        scene, J, F, n_aux, w = scenes.make_c4(num_frames=2), 300, 2, 2, (
+            "onthefly" if backend == "simt" else "stored")
     plan, psi, omega, tdoa, bounds, Y = _oracle_case(scene, J, F, n_aux, w)
+    plan.backend = backend
     psi_g, _ = plan.cross_spectra(dev(Y))
     assert np.max(np.abs(psi_g.cpu().numpy() - psi)) < 2e-6
     conv_ref = O.conventional_frames(psi, omega, tdoa, candidate_chunk=512)
@@ -212,7 +222,8 @@ def test_full_c2_frame_sharding_and_determinism():
                        for m, mp in pairs])
     tdoa = O.tdoa_table_nearfield(scene.mic_pos, scene.grid, pairs, 343.0)
     omega = O.bin_frequencies(16000.0, 1024)
-    plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=4)
+    # one kernel for every shard (auto would send a < 32-frame shard to SIMT)
+    plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=4, backend="tc")
     Y = dev(scene.Y)
     assert Y.shape == (311, 8, 512) and plan.J == 50000
     for path in ("approx", "conventional"):
