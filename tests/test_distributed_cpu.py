@@ -1,0 +1,89 @@
+"""Multi-process (world_size 2, gloo, CPU) tests of the sharding/gather logic
+used by the multi-GPU path (paper_2012_09499_b200/distributed.py)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2012_09499_b200 import distributed as D
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def orderable(v):
+    b = np.array([v + 0.0], dtype=np.float32).view(np.uint32)[0]
+    return int(~b & 0xFFFFFFFF) if b & 0x80000000 else int(b | 0x80000000)
+
+
+def make_key(v, j):
+    """Python mirror of common.cuh make_key (uint64 bits in an int64)."""
+    u = (orderable(v) << 32) | (0xFFFFFFFF - j)
+    return u - (1 << 64) if u >= (1 << 63) else u
+
+
+def _worker(rank, world, port, F, J, maps_all, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # frame sharding: each rank "computes" its frame block, then gathers
+        lo, hi = D.frame_ranges(F, world)[rank]
+        local = torch.from_numpy(maps_all[lo:hi].copy())
+        full = D.gather_frames(local, F)
+        ok_frames = torch.equal(full, torch.from_numpy(maps_all))
+        am_local = torch.from_numpy(np.argmax(maps_all[lo:hi], axis=1).astype(np.int64))
+        am_full = D.gather_frames(am_local, F)
+        ok_am = torch.equal(am_full, torch.from_numpy(np.argmax(maps_all, axis=1)))
+        # candidate sharding (batch-1): per-rank keys over a candidate slice,
+        # rebased to global indices and MAX-reduced
+        jlo, jhi = D.candidate_ranges(J, world, align=8)[rank]
+        keys = []
+        for f in range(F):
+            row = maps_all[f, jlo:jhi]
+            best = 0
+            for jl, v in enumerate(row):
+                k = make_key(float(v), jl)
+                best = k if (best == 0 or (k ^ D._TOP) > (best ^ D._TOP)) else best
+            keys.append(best)
+        kt = D.rebase_keys(torch.tensor(keys, dtype=torch.int64), jlo)
+        red = D.allreduce_argmax(kt)
+        idx = D.keys_index(red)
+        ok_cand = torch.equal(idx, torch.from_numpy(np.argmax(maps_all, axis=1)))
+        ret[rank] = (ok_frames, ok_am, ok_cand)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("F", [7, 16])
+def test_two_rank_gather_and_candidate_argmax(F):
+    rng = np.random.default_rng(F)
+    J = 37
+    maps_all = rng.standard_normal((F, J)).astype(np.float32)
+    maps_all[0, 5] = maps_all[0, 30] = 9.0   # exact tie across ranks: lowest j wins
+    maps_all[1, :] = 0.0                       # all-equal frame -> index 0
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, F, J, maps_all, ret), nprocs=2, join=True)
+    assert dict(ret) == {0: (True, True, True), 1: (True, True, True)}
+
+
+def test_ranges_cover_and_balance():
+    for F in (1, 2, 5, 311, 4096):
+        for w in (1, 2, 3, 8):
+            r = D.frame_ranges(F, w)
+            assert r[0][0] == 0 and r[-1][1] == F
+            assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+            sizes = [hi - lo for lo, hi in r]
+            assert max(sizes) - min(sizes) <= 1
+    c = D.candidate_ranges(200000, 8)
+    assert c[0][0] == 0 and c[-1][1] == 200000
+    assert all(lo % 128 == 0 for lo, _ in c)
