@@ -4,7 +4,7 @@ DRAM bytes, throughput %, tensor/FMA pipe activity, occupancy, stalls."""
 import csv, subprocess, sys
 
 METRICS = [
-    ("gpu__time_duration.sum", "us", 1e-3),
+    ("gpu__time_duration.sum", "us", 1e-3),  # base unit ns -> us
     ("dram__bytes_read.sum", "rd_MB", 1e-6),
     ("dram__bytes_write.sum", "wr_MB", 1e-6),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram%", 1),
@@ -34,7 +34,9 @@ def main(path):
             try:
                 x = float(v)
                 # normalise to base units before scaling
-                mult = {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+                mult = {"ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9, "nsecond": 1, "usecond": 1e3,
+                        "msecond": 1e6, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
+                        "Gbyte": 1e9}.get(u, 1)
                 x = x * mult * sc
                 cells.append(f"{lab}={x:.4g}")
             except ValueError:
