@@ -17,7 +17,17 @@ build/%.o: $(PKG)/csrc/%.cu $(HDR)
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart
 
-clean:
-	rm -rf build $(LIB)
+# instrumentation build (per-role cycle counters in the tcgen05 kernels)
+PROF_OBJ := $(patsubst $(PKG)/csrc/%.cu,build/prof/%.o,$(SRC))
+build/prof/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p build/prof
+	$(NVCC) $(NVFLAGS) -DSRPB_TC_PROFILE -c $< -o $@ 2> build/prof/$*.ptxas.log || (cat build/prof/$*.ptxas.log; exit 1)
 
-.PHONY: all clean
+prof: $(PKG)/libsrpb_prof.so
+$(PKG)/libsrpb_prof.so: $(PROF_OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(PROF_OBJ) -lcudart
+
+clean:
+	rm -rf build $(LIB) $(PKG)/libsrpb_prof.so
+
+.PHONY: all clean prof

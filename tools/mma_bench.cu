@@ -1,0 +1,131 @@
+// Microbenchmark: tcgen05.mma kind::tf32 issue rate on sm_100a with resident
+// operands, alone and next to the traffic the SRP kernels generate.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/mma_bench tools/mma_bench.cu
+// Modes (compile-time): 0 SS, 1 TS, 2 TS + 8 warps st.shared (~40 B/clk),
+// 3 TS + 8 warps tcgen05.st, 4 SS + 8 warps st.shared.
+#include <cstdio>
+
+#include "../paper_2012_09499_b200/csrc/umma.cuh"
+
+using namespace srpb::umma;
+
+template <int kMode>
+__global__ void __launch_bounds__(384, 1) bench(int N, int iters, int sts_per_round,
+                                                unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar[2];
+  __shared__ uint32_t tbase;
+  __shared__ volatile int done;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (32768 + 2 * 256 * 128 + 65536) / 4; i += blockDim.x)
+    reinterpret_cast<float*>(smem)[i] = 0.0f;
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  if (threadIdx.x == 32) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    done = 0;
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, tbase, 0);
+  constexpr bool ts = kMode == 1 || kMode == 2 || kMode == 3;
+  if (warp == 1) {
+    const uint32_t idesc = idesc_tf32(128, N);
+    const uint64_t da = sw128_kmajor_desc(smem_u32(smem)), db = sw128_kmajor_desc(smem_u32(smem + 32768));
+    const uint32_t a_tm = tmem + 320;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+          for (int r = 0; r < 3; ++r) {
+            if (ts)
+              mma_tf32_ts(tmem, a_tm + ks * 8, db + 2 * ks, idesc, 1u);
+            else
+              mma_tf32(tmem, da + 2 * ks, db + 2 * ks, idesc, 1u);
+          }
+        }
+        mma_commit(&bar[1]);
+      }
+      __syncwarp();
+    }
+    if (elect_one()) mma_commit(&bar[0]);
+    __syncwarp();
+    mbar_wait(&bar[0], 0);
+    long long t1 = clock64();
+    if (threadIdx.x == 32) {
+      done = 1;
+      atomicAdd(out, static_cast<unsigned long long>(t1 - t0));
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * q) << 16);
+    uint32_t r[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = threadIdx.x * 16 + i;
+    float4* sp = reinterpret_cast<float4*>(smem + 32768 + 2 * 256 * 128);
+    float acc = 0.0f;
+    long long t = clock64();
+    while (!done) {
+      if (kMode == 2 || kMode == 4) {
+        // ~ sts_per_round x 16 B per thread every 256 cycles
+        for (int i = 0; i < sts_per_round; ++i)
+          sp[(threadIdx.x * 8 + i) & 4095] = make_float4(acc, acc, acc, acc);
+      } else if (kMode == 3) {
+        tmem_st16(lane_base + 384 + 16 * (warp >> 3), r);
+        tmem_st16(lane_base + 416 + 16 * (warp >> 3), r);
+        tmem_wait_st();
+      } else {
+        break;
+      }
+      t += 256;
+      while (clock64() < t) {
+      }
+      acc += 1.0f;
+    }
+    if (acc == 12345.0f) out[1] = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int kMode>
+void run(const char* name, int sts) {
+  unsigned long long* d;
+  cudaMalloc(&d, 16);
+  const int iters = 2000;
+  const size_t smem = 1024 + 32768 + 2 * 256 * 128 + 65536;
+  cudaFuncSetAttribute(bench<kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int N : {128, 160, 256}) {
+    cudaMemset(d, 0, 16);
+    bench<kMode><<<148, 384, smem>>>(N, iters, sts, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    unsigned long long h = 0;
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    const double per_mma = double(h) / 148.0 / (iters * 12.0);
+    const double ideal = 128.0 * N / 256.0;
+    printf("%-28s N=%3d: %6.1f cycles/MMA (ideal %.0f) -> %3.0f%% ; %s\n", name, N, per_mma, ideal,
+           100.0 * ideal / per_mma, cudaGetErrorString(e));
+  }
+  cudaFree(d);
+}
+
+int main() {
+  run<0>("SS", 0);
+  run<1>("TS", 0);
+  run<2>("TS + sts 20 B/clk", 1);
+  run<2>("TS + sts 40 B/clk", 2);
+  run<2>("TS + sts 80 B/clk", 4);
+  run<3>("TS + tcgen05.st", 0);
+  run<4>("SS + sts 40 B/clk", 2);
+  return 0;
+}
