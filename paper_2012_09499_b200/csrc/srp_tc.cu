@@ -3,8 +3,9 @@
 //   maps[f, j] = scale * sum_kk A[j, kk] B[f, kk]
 //
 // K2 (conventional, srp.py:391-429): A = steering phases [cos, -sin] generated
-//    on the fly by SIMT warps straight into shared memory (never stored in
-//    HBM), B = Psi [F, 2 P Kb] (float view of the cross-spectra), scale 2.
+//    on the fly by SIMT warps straight into tensor memory (never stored in
+//    HBM or smem), B = Psi [F, 2 P Kb] (float view of the cross-spectra),
+//    scale 2.
 // K4 (approximate, srp.py:320-347): A = W [J, T_pad] sinc weights, B = Xi
 //    [F, T_pad] lattice samples, both streamed by TMA, scale 1.
 //
@@ -18,16 +19,26 @@
 // (ping-pong) and the epilogue warps fold it into round-to-nearest fp32
 // register totals while the MMA continues into the other buffer.
 //
-// Persistent: one CTA per SM loops over 128-candidate x N-frame output tiles
-// (N <= 160, multiple of 32; frame tile fastest so concurrently running CTAs
-// share A tiles in L2).  Stage/phase and TMEM-group counters run across
-// tiles, so a tile's final map/argmax write overlaps the next tile's MMAs.
-//   warp 0      TMA producer (B; and A for K4)           elected lane
-//   warp 1      TMEM allocator + MMA issuer              elected lane
+// CTA pairs (cta_group::2, kPair): the per-SM TMA ingress ceiling measured on
+// B200 is ~45-50 B/clk (tools/tma_bench.cu), below what a single-CTA 3xTF32
+// tile needs (K2: 42 B/clk of B; K4: 75 B/clk).  A CTA pair computes a
+// 256-candidate x N-frame tile with one M=256 MMA issued by the leader; each
+// CTA holds its own 128 rows of A and HALF of B's rows, so per-SM B ingress
+// halves.  Both CTAs' TMA loads and A-generators signal the leader's `full`
+// barrier; the leader's commits multicast to both CTAs' `empty`/`acc_full`;
+// both CTAs' epilogues release the leader's `acc_empty`.
+//
+// Persistent: one CTA (pair) per SM (pair) loops over tiles, frame tile
+// fastest so concurrently running CTAs share A tiles in L2.  Stage/phase and
+// TMEM-group counters run across tiles, so a tile's final map/argmax write
+// overlaps the next tile's MMAs.
+//   warp 0      TMA producer                              elected lane
+//   warp 1      TMEM allocator + MMA issuer (leader)      elected lane
 //   warps 4..11 epilogue: TMEM drains, map store, fused argmax; for K2 they
 //               also generate the A tiles (2 threads per candidate row)
-// Smem: 3 stages x {A_hi, A_lo: 128 x 128 B; B_hi, B_lo: N x 128 B}, SW128.
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "umma.cuh"
@@ -37,15 +48,23 @@ namespace srpb {
 using namespace umma;
 
 constexpr int kTcThreads = 384;
-constexpr int kTcStages = 3;
-constexpr int kTcM = 128;
+constexpr int kTcMaxStages = 4;
+constexpr int kTcM = 128;            // candidate rows per CTA
 constexpr int kTcMaxN = 160;
-constexpr int kTcKBlock = 32;  // fp32 elements per K block = one 128-B swizzle row
+constexpr int kTcKBlock = 32;        // fp32 elements per K block = one 128-B swizzle row
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 8;
 constexpr int kABytes = kTcM * 128;  // one of A_hi / A_lo per stage
 
 enum : int { kAFromTma = 0, kAPhase = 1 };
+
+template <int kAMode, bool kPair>
+struct TcCfg {
+  // smem stages: K4 pairs fit 4 x (32 KB A + N/2 rows of B hi/lo); K2 is
+  // bounded by its A stages in TMEM (2N + 64 S <= 512)
+  static constexpr int kStages = (kAMode == kAFromTma && kPair) ? 4 : 3;
+  static constexpr bool kASmem = kAMode == kAFromTma;
+};
 
 // Instrumentation build only (make prof -> libsrpb_prof.so, tools/tc_probe.py):
 // per-role cycle counters; compiled out of libsrpb.so.
@@ -65,7 +84,7 @@ __device__ unsigned long long g_tc_prof[16];
 struct TcParams {
   int F, J, N;        // frames, candidates, frames per tile
   int n_tiles;        // frame tiles
-  int num_tiles;      // n_tiles * candidate tiles
+  int num_items;      // n_tiles * candidate tiles (of 128, or 256 per pair)
   int num_kb;         // K blocks of 32 per tile
   int kb_per_group;   // TMEM drain period (K blocks)
   int groups_per_tile;
@@ -81,28 +100,30 @@ struct TcParams {
 };
 
 struct TcSmem {
-  uint64_t full[kTcStages];
-  uint64_t empty[kTcStages];
+  uint64_t full[kTcMaxStages];
+  uint64_t empty[kTcMaxStages];
   uint64_t acc_full[2];
   uint64_t acc_empty[2];
   unsigned long long tile_keys[4 * kTcMaxN];  // per-quarter, per-frame tile argmax
   uint32_t tmem_base;
 };
 
-// K4 stages hold A and B in smem; K2 stages hold only B (A lives in TMEM).
-__host__ __device__ inline size_t tc_stage_bytes(int N, bool a_in_smem) {
-  return (a_in_smem ? 2 * kABytes : 0) + 2 * size_t(N) * 128;
+// Per-CTA smem stage: A hi/lo (K4) + this CTA's B rows (all N, or N/2 per pair).
+__host__ __device__ inline size_t tc_stage_bytes(int N, bool a_in_smem, bool pair) {
+  return (a_in_smem ? 2 * kABytes : 0) + 2 * size_t(pair ? N / 2 : N) * 128;
 }
-__host__ __device__ inline size_t tc_smem_bytes(int N, bool a_in_smem) {
-  return 1024 /*align slack*/ + kTcStages * tc_stage_bytes(N, a_in_smem) + sizeof(TcSmem);
+__host__ __device__ inline size_t tc_smem_bytes(int N, bool a_in_smem, bool pair, int stages) {
+  return 1024 /*align slack*/ + stages * tc_stage_bytes(N, a_in_smem, pair) + sizeof(TcSmem);
 }
 // TMEM columns: accumulators [0, 2N); K2's A stages (hi 32 + lo 32 columns
-// each) from column 2N: 2N + 64 * kTcStages <= 512 for N <= 160.
+// each) from column 2N: 2N + 64 * 3 <= 512 for N <= 160.
 __host__ __device__ constexpr int tc_a_tmem_col(int N, int s) { return 2 * N + 64 * s; }
 
 // Fold TMEM accumulator buffer of global group `g` into this thread's totals:
-// row = 32*(warp%4) + lane, columns [half*N/2, half*N/2 + N/2).
-__device__ __forceinline__ void tc_drain(const TcParams& p, TcSmem* bar, uint32_t tmem, int g,
+// row = 32*(warp%4) + lane, columns [half*N/2, half*N/2 + N/2); release the
+// buffer on `acc_empty_addr` (the leader's barrier for pairs).
+__device__ __forceinline__ void tc_drain(const TcParams& p, TcSmem* bar, bool remote,
+                                         uint32_t acc_empty_addr0, uint32_t tmem, int g,
                                          int quarter, int half, float (&tot)[kTcMaxN / 2]) {
   const int b = g & 1;
   mbar_wait(&bar->acc_full[b], (g >> 1) & 1);
@@ -128,46 +149,75 @@ __device__ __forceinline__ void tc_drain(const TcParams& p, TcSmem* bar, uint32_
   }
   tc_fence_before();
   __syncwarp();
-  if ((threadIdx.x & 31) == 0) mbar_arrive(&bar->acc_empty[b]);
+  if ((threadIdx.x & 31) == 0) {
+    if (remote)  // pair peer: the leader's barrier
+      mbar_arrive_cluster(acc_empty_addr0 + 8u * b);
+    else
+      mbar_arrive(&bar->acc_empty[b]);
+  }
 }
 
 // Final output of one tile: scale, store maps, fused per-frame argmax
 // (lowest j on ties), then reset the totals for the next tile.  The four
 // lane-quarter warps of a column half combine their warp maxima in shared
-// memory (tile_keys, double-buffered by tile parity) so each tile issues one
-// global 64-bit atomicMax per frame instead of four.
-__device__ __forceinline__ void tc_write_tile(const TcParams& p, TcSmem* bar, int tile_parity,
-                                              int m0, int n0, int quarter, int half, int lane,
+// memory (tile_keys) so each tile issues one global 64-bit atomicMax per
+// frame instead of four.
+__device__ __forceinline__ void tc_write_tile(const TcParams& p, TcSmem* bar, int m0, int n0,
+                                              int quarter, int half, int lane,
                                               float (&tot)[kTcMaxN / 2]) {
+  // everything loop-invariant in registers; no per-column branches, so the
+  // compiler can overlap the columns' reduction chains
+  const int J = p.J;
   const int j = m0 + 32 * quarter + lane;
-  const bool jv = j < p.J;
+  const bool jv = j < J;
   const int cbase = half * (p.N / 2);
+  const int ncols = p.N / 2;
+  const int nv = max(0, min(ncols, p.F - (n0 + cbase)));  // columns with f < F
+  const float scale = p.scale;
+  float* const mcol = p.maps + (static_cast<size_t>(n0 + cbase) * J + j);
+  const bool store = jv && p.maps != nullptr;
   unsigned long long* tk = bar->tile_keys;  // [4 quarters][kTcMaxN columns]
-  (void)tile_parity;
+  TCP_DECL(w_loop);
+  TCP_DECL(w_flush);
+  { TCP_T0();
 #pragma unroll
-  for (int i = 0; i < kTcMaxN / 2; ++i) {
-    if (i < p.N / 2) {
-      const int f = n0 + cbase + i;
-      const float v = tot[i] * p.scale;
-      tot[i] = 0.0f;
-      if (f < p.F) {
-        if (jv && p.maps) p.maps[static_cast<size_t>(f) * p.J + j] = v;
-        if (p.keys) {
-          const uint32_t bits = jv ? orderable_bits(v) : 0u;
-          const uint32_t mx = __reduce_max_sync(0xffffffffu, bits);
-          const uint32_t hit = __ballot_sync(0xffffffffu, jv && bits == mx);
-          if (lane == 0) {  // this quarter's best for column cbase + i (0 = none)
-            const uint32_t jmin = static_cast<uint32_t>(m0 + 32 * quarter + __ffs(hit) - 1);
-            tk[quarter * kTcMaxN + cbase + i] =
-                hit != 0u ? (static_cast<unsigned long long>(mx) << 32) |
-                                static_cast<unsigned long long>(0xFFFFFFFFu - jmin)
-                          : 0ull;
-          }
+  for (int i = 0; i < kTcMaxN / 2; ++i) tot[i] *= scale;
+#pragma unroll
+  for (int i = 0; i < kTcMaxN / 2; ++i)
+    if (store && i < nv) mcol[static_cast<size_t>(i) * J] = tot[i];
+  if (p.keys) {
+    const uint32_t jbase = static_cast<uint32_t>(m0 + 32 * quarter);
+#pragma unroll
+    for (int c0 = 0; c0 < kTcMaxN / 2; c0 += 16) {
+      if (c0 < nv) {
+        uint32_t bits[16], mx[16], hit[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          bits[i] = (jv && c0 + i < nv) ? orderable_bits(tot[c0 + i]) : 0u;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) mx[i] = __reduce_max_sync(0xffffffffu, bits[i]);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          hit[i] = __ballot_sync(0xffffffffu, bits[i] == mx[i] && bits[i] != 0u);
+        if (lane == 0) {  // this quarter's best per column (0 = none)
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < ncols)
+              tk[quarter * kTcMaxN + cbase + c0 + i] =
+                  hit[i] != 0u
+                      ? (static_cast<unsigned long long>(mx[i]) << 32) |
+                            static_cast<unsigned long long>(0xFFFFFFFFu -
+                                                            (jbase + __ffs(hit[i]) - 1))
+                      : 0ull;
         }
       }
     }
   }
+#pragma unroll
+  for (int i = 0; i < kTcMaxN / 2; ++i) tot[i] = 0.0f;
+  TCP_ACC(w_loop); }
   if (p.keys) {
+    TCP_T0();
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
     const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..255
     for (int c = et; c < p.N; c += kEpiWarps * 32) {
@@ -178,50 +228,12 @@ __device__ __forceinline__ void tc_write_tile(const TcParams& p, TcSmem* bar, in
       if (k != 0ull && f < p.F) atomicMax(p.keys + f, k);
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");  // tk reusable
+    TCP_ACC(w_flush);
   }
-}
-
-// A tile of steering phases for K block kb: candidate row j (TMEM lane of
-// this thread), bins [k0 + 8*half, +8) of the block's pair, as (cos, -sin)
-// pairs, split hi/lo.  a_*_tmem carry this warp's lane quarter.
-__device__ __forceinline__ void tc_gen_phase(const TcParams& p, uint32_t a_hi_tmem,
-                                             uint32_t a_lo_tmem, int half, int kb, int j,
-                                             int& cur_pair, int& ti, float& tf, float& sc,
-                                             float& ss) {
-  const int pair = kb / p.kb_per_pair;
-  if (pair != cur_pair) {
-    cur_pair = pair;
-    ti = 0;
-    tf = 0.0f;
-    if (j < p.J) {
-      ti = p.tau_i[static_cast<size_t>(pair) * p.J + j];
-      tf = p.tau_f[static_cast<size_t>(pair) * p.J + j];
-    }
-    sincospif(2.0f * (static_cast<float>(ti) + tf) * p.inv_period, &ss, &sc);  // e^{j 2pi x/N}
+  if (threadIdx.x == kEpiWarp0 * 32) {
+    TCP_FLUSH(12, w_loop);
+    TCP_FLUSH(13, w_flush);
   }
-  const int k = (kb - pair * p.kb_per_pair) * 16 + 8 * half;
-  float c, s;
-  harmonic_phase(k, ti, tf, p.period, p.mask, p.inv_period, &c, &s);
-  float v[16];
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    v[2 * m] = c;
-    v[2 * m + 1] = -s;
-    const float cn = c * sc - s * ss;  // rotate by one bin
-    s = fmaf(c, ss, s * sc);
-    c = cn;
-  }
-  // tf32 split, straight into the TMEM A operand of this stage: this thread's
-  // lane (row r), columns [16*half, +16) of the 32-column K block.
-  uint32_t hi[16], lo[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const float h = to_tf32(v[i]);
-    hi[i] = __float_as_uint(h);
-    lo[i] = __float_as_uint(to_tf32(v[i] - h));
-  }
-  tmem_st16(a_hi_tmem + 16 * half, hi);
-  tmem_st16(a_lo_tmem + 16 * half, lo);
 }
 
 // Exact round-to-nearest (ties away) of a finite fp32 to tf32, in two integer
@@ -294,30 +306,35 @@ struct PhaseGen {
   }
 };
 
-template <int kAMode>
+template <int kAMode, bool kPair>
 __global__ void __launch_bounds__(kTcThreads, 1)
 srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
               const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
               const TcParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  constexpr bool kASmem = kAMode == kAFromTma;
-  const size_t stage_bytes = tc_stage_bytes(p.N, kASmem);
-  TcSmem* bar = reinterpret_cast<TcSmem*>(smem + kTcStages * stage_bytes);
+  using Cfg = TcCfg<kAMode, kPair>;
+  constexpr int S = Cfg::kStages;
+  constexpr bool kASmem = Cfg::kASmem;
+  constexpr int kCta = kPair ? 2 : 1;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-align by pointer arithmetic on the shared array (keeps the shared
+  // address space visible to the compiler: STS/LDS, not generic accesses)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const size_t stage_bytes = tc_stage_bytes(p.N, kASmem, kPair);
+  TcSmem* bar = reinterpret_cast<TcSmem*>(smem + S * stage_bytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t b_bytes = static_cast<uint32_t>(p.N) * 128;
-  // tiles of this CTA: t = blockIdx.x + it * gridDim.x
-  const int my_tiles =
-      p.num_tiles > static_cast<int>(blockIdx.x)
-          ? (p.num_tiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
-          : 0;
-  auto tile_m0 = [&](int it) {
-    return ((static_cast<int>(blockIdx.x) + it * static_cast<int>(gridDim.x)) / p.n_tiles) * kTcM;
-  };
-  auto tile_n0 = [&](int it) {
-    return ((static_cast<int>(blockIdx.x) + it * static_cast<int>(gridDim.x)) % p.n_tiles) * p.N;
-  };
+  const int b_rows = kPair ? p.N / 2 : p.N;  // B rows held by this CTA
+  const uint32_t b_bytes = static_cast<uint32_t>(b_rows) * 128;
+  const int rank = kPair ? static_cast<int>(cluster_ctarank()) : 0;
+  const bool leader = rank == 0;
+
+  // Work items: (frame tile, candidate tile of 128 x kCta rows); CTA (pair) c
+  // takes items c, c + #CTAs(pairs), ...; in a pair, CTA `rank` owns rows
+  // [128 rank, 128 rank + 128) of the 256-row tile.
+  const int cid = static_cast<int>(blockIdx.x) / kCta;
+  const int ncl = static_cast<int>(gridDim.x) / kCta;
+  const int my_tiles = p.num_items > cid ? (p.num_items - 1 - cid) / ncl + 1 : 0;
+  auto tile_m0 = [&](int it) { return (((cid + it * ncl) / p.n_tiles) * kCta + rank) * kTcM; };
+  auto tile_n0 = [&](int it) { return ((cid + it * ncl) % p.n_tiles) * p.N; };
 
   const size_t a_bytes = kASmem ? 2 * kABytes : 0;
   auto a_hi = [&](int s) { return smem + s * stage_bytes; };
@@ -328,58 +345,90 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmB_hi);
     tma_prefetch(&tmB_lo);
-    if (kAMode == kAFromTma) {
+    if (kASmem) {
       tma_prefetch(&tmA_hi);
       tma_prefetch(&tmA_lo);
     }
   }
-  if (warp == 1) tmem_alloc(&bar->tmem_base, 512);
+  if (warp == 1) {
+    if (kPair)
+      tmem_alloc_pair(&bar->tmem_base, 512);
+    else
+      tmem_alloc(&bar->tmem_base, 512);
+  }
   if (warp == 2 && lane == 0) {
-    for (int s = 0; s < kTcStages; ++s) {
-      mbar_init(&bar->full[s], kAMode == kAFromTma ? 1 : 1 + kEpiWarps);
+    // full: producers (x kCta) + K2 A-generator warps (x kCta) arrive on the
+    // leader's barrier; empty / acc_full: one commit from the leader's MMA;
+    // acc_empty: the epilogue warps of both CTAs arrive on the leader's.
+    const int full_count = kCta * (1 + (kAMode == kAPhase ? kEpiWarps : 0));
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&bar->full[s], full_count);
       mbar_init(&bar->empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar->acc_full[b], 1);
-      mbar_init(&bar->acc_empty[b], kEpiWarps);
+      mbar_init(&bar->acc_empty[b], kCta * kEpiWarps);
     }
     for (int c = 0; c < 4 * kTcMaxN; ++c) bar->tile_keys[c] = 0ull;
     fence_mbar_init();
   }
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_sync();  // the leader's barriers exist before peers signal them
   tc_fence_after();
   // make the TMEM base provably warp-uniform (it stays in a uniform register)
   const uint32_t tmem = __shfl_sync(0xffffffffu, bar->tmem_base, 0);
+  // barriers every CTA of the pair signals live in the leader
+  const uint32_t full_addr0 = kPair ? mapa(&bar->full[0], 0) : smem_u32(&bar->full[0]);
+  const uint32_t acc_empty_addr0 =
+      kPair ? mapa(&bar->acc_empty[0], 0) : smem_u32(&bar->acc_empty[0]);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     // warp-wide loop, one elected lane issues (uniform operands, no per-issue
     // register broadcasts)
-    const uint32_t tx = 2 * b_bytes + (kAMode == kAFromTma ? 2 * kABytes : 0);
+    const uint32_t tx = static_cast<uint32_t>(kCta) * (2 * b_bytes + (kASmem ? 2 * kABytes : 0));
     int kg = 0;
     TCP_DECL(w_empty);
     TCP_DECL(t_all);
     { TCP_T0();
     for (int it = 0; it < my_tiles; ++it) {
-      const int m0 = tile_m0(it), n0 = tile_n0(it);
+      const int m0 = tile_m0(it);
+      const int nb = tile_n0(it) + rank * b_rows;  // this CTA's B rows
       for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
-        const int s = kg % kTcStages;
+        const int s = kg % S;
         { TCP_T0();
-        mbar_wait(&bar->empty[s], ((kg / kTcStages) & 1) ^ 1);
+        mbar_wait(&bar->empty[s], ((kg / S) & 1) ^ 1);
         TCP_ACC(w_empty); }
         if (elect_one()) {
-          mbar_expect_tx(&bar->full[s], tx);
-          tma_load_2d(b_hi(s), &tmB_hi, &bar->full[s], kb * kTcKBlock, n0);
-          tma_load_2d(b_lo(s), &tmB_lo, &bar->full[s], kb * kTcKBlock, n0);
-          if (kAMode == kAFromTma) {
-            tma_load_2d(a_hi(s), &tmA_hi, &bar->full[s], kb * kTcKBlock, m0);
-            tma_load_2d(a_lo(s), &tmA_lo, &bar->full[s], kb * kTcKBlock, m0);
+          const uint32_t fb = full_addr0 + 8u * s;
+          if (kPair) {
+            // leader arms the pair's byte count, the peer arrives remotely
+            if (leader)
+              mbar_expect_tx(&bar->full[s], tx);
+            else
+              mbar_arrive_cluster_relaxed(fb);
+            tma_load_2d_pair(b_hi(s), &tmB_hi, fb, kb * kTcKBlock, nb);
+            tma_load_2d_pair(b_lo(s), &tmB_lo, fb, kb * kTcKBlock, nb);
+            if (kASmem) {
+              tma_load_2d_pair(a_hi(s), &tmA_hi, fb, kb * kTcKBlock, m0);
+              tma_load_2d_pair(a_lo(s), &tmA_lo, fb, kb * kTcKBlock, m0);
+            }
+          } else {
+            mbar_expect_tx(&bar->full[s], tx);
+            tma_load_2d(b_hi(s), &tmB_hi, &bar->full[s], kb * kTcKBlock, nb);
+            tma_load_2d(b_lo(s), &tmB_lo, &bar->full[s], kb * kTcKBlock, nb);
+            if (kASmem) {
+              tma_load_2d(a_hi(s), &tmA_hi, &bar->full[s], kb * kTcKBlock, m0);
+              tma_load_2d(a_lo(s), &tmA_lo, &bar->full[s], kb * kTcKBlock, m0);
+            }
           }
         }
         __syncwarp();
       }
     }
+    // tail: every stage's last release has landed before this CTA may exit
+    for (int t = 0; t < S; ++t, ++kg) mbar_wait(&bar->empty[kg % S], ((kg / S) & 1) ^ 1);
     TCP_ACC(t_all); }
     if (lane == 0) {
       TCP_FLUSH(3, w_empty);
@@ -387,74 +436,94 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------- MMA issuer
-    // warp-wide loop; descriptors are base + byte-offset>>4 arithmetic on
-    // uniform values; one elected lane issues the MMAs and their commits.
-    const uint32_t idesc = idesc_tf32(kTcM, p.N);
-    const uint64_t db0 = sw128_kmajor_desc(smem_u32(b_hi(0)));  // stage 0 B_hi
-    const uint64_t da0 = sw128_kmajor_desc(smem_u32(a_hi(0)));  // stage 0 A_hi (K4)
-    const uint32_t stage16 = static_cast<uint32_t>(stage_bytes >> 4);
-    const uint32_t b16 = b_bytes >> 4, a16 = kABytes >> 4;
-    int kg = 0;
-    TCP_DECL(w_full);
-    TCP_DECL(w_acc);
-    TCP_DECL(t_all);
-    { TCP_T0();
-    for (int it = 0; it < my_tiles; ++it) {
-      for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
-        const int s = kg % kTcStages;
-        const int gl = kb / p.kb_per_group;                 // group within the tile
-        const int g = it * p.groups_per_tile + gl;          // global group
-        const int in_group = kb - gl * p.kb_per_group;
-        const uint32_t d = tmem + static_cast<uint32_t>((g & 1) * p.N);
-        if (in_group == 0) {
-          TCP_T0();
-          mbar_wait(&bar->acc_empty[g & 1], ((g >> 1) & 1) ^ 1);
-          TCP_ACC(w_acc);
+    // warp-wide loop (leader CTA only for pairs); descriptors are base +
+    // byte-offset>>4 arithmetic on uniform values; one elected lane issues
+    // the MMAs and their commits.
+    if (leader) {
+      const uint32_t idesc = idesc_tf32(kTcM * kCta, p.N);
+      const uint64_t db0 = sw128_kmajor_desc(smem_u32(b_hi(0)));  // stage 0 B_hi
+      const uint64_t da0 = sw128_kmajor_desc(smem_u32(a_hi(0)));  // stage 0 A_hi (K4)
+      const uint32_t stage16 = static_cast<uint32_t>(stage_bytes >> 4);
+      const uint32_t b16 = b_bytes >> 4, a16 = kABytes >> 4;
+      int kg = 0;
+      TCP_DECL(w_full);
+      TCP_DECL(w_acc);
+      TCP_DECL(t_all);
+      { TCP_T0();
+      for (int it = 0; it < my_tiles; ++it) {
+        for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
+          const int s = kg % S;
+          const int gl = kb / p.kb_per_group;                 // group within the tile
+          const int g = it * p.groups_per_tile + gl;          // global group
+          const int in_group = kb - gl * p.kb_per_group;
+          const uint32_t d = tmem + static_cast<uint32_t>((g & 1) * p.N);
+          if (in_group == 0) {
+            TCP_T0();
+            mbar_wait(&bar->acc_empty[g & 1], ((g >> 1) & 1) ^ 1);
+            TCP_ACC(w_acc);
+            tc_fence_after();
+          }
+          { TCP_T0();
+          mbar_wait(&bar->full[s], (kg / S) & 1);
+          TCP_ACC(w_full); }
           tc_fence_after();
-        }
-        { TCP_T0();
-        mbar_wait(&bar->full[s], (kg / kTcStages) & 1);
-        TCP_ACC(w_full); }
-        tc_fence_after();
-        const uint64_t bh = db0 + static_cast<uint64_t>(s * stage16);
-        const uint64_t bl = bh + b16;
-        if (elect_one()) {
-          if (kASmem) {  // K4: A from smem (SS)
-            const uint64_t ah = da0 + static_cast<uint64_t>(s * stage16);
-            const uint64_t al = ah + a16;
+          const uint64_t bh = db0 + static_cast<uint64_t>(s * stage16);
+          const uint64_t bl = bh + b16;
+          if (elect_one()) {
+            if (kASmem) {  // K4: A from smem (SS)
+              const uint64_t ah = da0 + static_cast<uint64_t>(s * stage16);
+              const uint64_t al = ah + a16;
 #pragma unroll
-            for (int ks = 0; ks < kTcKBlock / 8; ++ks) {
-              const uint32_t o = 2 * ks;  // 32 bytes along K, in 16-byte units
-              const uint32_t acc0 = (in_group > 0 || ks > 0) ? 1u : 0u;
-              mma_tf32(d, al + o, bh + o, idesc, acc0);
-              mma_tf32(d, ah + o, bl + o, idesc, 1u);
-              mma_tf32(d, ah + o, bh + o, idesc, 1u);
+              for (int ks = 0; ks < kTcKBlock / 8; ++ks) {
+                const uint32_t o = 2 * ks;  // 32 bytes along K, in 16-byte units
+                const uint32_t acc0 = (in_group > 0 || ks > 0) ? 1u : 0u;
+                if (kPair) {
+                  mma_tf32_pair(d, al + o, bh + o, idesc, acc0);
+                  mma_tf32_pair(d, ah + o, bl + o, idesc, 1u);
+                  mma_tf32_pair(d, ah + o, bh + o, idesc, 1u);
+                } else {
+                  mma_tf32(d, al + o, bh + o, idesc, acc0);
+                  mma_tf32(d, ah + o, bl + o, idesc, 1u);
+                  mma_tf32(d, ah + o, bh + o, idesc, 1u);
+                }
+              }
+            } else {  // K2: A from TMEM (TS), written there by the generator warps
+              const uint32_t ah = tmem + static_cast<uint32_t>(tc_a_tmem_col(p.N, s));
+              const uint32_t al = ah + 32;
+#pragma unroll
+              for (int ks = 0; ks < kTcKBlock / 8; ++ks) {
+                const uint32_t o = 2 * ks;
+                const uint32_t acc0 = (in_group > 0 || ks > 0) ? 1u : 0u;
+                if (kPair) {
+                  mma_tf32_ts_pair(d, al + 8 * ks, bh + o, idesc, acc0);
+                  mma_tf32_ts_pair(d, ah + 8 * ks, bl + o, idesc, 1u);
+                  mma_tf32_ts_pair(d, ah + 8 * ks, bh + o, idesc, 1u);
+                } else {
+                  mma_tf32_ts(d, al + 8 * ks, bh + o, idesc, acc0);
+                  mma_tf32_ts(d, ah + 8 * ks, bl + o, idesc, 1u);
+                  mma_tf32_ts(d, ah + 8 * ks, bh + o, idesc, 1u);
+                }
+              }
             }
-          } else {  // K2: A from TMEM (TS), written there by the generator warps
-            const uint32_t ah = tmem + static_cast<uint32_t>(tc_a_tmem_col(p.N, s));
-            const uint32_t al = ah + 32;
-#pragma unroll
-            for (int ks = 0; ks < kTcKBlock / 8; ++ks) {
-              const uint32_t o = 2 * ks;
-              const uint32_t acc0 = (in_group > 0 || ks > 0) ? 1u : 0u;
-              mma_tf32_ts(d, al + 8 * ks, bh + o, idesc, acc0);
-              mma_tf32_ts(d, ah + 8 * ks, bl + o, idesc, 1u);
-              mma_tf32_ts(d, ah + 8 * ks, bh + o, idesc, 1u);
+            const bool last_in_group = in_group == p.kb_per_group - 1 || kb == p.num_kb - 1;
+            if (kPair) {
+              mma_commit_pair_mc(&bar->empty[s], 0x3);
+              if (last_in_group) mma_commit_pair_mc(&bar->acc_full[g & 1], 0x3);
+            } else {
+              mma_commit(&bar->empty[s]);
+              if (last_in_group) mma_commit(&bar->acc_full[g & 1]);
             }
           }
-          mma_commit(&bar->empty[s]);
-          if (in_group == p.kb_per_group - 1 || kb == p.num_kb - 1)
-            mma_commit(&bar->acc_full[g & 1]);
+          __syncwarp();
         }
-        __syncwarp();
       }
-    }
-    TCP_ACC(t_all); }
-    if (lane == 0) {
-      TCP_FLUSH(0, t_all);
-      TCP_FLUSH(1, w_full);
-      TCP_FLUSH(2, w_acc);
-      TCP_FLUSH(11, 1);
+      TCP_ACC(t_all); }
+      if (lane == 0) {
+        TCP_FLUSH(0, t_all);
+        TCP_FLUSH(1, w_full);
+        TCP_FLUSH(2, w_acc);
+        TCP_FLUSH(11, 1);
+      }
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     // ------------------------------------- epilogue (+ A generation for K2)
@@ -477,11 +546,11 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     TCP_DECL(c_all);
     auto fold_next = [&]() {
       { TCP_T0();
-      tc_drain(p, bar, tmem, drained, quarter, half, tot);
+      tc_drain(p, bar, !leader, acc_empty_addr0, tmem, drained, quarter, half, tot);
       TCP_ACC(c_drain); }
       if (d_gl == p.groups_per_tile - 1) {
         TCP_T0();
-        tc_write_tile(p, bar, d_it & 1, tile_m0(d_it), tile_n0(d_it), quarter, half, lane, tot);
+        tc_write_tile(p, bar, tile_m0(d_it), tile_n0(d_it), quarter, half, lane, tot);
         TCP_ACC(c_write);
         ++d_it;
         d_gl = 0;
@@ -515,13 +584,18 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
           tc_fence_before();
           __syncwarp();
           TCP_ACC(c_gen); }
-          if (lane == 0) mbar_arrive(&bar->full[s]);
-          if (++s == kTcStages) {
+          if (lane == 0) {
+            if (leader)
+              mbar_arrive(&bar->full[s]);
+            else  // pair peer: its TMEM A tile is complete (wait::st + fence above)
+              mbar_arrive_cluster_relaxed(full_addr0 + 8u * s);
+          }
+          if (++s == S) {
             s = 0;
             ph ^= 1;
           }
-          // fold groups whose last K block is at least kTcStages behind
-          while (drained < total_groups && d_last_kg <= kg - kTcStages) fold_next();
+          // fold groups whose last K block is at least S behind
+          while (drained < total_groups && d_last_kg <= kg - S) fold_next();
         }
       }
     }
@@ -537,9 +611,13 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   }
   tc_fence_before();
   __syncthreads();
+  if (kPair) cluster_sync();  // the pair leaves together (remote arrivals landed)
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    if (kPair)
+      tmem_dealloc_pair(tmem, 512);
+    else
+      tmem_dealloc(tmem, 512);
   }
 }
 
@@ -581,11 +659,28 @@ int pick_n(int F) {
   return (per + 31) / 32 * 32;
 }
 
-void finish_params(TcParams& p, int kb_per_group) {
+// CTA pairs by default when there are >= 2 candidate tiles; SRPB_TC_PAIR=0
+// forces single-CTA tiles (tuning / A-B comparison).
+// Measured on B200 (C2): K4 108.5 us paired vs 116 us single; K2 4.36 ms
+// paired vs 3.60 ms single (its 3-stage TMEM A ring cannot absorb the
+// cross-SM signalling latency), so pairs are the default for K4 only.
+bool use_pair(int m_tiles, bool default_on) {
+  static int env = -2;
+  if (env == -2) {
+    const char* s = getenv("SRPB_TC_PAIR");
+    env = s ? atoi(s) : -1;
+  }
+  if (m_tiles < 2 || env == 0) return false;
+  return env == 1 || default_on;
+}
+
+void finish_params(TcParams& p, int kb_per_group, bool pair) {
   p.N = pick_n(p.F);
   p.n_tiles = (p.F + p.N - 1) / p.N;
-  p.num_tiles = p.n_tiles * ((p.J + kTcM - 1) / kTcM);
-  p.kb_per_group = max(kTcStages + 1, kb_per_group);
+  const int m_tiles = (p.J + kTcM - 1) / kTcM;
+  const int cta = pair ? 2 : 1;
+  p.num_items = p.n_tiles * ((m_tiles + cta - 1) / cta);
+  p.kb_per_group = max(4, kb_per_group);
   p.groups_per_tile = (p.num_kb + p.kb_per_group - 1) / p.kb_per_group;
 }
 
@@ -600,16 +695,31 @@ int num_sms() {
   return n;
 }
 
-template <int kAMode>
+template <int kAMode, bool kPair>
 cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                       const CUtensorMap& bl, const TcParams& p, cudaStream_t stream) {
-  const size_t smem = tc_smem_bytes(p.N, kAMode == kAFromTma);
-  cudaError_t e = cudaFuncSetAttribute(srp_tc_kernel<kAMode>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+  using Cfg = TcCfg<kAMode, kPair>;
+  const size_t smem = tc_smem_bytes(p.N, Cfg::kASmem, kPair, Cfg::kStages);
+  auto kern = srp_tc_kernel<kAMode, kPair>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  const int grid = min(p.num_tiles, num_sms());
-  srp_tc_kernel<kAMode><<<grid, kTcThreads, smem, stream>>>(ah, al, bh, bl, p);
+  constexpr int cta = kPair ? 2 : 1;
+  const int units = min(p.num_items, num_sms() / cta);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * cta);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cta;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -625,7 +735,8 @@ cudaError_t launch_conventional_tc(const float* psi_hi, const float* psi_lo, int
   p.J = J;
   p.kb_per_pair = Kb / 16;
   p.num_kb = P * p.kb_per_pair;
-  finish_params(p, kb_per_group);
+  const bool pair = use_pair((J + kTcM - 1) / kTcM, false);
+  finish_params(p, kb_per_group, pair);
   p.scale = 2.0f;
   p.maps = maps;
   p.keys = keys;
@@ -636,10 +747,12 @@ cudaError_t launch_conventional_tc(const float* psi_hi, const float* psi_lo, int
   p.inv_period = 1.0f / static_cast<float>(period);
   CUtensorMap bh, bl;
   const int cols = 2 * P * Kb;
-  cudaError_t e = make_map(&bh, psi_hi, F, cols, p.N);
-  if (e == cudaSuccess) e = make_map(&bl, psi_lo, F, cols, p.N);
+  const int brows = pair ? p.N / 2 : p.N;  // B rows per CTA
+  cudaError_t e = make_map(&bh, psi_hi, F, cols, brows);
+  if (e == cudaSuccess) e = make_map(&bl, psi_lo, F, cols, brows);
   if (e != cudaSuccess) return e;
-  return launch_tc<kAPhase>(bh, bl, bh, bl, p, stream);
+  return pair ? launch_tc<kAPhase, true>(bh, bl, bh, bl, p, stream)
+              : launch_tc<kAPhase, false>(bh, bl, bh, bl, p, stream);
 }
 
 cudaError_t launch_interp_tc(const float* w_hi, const float* w_lo, const float* xi_hi,
@@ -650,17 +763,20 @@ cudaError_t launch_interp_tc(const float* w_hi, const float* w_lo, const float* 
   p.F = F;
   p.J = J;
   p.num_kb = T_pad / kTcKBlock;
-  finish_params(p, kb_per_group);
+  const bool pair = use_pair((J + kTcM - 1) / kTcM, true);
+  finish_params(p, kb_per_group, pair);
   p.scale = 1.0f;
   p.maps = maps;
   p.keys = keys;
   CUtensorMap ah, al, bh, bl;
+  const int brows = pair ? p.N / 2 : p.N;
   cudaError_t e = make_map(&ah, w_hi, J, T_pad, kTcM);
   if (e == cudaSuccess) e = make_map(&al, w_lo, J, T_pad, kTcM);
-  if (e == cudaSuccess) e = make_map(&bh, xi_hi, F, T_pad, p.N);
-  if (e == cudaSuccess) e = make_map(&bl, xi_lo, F, T_pad, p.N);
+  if (e == cudaSuccess) e = make_map(&bh, xi_hi, F, T_pad, brows);
+  if (e == cudaSuccess) e = make_map(&bl, xi_lo, F, T_pad, brows);
   if (e != cudaSuccess) return e;
-  return launch_tc<kAFromTma>(ah, al, bh, bl, p, stream);
+  return pair ? launch_tc<kAFromTma, true>(ah, al, bh, bl, p, stream)
+              : launch_tc<kAFromTma, false>(ah, al, bh, bl, p, stream);
 }
 
 // hi = tf32(x), lo = tf32(x - hi): operand split for 3xTF32

@@ -82,12 +82,17 @@ class SrpPlan:
     def __init__(self, tdoa_table, pair_m, pair_mp, tdoa_bounds, bin_frequencies,
                  sample_period=None, n_aux=None, weights="auto", device=None,
                  max_weight_bytes=DEFAULT_MAX_WEIGHT_BYTES, conventional=True, backend="auto",
-                 kb_per_group=4):
+                 kb_per_group=4, interp_kb_per_group=10):
         self.device = N.require_cuda(device)
         if backend not in ("auto", "simt", "tc"):
             raise ValueError(f"backend must be auto|simt|tc, got {backend!r}")
         self.backend = backend
+        # TMEM drain periods (32-column K blocks per accumulator group): the
+        # tensor core's accumulation drifts toward zero over long chains, so
+        # K2's long K (2 P Kb) folds every 4 blocks (48 MMA steps, ~6e-7);
+        # K4's short K (C2: 19 blocks) folds every 10 (120 steps, ~1.5e-6).
         self.kb_per_group = int(kb_per_group)
+        self.interp_kb_per_group = int(interp_kb_per_group)
         self.W_hi = self.W_lo = None
         table = np.asarray(tdoa_table, dtype=np.float64)
         omega = np.asarray(bin_frequencies, dtype=np.float64)
@@ -299,7 +304,7 @@ class SrpPlan:
                 self.W_hi, self.W_lo = self.split_tf32(self.W)
             xh, xl = self.split_tf32(xi)
             self._main("srpb_interp_tc", N.ptr(self.W_hi), N.ptr(self.W_lo), N.ptr(xh), N.ptr(xl), F,
-                   self.J, self.T_pad, N.ptr(out), N.ptr(keys), self.kb_per_group, s)
+                   self.J, self.T_pad, N.ptr(out), N.ptr(keys), self.interp_kb_per_group, s)
         elif self.W is not None:
             self._main("srpb_interp", N.ptr(self.W), N.ptr(xi), F, self.J, self.T_pad, N.ptr(out),
                    N.ptr(keys), s)

@@ -1,0 +1,28 @@
+#!/usr/bin/env python
+"""Time K2/K4 (CUDA events) for cluster sizes 1/2/4 (SRPB_TC_CLUSTER) in
+separate processes: python tools/cluster_sweep.py"""
+import os, subprocess, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CODE = r'''
+import sys, torch
+sys.path.insert(0, %r)
+import bench
+from paper_2012_09499_b200.plan import SrpPlan
+scene, pm, pmp, bounds, tdoa, omega = bench.workload(0)
+Y = torch.from_numpy(scene.Y).cuda()
+plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=bench.T, n_aux=4, weights="stored")
+psi, _ = plan.cross_spectra(Y); xi = plan.lattice(psi)
+for name, fn in (("approx", lambda: plan.approx(xi)), ("conv", lambda: plan.conventional(psi))):
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+    a.record()
+    n = 10 if name == "approx" else 3
+    for _ in range(n): fn()
+    b.record(); b.synchronize()
+    print(f"  {name}: {a.elapsed_time(b)/n*1e3:.1f} us")
+''' % ROOT
+for cm in ("1", "2", "4"):
+    env = dict(os.environ, SRPB_TC_CLUSTER=cm)
+    print("cluster", cm, flush=True)
+    subprocess.run([sys.executable, "-c", CODE], env=env, check=False)

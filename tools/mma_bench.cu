@@ -18,8 +18,14 @@ __global__ void __launch_bounds__(384, 1) bench(int N, int iters, int sts_per_ro
   __shared__ uint32_t tbase;
   __shared__ volatile int done;
   const int warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < (32768 + 2 * 256 * 128 + 65536) / 4; i += blockDim.x)
-    reinterpret_cast<float*>(smem)[i] = 0.0f;
+  for (int i = threadIdx.x; i < (32768 + 2 * 256 * 128 + 65536) / 4; i += blockDim.x) {
+    // random-looking operands (kMode >= 6) vs zeros: the tensor core's power
+    // and hence its sustained rate depend on the data
+    uint32_t h = (i + 1) * 2654435761u;
+    h ^= h >> 13;
+    reinterpret_cast<float*>(smem)[i] =
+        kMode >= 6 ? __uint_as_float((h & 0x807FFFFFu) | 0x3F000000u) : 0.0f;
+  }
   if (warp == 0) tmem_alloc(&tbase, 512);
   if (threadIdx.x == 32) {
     mbar_init(&bar[0], 1);
@@ -32,13 +38,33 @@ __global__ void __launch_bounds__(384, 1) bench(int N, int iters, int sts_per_ro
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, tbase, 0);
-  constexpr bool ts = kMode == 1 || kMode == 2 || kMode == 3;
+  constexpr bool ts = kMode == 1 || kMode == 2 || kMode == 3 || kMode == 5 || kMode == 7;
+  if (kMode == 7 && warp >= 4 && warp < 8) {  // random A operand in TMEM
+    uint32_t r[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      uint32_t h = (threadIdx.x * 16 + i + 7) * 2246822519u;
+      h ^= h >> 15;
+      r[i] = (h & 0x807FFFFFu) | 0x3F000000u;
+    }
+    const uint32_t lb = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
+    tmem_st16(lb + 320, r);
+    tmem_st16(lb + 336, r);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
   if (warp == 1) {
     const uint32_t idesc = idesc_tf32(128, N);
     const uint64_t da = sw128_kmajor_desc(smem_u32(smem)), db = sw128_kmajor_desc(smem_u32(smem + 32768));
     const uint32_t a_tm = tmem + 320;
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
+      if (kMode == 5) {  // the real issuer's per-block wait (already complete) + fence
+        mbar_wait(&bar[0], 1);
+        tc_fence_after();
+      }
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
@@ -127,5 +153,8 @@ int main() {
   run<2>("TS + sts 80 B/clk", 4);
   run<3>("TS + tcgen05.st", 0);
   run<4>("SS + sts 40 B/clk", 2);
+  run<5>("TS + wait/fence per block", 0);
+  run<6>("SS random operands", 0);
+  run<7>("TS random operands", 0);
   return 0;
 }

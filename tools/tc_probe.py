@@ -28,7 +28,7 @@ from paper_2012_09499_b200.plan import SrpPlan  # noqa: E402
 
 NAMES = {0: "mma_total", 1: "mma_wait_full", 2: "mma_wait_acc_empty", 3: "tma_wait_empty",
          4: "tma_total", 5: "epi_gen_wait_empty", 6: "epi_gen", 7: "epi_drain", 9: "epi_write",
-         10: "epi_total", 11: "ctas"}
+         10: "epi_total", 11: "ctas", 12: "write_loop", 13: "write_flush"}
 
 
 def read():
@@ -48,16 +48,18 @@ def report(tag, c):
 
 def main():
     scene, pm, pmp, bounds, tdoa, omega = bench.workload(0)
+    kbg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
     plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=bench.T, n_aux=bench.N_AUX,
-                   weights="stored")
+                   weights="stored", kb_per_group=kbg)
     Y = torch.from_numpy(scene.Y).cuda()
-    for path in ("approx", "conventional"):
+    paths = sys.argv[2].split(",") if len(sys.argv) > 2 else ["approx", "conventional"]
+    for path in paths:
         plan.run(Y, path)  # warm
         torch.cuda.synchronize()
         read()
         plan.run(Y, path)
         torch.cuda.synchronize()
-        report(path, read())
+        report(f"{path} kb_per_group={kbg}", read())
 
 
 if __name__ == "__main__":
