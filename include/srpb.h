@@ -62,6 +62,15 @@ int srpb_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
                   double abs_floor, float* Psi, double* floor_out, void* stream);
 
 /*
+ * K1a: the per-frame PHAT floor alone, floor_rel * sqrt(mean_{p,k} |raw|^2)
+ * accumulated in fp64 (spectral.py:268-275); feeds
+ * srpb_lattice_from_spectra.  floor_out [F] float64.
+ */
+int srpb_gcc_floor(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                   const int32_t* pair_mp, int P, double floor_rel, double* floor_out,
+                   void* stream);
+
+/*
  * K2 conventional SRP maps (harmonic bins w_k = k w_1).
  * Replaces srp.srp_conventional_frames (srp.py:391-429) incl. the steering
  * phases of srp._phase_matrix (srp.py:350-373), generated on the fly:
@@ -108,6 +117,23 @@ int srpb_lattice_twiddles(const double* omega, int Kb, double sample_period, int
 int srpb_lattice(const float* Psi, int F, int P, int Kb, const float* tw, int L,
                  const int32_t* off, const int32_t* reach, int T_pad, float* Xi,
                  void* stream);
+
+/*
+ * K1b+K3 fused: lattice GCC samples straight from the channel spectra.
+ * Same output as srpb_gcc_phat followed by srpb_lattice, but the GCC-PHAT
+ * cross-spectra are formed in the lattice kernel's staging pass and never
+ * stored (spectral.cross_spectrum spectral.py:218-285 feeding
+ * srp.build_gcc_lattice srp.py:201-247).
+ *   floors [F] float64 (srpb_gcc_floor) for PHAT with the relative floor, or
+ *   NULL with abs_floor > 0 (explicit floor); ignored for identity weighting.
+ *   Xi [F, T_pad] float32 out and/or Xi_hi, Xi_lo [F, T_pad]: its tf32
+ *   operand split (hi = rna(Xi), lo = rna(Xi - hi)) for srpb_interp_tc.
+ */
+int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                              const int32_t* pair_mp, int P, int weighting, const double* floors,
+                              double abs_floor, const float* tw, int L, const int32_t* off,
+                              const int32_t* reach, int T_pad, float* Xi, float* Xi_hi,
+                              float* Xi_lo, void* stream);
 
 /*
  * Sinc interpolation table W[j, off[p] + n + reach[p]] = sinc(x[j,p] - n),

@@ -30,6 +30,11 @@ _SIGNATURES = {
     "srpb_lattice_twiddles": [c_void_p, c_int, c_double, c_int, c_void_p, c_void_p],
     "srpb_lattice": [c_void_p, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_void_p, c_int,
                      c_void_p, c_void_p],
+    "srpb_gcc_floor": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_double,
+                       c_void_p, c_void_p],
+    "srpb_lattice_from_spectra": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
+                                  c_void_p, c_double, c_void_p, c_int, c_void_p, c_void_p, c_int,
+                                  c_void_p, c_void_p, c_void_p, c_void_p],
     "srpb_sinc_table": [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p,
                         c_void_p],
     "srpb_interp": [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],
@@ -96,6 +101,8 @@ def stream_handle(device=None):
 
 
 _LAUNCHING = {n for n in _SIGNATURES if n not in ("srpb_abi_version", "srpb_last_error")}
+# entry points that launch more than one kernel (floor/fill pass + psi pass)
+_KERNELS_PER_CALL = {"srpb_gcc_phat": 2}
 _launches = 0
 
 
@@ -114,7 +121,7 @@ def call(name, *args):
     lib = load()
     rc = getattr(lib, name)(*args)
     if name in _LAUNCHING:
-        _launches += 1
+        _launches += _KERNELS_PER_CALL.get(name, 1)
     if rc != 0:
         msg = lib.srpb_last_error().decode(errors="replace")
         if rc < 0:

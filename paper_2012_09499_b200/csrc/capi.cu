@@ -9,6 +9,12 @@
 namespace srpb {
 cudaError_t launch_gcc_phat(const float*, int, int, int, const int32_t*, const int32_t*, int, int,
                             double, double, float*, double*, cudaStream_t);
+cudaError_t launch_gcc_floor(const float*, int, int, int, const int32_t*, const int32_t*, int,
+                             double, double*, cudaStream_t);
+cudaError_t launch_lattice_from_spectra(const float*, int, int, int, const int32_t*,
+                                        const int32_t*, int, int, const double*, double,
+                                        const float*, int, const int32_t*, const int32_t*, int,
+                                        int, float*, float*, float*, cudaStream_t);
 cudaError_t launch_conventional(const float*, int, int, int, int, const int32_t*, const float*,
                                 int, float*, unsigned long long*, cudaStream_t);
 cudaError_t launch_conventional_general(const float*, int, int, int, const double*,
@@ -84,6 +90,18 @@ int srpb_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
                 "srpb_gcc_phat");
 }
 
+int srpb_gcc_floor(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                   const int32_t* pair_mp, int P, double floor_rel, double* floor_out,
+                   void* stream) {
+  REQUIRE(F >= 0 && M >= 1 && Kb >= 1 && P >= 1, "srpb_gcc_floor: bad shape F=%d M=%d Kb=%d P=%d",
+          F, M, Kb, P);
+  REQUIRE(M <= 64, "srpb_gcc_floor: at most 64 channels supported, got %d", M);
+  REQUIRE(F == 0 || (Y && pair_m && pair_mp && floor_out), "srpb_gcc_floor: null pointer");
+  return status(srpb::launch_gcc_floor(Y, F, M, Kb, pair_m, pair_mp, P, floor_rel, floor_out,
+                                       S(stream)),
+                "srpb_gcc_floor");
+}
+
 int srpb_conventional(const float* Psi, int F, int P, int Kb, int period, const int32_t* tau_i,
                       const float* tau_f, int J, float* maps, unsigned long long* keys,
                       void* stream) {
@@ -122,6 +140,28 @@ int srpb_lattice(const float* Psi, int F, int P, int Kb, const float* tw, int L,
   return status(srpb::launch_lattice(Psi, F, P, Kb, tw, L, off, reach, 2 * L + 1, T_pad, Xi,
                                      S(stream)),
                 "srpb_lattice");
+}
+
+int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                              const int32_t* pair_mp, int P, int weighting, const double* floors,
+                              double abs_floor, const float* tw, int L, const int32_t* off,
+                              const int32_t* reach, int T_pad, float* Xi, float* Xi_hi,
+                              float* Xi_lo, void* stream) {
+  REQUIRE(F >= 0 && M >= 1 && P >= 1 && Kb >= 1 && L >= 0 && T_pad >= 1,
+          "srpb_lattice_from_spectra: bad shape");
+  REQUIRE(weighting == SRPB_WEIGHT_PHAT || weighting == SRPB_WEIGHT_IDENTITY,
+          "srpb_lattice_from_spectra: unknown weighting %d", weighting);
+  REQUIRE(weighting != SRPB_WEIGHT_PHAT || floors || abs_floor > 0.0,
+          "srpb_lattice_from_spectra: PHAT needs per-frame floors or abs_floor > 0");
+  REQUIRE((Xi_hi == nullptr) == (Xi_lo == nullptr),
+          "srpb_lattice_from_spectra: Xi_hi and Xi_lo go together");
+  REQUIRE(Xi || Xi_hi, "srpb_lattice_from_spectra: need Xi and/or Xi_hi/Xi_lo output");
+  REQUIRE(F == 0 || (Y && pair_m && pair_mp && tw && off && reach),
+          "srpb_lattice_from_spectra: null pointer");
+  return status(srpb::launch_lattice_from_spectra(Y, F, M, Kb, pair_m, pair_mp, P, weighting,
+                                                  floors, abs_floor, tw, L, off, reach, 2 * L + 1,
+                                                  T_pad, Xi, Xi_hi, Xi_lo, S(stream)),
+                "srpb_lattice_from_spectra");
 }
 
 int srpb_sinc_table(const int32_t* sx_i, const float* sx_f, int J, int P, const int32_t* off,

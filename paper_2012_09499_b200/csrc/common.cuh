@@ -56,4 +56,27 @@ __device__ __forceinline__ void harmonic_phase(int k, int ti, float tf, int peri
   sincospif(2.0f * harmonic_turns(k, ti, tf, period, mask, inv_period), s, c);
 }
 
+// GCC-PHAT weighting of one bin (spectral.py:258-277): raw = a conj(b),
+// psi = raw / max(|raw|, floor), exact 0 where raw == 0; identity: raw.
+__device__ __forceinline__ float2 phat_one(float2 a, float2 b, int weighting, double floor) {
+  if (weighting != 0) {  // identity: raw product, correctly rounded from fp64
+    const double re = static_cast<double>(a.x) * b.x + static_cast<double>(a.y) * b.y;
+    const double im = static_cast<double>(a.y) * b.x - static_cast<double>(a.x) * b.y;
+    return make_float2(static_cast<float>(re), static_cast<float>(im));
+  }
+  if ((a.x == 0.0f && a.y == 0.0f) || (b.x == 0.0f && b.y == 0.0f))
+    return make_float2(0.0f, 0.0f);  // exact-zero product stays zero
+  const float ma = hypotf(a.x, a.y), mb = hypotf(b.x, b.y);
+  const double mag = static_cast<double>(ma) * mb;
+  if (mag >= floor) {
+    // raw/|raw| = (a/|a|) conj(b/|b|): unit modulus, no over/underflow
+    const float ua = 1.0f / ma, ub = 1.0f / mb;
+    const float ax = a.x * ua, ay = a.y * ua, bx = b.x * ub, by = b.y * ub;
+    return make_float2(ax * bx + ay * by, ay * bx - ax * by);
+  }
+  const double re = static_cast<double>(a.x) * b.x + static_cast<double>(a.y) * b.y;
+  const double im = static_cast<double>(a.y) * b.x - static_cast<double>(a.x) * b.y;
+  return make_float2(static_cast<float>(re / floor), static_cast<float>(im / floor));
+}
+
 }  // namespace srpb

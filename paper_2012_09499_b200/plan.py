@@ -188,9 +188,8 @@ class SrpPlan:
                              f"{t.dtype} {tuple(t.shape)}")
 
     # -------------------------------------------------------------- hot path
-    def cross_spectra(self, Y, weighting="phat", phat_floor=None, out=None):
-        """K1: ``Y`` [F, M, Kb] complex64 -> (Psi [F, P, Kb] complex64,
-        applied floors [F] float64)."""
+    def _check_spectra(self, Y, weighting, phat_floor):
+        """Validate ``Y`` [F, M, Kb] complex64 -> (F, weighting code, abs floor)."""
         if weighting not in ("phat", "identity"):
             raise ValueError(f"unknown weighting {weighting!r}")
         if Y.dim() != 3 or Y.shape[2] != self.Kb:
@@ -198,20 +197,49 @@ class SrpPlan:
         if Y.shape[1] < self.M:
             raise ValueError(f"pair index {self.M - 1} out of range for {Y.shape[1]} channels")
         self._check_frames(Y, (Y.shape[1], self.Kb), torch.complex64, "Y")
-        F = Y.shape[0]
         abs_floor = -1.0
         if weighting == "phat" and phat_floor is not None:
             if not (phat_floor > 0 and math.isfinite(phat_floor)):
                 raise ValueError(f"phat_floor must be positive, got {phat_floor}")
             abs_floor = float(phat_floor)
+        return Y.shape[0], (0 if weighting == "phat" else 1), abs_floor
+
+    def cross_spectra(self, Y, weighting="phat", phat_floor=None, out=None):
+        """K1: ``Y`` [F, M, Kb] complex64 -> (Psi [F, P, Kb] complex64,
+        applied floors [F] float64)."""
+        F, wcode, abs_floor = self._check_spectra(Y, weighting, phat_floor)
         psi = out if out is not None else torch.empty((F, self.P, self.Kb), dtype=torch.complex64,
                                                       device=self.device)
         floors = torch.empty(F, dtype=torch.float64, device=self.device)
         N.call("srpb_gcc_phat", N.ptr(Y), F, Y.shape[1], self.Kb, N.ptr(self.pair_m),
-               N.ptr(self.pair_mp), self.P, 0 if weighting == "phat" else 1,
-               DEFAULT_PHAT_FLOOR_REL, abs_floor, N.ptr(psi), N.ptr(floors),
-               N.stream_handle(self.device))
+               N.ptr(self.pair_mp), self.P, wcode, DEFAULT_PHAT_FLOOR_REL, abs_floor, N.ptr(psi),
+               N.ptr(floors), N.stream_handle(self.device))
         return psi, floors
+
+    def lattice_from_spectra(self, Y, weighting="phat", phat_floor=None, split=False):
+        """K1a + fused K1b/K3: ``Y`` [F, M, Kb] -> Xi [F, T_pad] fp32, or its
+        tf32 split (Xi_hi, Xi_lo) with ``split=True``; the cross-spectra are
+        formed inside the lattice kernel and never stored."""
+        if self.sample_period is None:
+            raise ValueError("plan was built without a lattice (sample_period)")
+        F, wcode, abs_floor = self._check_spectra(Y, weighting, phat_floor)
+        s = N.stream_handle(self.device)
+        floors = None
+        if wcode == 0 and abs_floor <= 0:
+            floors = torch.empty(F, dtype=torch.float64, device=self.device)
+            self._main("srpb_gcc_floor", N.ptr(Y), F, Y.shape[1], self.Kb, N.ptr(self.pair_m),
+                       N.ptr(self.pair_mp), self.P, DEFAULT_PHAT_FLOOR_REL, N.ptr(floors), s)
+        shape = (F, self.T_pad)
+        if split:
+            outs = (None, torch.empty(shape, dtype=torch.float32, device=self.device),
+                    torch.empty(shape, dtype=torch.float32, device=self.device))
+        else:
+            outs = (torch.empty(shape, dtype=torch.float32, device=self.device), None, None)
+        self._main("srpb_lattice_from_spectra", N.ptr(Y), F, Y.shape[1], self.Kb,
+                   N.ptr(self.pair_m), N.ptr(self.pair_mp), self.P, wcode, N.ptr(floors),
+                   abs_floor, N.ptr(self.twiddles), self.L, N.ptr(self.off), N.ptr(self.reach),
+                   self.T_pad, *(N.ptr(o) for o in outs), s)
+        return outs[1:] if split else outs[0]
 
     def _use_tc(self, F, kind):
         """Size heuristic for the tensor-core kernels (not a backend switch:
@@ -300,11 +328,7 @@ class SrpPlan:
         keys = self._keys(F)
         s = N.stream_handle(self.device)
         if self._use_tc(F, "interp"):
-            if self.W_hi is None:
-                self.W_hi, self.W_lo = self.split_tf32(self.W)
-            xh, xl = self.split_tf32(xi)
-            self._main("srpb_interp_tc", N.ptr(self.W_hi), N.ptr(self.W_lo), N.ptr(xh), N.ptr(xl), F,
-                   self.J, self.T_pad, N.ptr(out), N.ptr(keys), self.interp_kb_per_group, s)
+            return self._approx_tc(*self.split_tf32(xi), out, keys)
         elif self.W is not None:
             self._main("srpb_interp", N.ptr(self.W), N.ptr(xi), F, self.J, self.T_pad, N.ptr(out),
                    N.ptr(keys), s)
@@ -312,6 +336,14 @@ class SrpPlan:
             self._main("srpb_interp_onthefly", N.ptr(self.sx_i), N.ptr(self.sx_f), self.P,
                    N.ptr(self.off), N.ptr(self.reach), N.ptr(xi), F, self.J, self.T_pad,
                    N.ptr(out), N.ptr(keys), s)
+        return out, self.keys_to_index(keys)
+
+    def _approx_tc(self, xh, xl, out, keys):
+        if self.W_hi is None:
+            self.W_hi, self.W_lo = self.split_tf32(self.W)
+        self._main("srpb_interp_tc", N.ptr(self.W_hi), N.ptr(self.W_lo), N.ptr(xh), N.ptr(xl),
+                   xh.shape[0], self.J, self.T_pad, N.ptr(out), N.ptr(keys),
+                   self.interp_kb_per_group, N.stream_handle(self.device))
         return out, self.keys_to_index(keys)
 
     def argmax(self, maps):
@@ -324,12 +356,19 @@ class SrpPlan:
         return self.keys_to_index(keys)
 
     def run(self, Y, path="approx", maps=True, weighting="phat", phat_floor=None):
-        """Y [F, M, Kb] complex64 -> (maps | None, argmax) along ``path``."""
-        psi, _ = self.cross_spectra(Y, weighting, phat_floor)
+        """Y [F, M, Kb] complex64 -> (maps | None, argmax) along ``path``.
+        The approximate path fuses K1's cross-spectra into K3."""
         if path == "conventional":
+            psi, _ = self.cross_spectra(Y, weighting, phat_floor)
             return self.conventional(psi, maps)
         if path == "approx":
-            return self.approx(self.lattice(psi), maps)
+            F = Y.shape[0]
+            if self.sample_period is not None and self._use_tc(F, "interp"):
+                xh, xl = self.lattice_from_spectra(Y, weighting, phat_floor, split=True)
+                out = torch.empty((F, self.J), dtype=torch.float32,
+                                  device=self.device) if maps else None
+                return self._approx_tc(xh, xl, out, self._keys(F))
+            return self.approx(self.lattice_from_spectra(Y, weighting, phat_floor), maps)
         raise ValueError(f"unknown path {path!r}")
 
 

@@ -100,6 +100,50 @@ def test_lattice_matches_reference(name):
             assert rel_l2(xi[f, :total], g[f"lattice_{n_aux}"][f]) <= REL_L2_TOL
 
 
+@pytest.mark.parametrize("name", ["c1", "c2_subset", "random_small", "on_lattice"])
+def test_lattice_from_spectra_fused(name):
+    """K1b fused into K3: identical to K1 -> K3 (same per-bin psi rounding,
+    same accumulation order) and to the reference lattice; the tf32 split
+    outputs equal srpb_tf32_split of Xi bitwise."""
+    g = load_golden(name)
+    Y = dev(g["Y"])
+    for n_aux in g["n_aux"]:
+        plan = plan_from_golden(g, int(n_aux))
+        for kw in ({}, {"weighting": "identity"}, {"phat_floor": 1e-3}):
+            two_step = plan.lattice(plan.cross_spectra(Y, **kw)[0])
+            fused = plan.lattice_from_spectra(Y, **kw)
+            assert torch.equal(fused, two_step), (name, n_aux, kw)
+            hi, lo = plan.lattice_from_spectra(Y, split=True, **kw)
+            h2, l2 = plan.split_tf32(fused)
+            assert torch.equal(hi, h2) and torch.equal(lo, l2)
+        xi = plan.lattice_from_spectra(Y).cpu().numpy()
+        total = plan.total_samples
+        assert np.all(xi[:, total:] == 0.0)
+        for f in range(xi.shape[0]):
+            assert rel_l2(xi[f, :total], g[f"lattice_{n_aux}"][f]) <= REL_L2_TOL
+
+
+def test_lattice_from_spectra_odd_bins_and_ragged_tiles():
+    """Odd Kb (partial bin chunk), F not a multiple of the 64-frame tile,
+    reach > 32 lags (several lag tiles) vs the oracle."""
+    rng = np.random.default_rng(7)
+    M, Kb, F = 5, 77, 70
+    pairs = O.canonical_pairs(M)
+    pm = np.array([m for m, _ in pairs], np.int32)
+    pmp = np.array([mp for _, mp in pairs], np.int32)
+    bounds = rng.uniform(1e-3, 3e-3, len(pairs))  # up to 48 samples -> T_p up to 101
+    omega = np.arange(1, Kb + 1) * (2 * np.pi * 16000.0 / 200.0)
+    tdoa = rng.uniform(-1, 1, (9, len(pairs))) * bounds
+    Y = (rng.standard_normal((F, M, Kb)) + 1j * rng.standard_normal((F, M, Kb))).astype(np.complex64)
+    plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=3)
+    xi = plan.lattice_from_spectra(dev(Y)).cpu().numpy()
+    for f in (0, 37, 69):
+        psi = O.cross_spectrum(Y[f].astype(complex), pm, pmp)[0]
+        ref = np.concatenate(O.gcc_lattice(psi, omega, bounds, T, 3)[1])
+        assert rel_l2(xi[f, : plan.total_samples], ref) <= REL_L2_TOL
+    assert np.all(xi[:, plan.total_samples:] == 0.0)
+
+
 # --------------------------------------------------------------------- W
 def test_sinc_table_matches_reference():
     g = load_golden("random_small")
@@ -207,6 +251,8 @@ def test_config_shapes_vs_oracle(cfg, backend):
                            for f in range(F)])
     maps, am = plan.approx(plan.lattice(psi_g))
     assert_maps_match(maps.cpu().numpy(), approx_ref, am.cpu().numpy(), what=f"{cfg} approx")
+    maps, am = plan.run(dev(Y), "approx")  # fused K1b/K3 front end
+    assert_maps_match(maps.cpu().numpy(), approx_ref, am.cpu().numpy(), what=f"{cfg} run")
 
 
 # ------------------------------------ size-independent properties at full C2
