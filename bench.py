@@ -287,10 +287,7 @@ def run_ours(args):
             return out
 
     def step(path):
-        psi, _ = plan.cross_spectra(Y)
-        if path == "approx":
-            return plan.approx(plan.lattice(psi))
-        return plan.conventional(psi)
+        return plan.run(Y, path)
 
     def e2e_step(path):
         Y.copy_(Y_host, non_blocking=True)

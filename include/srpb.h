@@ -47,7 +47,8 @@ const char* srpb_last_error(void);
  * Replaces spectral.cross_spectrum (pkg/src/srpfast/spectral.py:218-285),
  * batched over frames.
  *   Y        [F, M, Kb] complex64 STFT frames
- *   pair_m, pair_mp [P] int32 channel indices (index_m, index_m_prime)
+ *   pair_m, pair_mp [P] int32 channel indices (index_m, index_m_prime);
+ *            M <= 64, P <= 2016
  *   weighting SRPB_WEIGHT_PHAT or SRPB_WEIGHT_IDENTITY
  *   floor_rel adaptive floor factor (DEFAULT_PHAT_FLOOR_REL = 1e-12,
  *             spectral.py:31-32) used when abs_floor <= 0
@@ -63,12 +64,16 @@ int srpb_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
 
 /*
  * K1a: the per-frame PHAT floor alone, floor_rel * sqrt(mean_{p,k} |raw|^2)
- * accumulated in fp64 (spectral.py:268-275); feeds
- * srpb_lattice_from_spectra.  floor_out [F] float64.
+ * accumulated in fp64 (spectral.py:268-275), and per-frame range flags;
+ * feeds srpb_lattice_from_spectra.
+ *   floor_out [F] float64 out or NULL
+ *   clean_out [F] int32 out or NULL: 1 when every |y_m[k]|^2 (fp32) of the
+ *             frame is 0 or inside (1e-30, 1e30) -- the fused lattice then
+ *             skips its per-bin range test (results are identical)
  */
 int srpb_gcc_floor(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
                    const int32_t* pair_mp, int P, double floor_rel, double* floor_out,
-                   void* stream);
+                   int32_t* clean_out, void* stream);
 
 /*
  * K2 conventional SRP maps (harmonic bins w_k = k w_1).
@@ -98,9 +103,11 @@ int srpb_conventional_general(const float* Psi, int F, int P, int Kb,
                               float* maps, unsigned long long* keys, void* stream);
 
 /*
- * Lattice twiddles e^{j w_k n T} for n in [-L, L], fp64 phases rounded to fp32.
- * Signal-independent table of srp.build_gcc_lattice (srp.py:235-236).
- *   omega [Kb] float64, tw [2L+1, Kb] complex64 out (row 0 = lag -L)
+ * Lattice twiddles e^{j w_k n T} for the half-lags n in [0, L] (lag -n is the
+ * conjugate), fp64 phases rounded to fp32.  Signal-independent table of
+ * srp.build_gcc_lattice (srp.py:235-236).
+ *   omega [Kb] float64, tw [Kb, Hs] complex64 out (bin-major), Hs = L+1
+ *   rounded up to a multiple of 16, columns n > L zero
  */
 int srpb_lattice_twiddles(const double* omega, int Kb, double sample_period, int L,
                           float* tw, void* stream);
@@ -108,7 +115,8 @@ int srpb_lattice_twiddles(const double* omega, int Kb, double sample_period, int
 /*
  * K3 lattice GCC samples for F frames.
  * Replaces srp.build_gcc_lattice (srp.py:201-247):
- *   Xi[f, off[p] + n + reach[p]] = 2 Re sum_k psi[f,p,k] tw[L + n, k]
+ *   Xi[f, off[p] + n + reach[p]] = 2 Re sum_k psi[f,p,k] e^{j w_k n T}
+ *   with tw [Kb, Hs] from srpb_lattice_twiddles (lag -n via conjugation)
  *   for n in [-reach[p], reach[p]], reach[p] = N_p + n_aux.
  *   off [P+1] int32 prefix sums of 2 reach + 1; pad columns [off[P], T_pad)
  *   are written as 0.
@@ -126,14 +134,16 @@ int srpb_lattice(const float* Psi, int F, int P, int Kb, const float* tw, int L,
  * srp.build_gcc_lattice srp.py:201-247).
  *   floors [F] float64 (srpb_gcc_floor) for PHAT with the relative floor, or
  *   NULL with abs_floor > 0 (explicit floor); ignored for identity weighting.
+ *   clean [F] int32 (srpb_gcc_floor) or NULL (every bin range-tested).
+ *   tw 16-byte aligned.
  *   Xi [F, T_pad] float32 out and/or Xi_hi, Xi_lo [F, T_pad]: its tf32
  *   operand split (hi = rna(Xi), lo = rna(Xi - hi)) for srpb_interp_tc.
  */
 int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
                               const int32_t* pair_mp, int P, int weighting, const double* floors,
-                              double abs_floor, const float* tw, int L, const int32_t* off,
-                              const int32_t* reach, int T_pad, float* Xi, float* Xi_hi,
-                              float* Xi_lo, void* stream);
+                              double abs_floor, const int32_t* clean, const float* tw, int L,
+                              const int32_t* off, const int32_t* reach, int T_pad, float* Xi,
+                              float* Xi_hi, float* Xi_lo, void* stream);
 
 /*
  * Sinc interpolation table W[j, off[p] + n + reach[p]] = sinc(x[j,p] - n),

@@ -31,10 +31,10 @@ _SIGNATURES = {
     "srpb_lattice": [c_void_p, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_void_p, c_int,
                      c_void_p, c_void_p],
     "srpb_gcc_floor": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_double,
-                       c_void_p, c_void_p],
+                       c_void_p, c_void_p, c_void_p],
     "srpb_lattice_from_spectra": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
-                                  c_void_p, c_double, c_void_p, c_int, c_void_p, c_void_p, c_int,
-                                  c_void_p, c_void_p, c_void_p, c_void_p],
+                                  c_void_p, c_double, c_void_p, c_void_p, c_int, c_void_p,
+                                  c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p],
     "srpb_sinc_table": [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p,
                         c_void_p],
     "srpb_interp": [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],

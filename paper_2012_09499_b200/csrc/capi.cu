@@ -10,11 +10,12 @@ namespace srpb {
 cudaError_t launch_gcc_phat(const float*, int, int, int, const int32_t*, const int32_t*, int, int,
                             double, double, float*, double*, cudaStream_t);
 cudaError_t launch_gcc_floor(const float*, int, int, int, const int32_t*, const int32_t*, int,
-                             double, double*, cudaStream_t);
+                             double, double*, int32_t*, cudaStream_t);
 cudaError_t launch_lattice_from_spectra(const float*, int, int, int, const int32_t*,
                                         const int32_t*, int, int, const double*, double,
-                                        const float*, int, const int32_t*, const int32_t*, int,
-                                        int, float*, float*, float*, cudaStream_t);
+                                        const int32_t*, const float*, int, const int32_t*,
+                                        const int32_t*, int, int, float*, float*, float*,
+                                        cudaStream_t);
 cudaError_t launch_conventional(const float*, int, int, int, int, const int32_t*, const float*,
                                 int, float*, unsigned long long*, cudaStream_t);
 cudaError_t launch_conventional_general(const float*, int, int, int, const double*,
@@ -72,7 +73,7 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 extern "C" {
 
-int srpb_abi_version(void) { return 1; }
+int srpb_abi_version(void) { return 2; }
 
 const char* srpb_last_error(void) { return g_err; }
 
@@ -82,9 +83,11 @@ int srpb_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
   REQUIRE(F >= 0 && M >= 1 && Kb >= 1 && P >= 1, "srpb_gcc_phat: bad shape F=%d M=%d Kb=%d P=%d",
           F, M, Kb, P);
   REQUIRE(M <= 64, "srpb_gcc_phat: at most 64 channels supported, got %d", M);
+  REQUIRE(P <= 2016, "srpb_gcc_phat: at most 2016 pairs supported, got %d", P);
   REQUIRE(weighting == SRPB_WEIGHT_PHAT || weighting == SRPB_WEIGHT_IDENTITY,
           "srpb_gcc_phat: unknown weighting %d", weighting);
   REQUIRE(F == 0 || (Y && Psi && pair_m && pair_mp), "srpb_gcc_phat: null pointer");
+  REQUIRE(static_cast<long long>(F) * P <= 2147483647LL, "srpb_gcc_phat: F*P too large");
   return status(srpb::launch_gcc_phat(Y, F, M, Kb, pair_m, pair_mp, P, weighting, floor_rel,
                                       abs_floor, Psi, floor_out, S(stream)),
                 "srpb_gcc_phat");
@@ -92,13 +95,15 @@ int srpb_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
 
 int srpb_gcc_floor(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
                    const int32_t* pair_mp, int P, double floor_rel, double* floor_out,
-                   void* stream) {
+                   int32_t* clean_out, void* stream) {
   REQUIRE(F >= 0 && M >= 1 && Kb >= 1 && P >= 1, "srpb_gcc_floor: bad shape F=%d M=%d Kb=%d P=%d",
           F, M, Kb, P);
   REQUIRE(M <= 64, "srpb_gcc_floor: at most 64 channels supported, got %d", M);
-  REQUIRE(F == 0 || (Y && pair_m && pair_mp && floor_out), "srpb_gcc_floor: null pointer");
+  REQUIRE(P <= 2016, "srpb_gcc_floor: at most 2016 pairs supported, got %d", P);
+  REQUIRE(floor_out || clean_out, "srpb_gcc_floor: need floor_out and/or clean_out");
+  REQUIRE(F == 0 || (Y && pair_m && pair_mp), "srpb_gcc_floor: null pointer");
   return status(srpb::launch_gcc_floor(Y, F, M, Kb, pair_m, pair_mp, P, floor_rel, floor_out,
-                                       S(stream)),
+                                       clean_out, S(stream)),
                 "srpb_gcc_floor");
 }
 
@@ -137,6 +142,7 @@ int srpb_lattice(const float* Psi, int F, int P, int Kb, const float* tw, int L,
                  const int32_t* off, const int32_t* reach, int T_pad, float* Xi, void* stream) {
   REQUIRE(F >= 0 && P >= 1 && Kb >= 1 && L >= 0 && T_pad >= 1, "srpb_lattice: bad shape");
   REQUIRE(F == 0 || (Psi && tw && off && reach && Xi), "srpb_lattice: null pointer");
+  REQUIRE((reinterpret_cast<uintptr_t>(tw) & 15) == 0, "srpb_lattice: tw must be 16-byte aligned");
   return status(srpb::launch_lattice(Psi, F, P, Kb, tw, L, off, reach, 2 * L + 1, T_pad, Xi,
                                      S(stream)),
                 "srpb_lattice");
@@ -144,7 +150,8 @@ int srpb_lattice(const float* Psi, int F, int P, int Kb, const float* tw, int L,
 
 int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
                               const int32_t* pair_mp, int P, int weighting, const double* floors,
-                              double abs_floor, const float* tw, int L, const int32_t* off,
+                              double abs_floor, const int32_t* clean, const float* tw, int L,
+                              const int32_t* off,
                               const int32_t* reach, int T_pad, float* Xi, float* Xi_hi,
                               float* Xi_lo, void* stream) {
   REQUIRE(F >= 0 && M >= 1 && P >= 1 && Kb >= 1 && L >= 0 && T_pad >= 1,
@@ -158,8 +165,11 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
   REQUIRE(Xi || Xi_hi, "srpb_lattice_from_spectra: need Xi and/or Xi_hi/Xi_lo output");
   REQUIRE(F == 0 || (Y && pair_m && pair_mp && tw && off && reach),
           "srpb_lattice_from_spectra: null pointer");
+  REQUIRE((reinterpret_cast<uintptr_t>(tw) & 15) == 0,
+          "srpb_lattice_from_spectra: tw must be 16-byte aligned");
   return status(srpb::launch_lattice_from_spectra(Y, F, M, Kb, pair_m, pair_mp, P, weighting,
-                                                  floors, abs_floor, tw, L, off, reach, 2 * L + 1,
+                                                  floors, abs_floor, clean, tw, L, off, reach,
+                                                  2 * L + 1,
                                                   T_pad, Xi, Xi_hi, Xi_lo, S(stream)),
                 "srpb_lattice_from_spectra");
 }

@@ -58,18 +58,23 @@ __device__ __forceinline__ void harmonic_phase(int k, int ti, float tf, int peri
 
 // GCC-PHAT weighting of one bin (spectral.py:258-277): raw = a conj(b),
 // psi = raw / max(|raw|, floor), exact 0 where raw == 0; identity: raw.
-__device__ __forceinline__ float2 phat_one(float2 a, float2 b, int weighting, double floor) {
-  if (weighting != 0) {  // identity: raw product, correctly rounded from fp64
-    const double re = static_cast<double>(a.x) * b.x + static_cast<double>(a.y) * b.y;
-    const double im = static_cast<double>(a.y) * b.x - static_cast<double>(a.x) * b.y;
-    return make_float2(static_cast<float>(re), static_cast<float>(im));
-  }
-  if ((a.x == 0.0f && a.y == 0.0f) || (b.x == 0.0f && b.y == 0.0f))
-    return make_float2(0.0f, 0.0f);  // exact-zero product stays zero
+// Per-frame floor constants: the fp64 floor and its fp32 reciprocal (inf for
+// a zero floor; within 1 ulp of 1/floor, it only moves the exact switch-over
+// point, where both branches agree).
+struct PhatFloor {
+  double floor;
+  float inv_floor;
+};
+
+__device__ __forceinline__ PhatFloor make_phat_floor(double floor) {
+  return {floor, __frcp_rn(static_cast<float>(floor))};  // 1/0 = inf
+}
+
+static __device__ __forceinline__ float2 phat_slow(float2 a, float2 b, double floor) {
+  // extreme magnitudes: normalise each factor first (no over/underflow)
   const float ma = hypotf(a.x, a.y), mb = hypotf(b.x, b.y);
   const double mag = static_cast<double>(ma) * mb;
   if (mag >= floor) {
-    // raw/|raw| = (a/|a|) conj(b/|b|): unit modulus, no over/underflow
     const float ua = 1.0f / ma, ub = 1.0f / mb;
     const float ax = a.x * ua, ay = a.y * ua, bx = b.x * ub, by = b.y * ub;
     return make_float2(ax * bx + ay * by, ay * bx - ax * by);
@@ -77,6 +82,74 @@ __device__ __forceinline__ float2 phat_one(float2 a, float2 b, int weighting, do
   const double re = static_cast<double>(a.x) * b.x + static_cast<double>(a.y) * b.y;
   const double im = static_cast<double>(a.y) * b.x - static_cast<double>(a.x) * b.y;
   return make_float2(static_cast<float>(re / floor), static_cast<float>(im / floor));
+}
+
+__device__ __forceinline__ float rsqrt_approx_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Range in which the fast PHAT is exact to fp32 rounding: |y|^2 in
+// (1e-30, 1e30) or exactly 0.  K1a flags frames whose every channel power
+// qualifies ("clean" frames); those skip the per-bin range test.
+__device__ __forceinline__ bool phat_power_clean(float pw) {
+  return pw == 0.0f || (pw > 1e-30f && pw < 1e30f);
+}
+
+// Fast PHAT: 1/|raw| = rsqrt(pa) rsqrt(pb) and raw / max(|raw|, floor) =
+// raw * min(1/|raw|, 1/floor).  The powers are clamped below at 1e-30 so an
+// exact-zero factor gives raw = 0 times a finite scale (= 0, as required).
+// Exact (to fp32 rounding) when both powers are phat_power_clean; other
+// inputs must take phat_slow.
+__device__ __forceinline__ float2 phat_fast(float2 a, float2 b, PhatFloor fl, float& pa,
+                                            float& pb) {
+  pa = fmaf(a.x, a.x, a.y * a.y);
+  pb = fmaf(b.x, b.x, b.y * b.y);
+  const float s = fminf(rsqrt_approx_ftz(fmaxf(pa, 1e-30f)) * rsqrt_approx_ftz(fmaxf(pb, 1e-30f)),
+                        fl.inv_floor);
+  const float re = fmaf(a.x, b.x, a.y * b.y), im = fmaf(a.y, b.x, -(a.x * b.y));
+  return make_float2(re * s, im * s);
+}
+
+__device__ __forceinline__ float2 phat_identity(float2 a, float2 b) {
+  // raw product, correctly rounded from fp64
+  const double re = static_cast<double>(a.x) * b.x + static_cast<double>(a.y) * b.y;
+  const double im = static_cast<double>(a.y) * b.x - static_cast<double>(a.x) * b.y;
+  return make_float2(static_cast<float>(re), static_cast<float>(im));
+}
+
+// per-thread form (any thread subset)
+__device__ __forceinline__ float2 phat_one(float2 a, float2 b, int weighting, PhatFloor fl) {
+  if (weighting != 0) return phat_identity(a, b);
+  float pa, pb;
+  const float2 v = phat_fast(a, b, fl, pa, pb);
+  return phat_power_clean(pa) && phat_power_clean(pb) ? v : phat_slow(a, b, fl.floor);
+}
+
+// Cross-spectrum modes of the fused lattice (CTA-uniform, compile-time):
+enum PsiMode { kPsiStaged = 0, kPsiIdentity = 1, kPsiPhatClean = 2, kPsiPhatChecked = 3 };
+
+// warp form (all 32 lanes active), same values as phat_one: kPsiPhatClean
+// (every lane's frame flagged clean by K1a) skips the range test;
+// kPsiPhatChecked enters the slow path only when some lane needs it
+template <int kMode>
+__device__ __forceinline__ float2 psi_warp(float2 a, float2 b, PhatFloor fl) {
+  if constexpr (kMode == kPsiStaged) {
+    return a;
+  } else if constexpr (kMode == kPsiIdentity) {
+    return phat_identity(a, b);
+  } else {
+    float pa, pb;
+    float2 v = phat_fast(a, b, fl, pa, pb);
+    if constexpr (kMode == kPsiPhatChecked) {
+      const bool slow = !(phat_power_clean(pa) && phat_power_clean(pb));
+      if (__any_sync(0xffffffffu, slow)) {
+        if (slow) v = phat_slow(a, b, fl.floor);
+      }
+    }
+    return v;
+  }
 }
 
 }  // namespace srpb

@@ -19,55 +19,59 @@
 
 namespace srpb {
 
-constexpr int kFloorThreads = 256;
-constexpr int kFloorBinChunk = 64;
-constexpr int kGccMaxSmemChannels = 64;
+constexpr int kFloorThreads = 512;
+constexpr int kFloorSmemPowers = 4096;  // fp64 channel powers staged per pass (32 KB)
+constexpr int kFloorMaxPairs = 2016;    // 64 channels
 
+// One CTA per frame, thread <-> bin: stage |y_m[k]|^2 (fp64) for up to 4096
+// (channel, bin) values per pass (all of them for M <= 8, Kb <= 512: each
+// thread's M loads are in flight together), then accumulate
+// sum_p pw[m_p][k] pw[m'_p][k] with pair indices broadcast from shared
+// memory.  Also flags the frame "clean" when every fp32 channel power lies in
+// the fast PHAT range (phat_power_clean), letting the fused lattice skip its
+// per-bin range tests.
 __global__ void __launch_bounds__(kFloorThreads)
 gcc_floor_kernel(const float2* __restrict__ Y, int M, int Kb, const int32_t* __restrict__ pm,
                  const int32_t* __restrict__ pmp, int P, double floor_rel,
-                 double* __restrict__ floor_out) {
+                 double* __restrict__ floor_out, int32_t* __restrict__ clean_out) {
   const int f = blockIdx.x;
   const float2* y = Y + static_cast<size_t>(f) * M * Kb;
-  __shared__ double s_pow[kGccMaxSmemChannels][kFloorBinChunk];
-  __shared__ int s_pm[1024], s_pmp[1024];
+  __shared__ double s_pow[kFloorSmemPowers];
+  __shared__ int2 s_pair[kFloorMaxPairs];
   __shared__ double s_red[kFloorThreads / 32];
-  const bool pairs_in_smem = P <= 1024;
-  if (pairs_in_smem)
-    for (int e = threadIdx.x; e < P; e += blockDim.x) {
-      s_pm[e] = pm[e];
-      s_pmp[e] = pmp[e];
-    }
+  for (int e = threadIdx.x; e < P; e += kFloorThreads) s_pair[e] = make_int2(pm[e], pmp[e]);
+  const int kc_max = max(1, min(Kb, kFloorSmemPowers / M));
   double acc = 0.0;
-  for (int k0 = 0; k0 < Kb; k0 += kFloorBinChunk) {
-    const int kc = min(kFloorBinChunk, Kb - k0);
-    for (int e = threadIdx.x; e < M * kFloorBinChunk; e += blockDim.x) {
-      const int m = e / kFloorBinChunk, kk = e - m * kFloorBinChunk;
-      double pw = 0.0;
-      if (kk < kc) {
-        const float2 v = y[static_cast<size_t>(m) * Kb + k0 + kk];
-        pw = static_cast<double>(v.x) * v.x + static_cast<double>(v.y) * v.y;
+  bool clean = true;
+  for (int k0 = 0; k0 < Kb; k0 += kc_max) {
+    const int kc = min(kc_max, Kb - k0);
+    for (int kk = threadIdx.x; kk < kc; kk += kFloorThreads) {
+#pragma unroll 8
+      for (int m = 0; m < M; ++m) {
+        const float2 v = __ldg(y + static_cast<size_t>(m) * Kb + k0 + kk);
+        s_pow[m * kc + kk] = static_cast<double>(v.x) * v.x + static_cast<double>(v.y) * v.y;
+        clean = clean && phat_power_clean(fmaf(v.x, v.x, v.y * v.y));
       }
-      s_pow[m][kk] = pw;
     }
     __syncthreads();
-    // thread <-> bin (kk = lane-fast): conflict-free rows of s_pow
-    for (int e = threadIdx.x; e < P * kFloorBinChunk; e += blockDim.x) {
-      const int p = e / kFloorBinChunk, kk = e - p * kFloorBinChunk;
-      const int a = pairs_in_smem ? s_pm[p] : pm[p];
-      const int b = pairs_in_smem ? s_pmp[p] : pmp[p];
-      acc += s_pow[a][kk] * s_pow[b][kk];
+    for (int kk = threadIdx.x; kk < kc; kk += kFloorThreads) {
+#pragma unroll 4
+      for (int pp = 0; pp < P; ++pp) {
+        const int2 ab = s_pair[pp];
+        acc += s_pow[ab.x * kc + kk] * s_pow[ab.y * kc + kk];
+      }
     }
     __syncthreads();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
-  __syncthreads();
+  const bool all_clean = __syncthreads_and(clean);
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int w = 0; w < kFloorThreads / 32; ++w) t += s_red[w];
-    floor_out[f] = floor_rel * sqrt(t / (static_cast<double>(P) * Kb));
+    double sum = 0.0;
+    for (int w = 0; w < kFloorThreads / 32; ++w) sum += s_red[w];
+    if (floor_out) floor_out[f] = floor_rel * sqrt(sum / (static_cast<double>(P) * Kb));
+    if (clean_out) clean_out[f] = all_clean ? 1 : 0;
   }
 }
 
@@ -76,51 +80,49 @@ __global__ void fill_kernel(double* __restrict__ out, int n, double v) {
   if (i < n) out[i] = v;
 }
 
-// one thread per (frame, pair, 2 bins); Kb even
-__global__ void __launch_bounds__(256)
-gcc_psi_kernel(const float4* __restrict__ Y, int F, int M, int Kb2, const int32_t* __restrict__ pm,
+// One CTA per (frame, pair) row, threads along the bins: 16-byte loads of
+// two bins of y_m and y_m' (L2-resident after K1a) and a 16-byte psi store.
+constexpr int kPsiThreads = 128;
+
+__global__ void __launch_bounds__(kPsiThreads)
+gcc_psi_kernel(const float4* __restrict__ Y, int M, int Kb2, const int32_t* __restrict__ pm,
                const int32_t* __restrict__ pmp, int P, int weighting,
                const double* __restrict__ floors, double const_floor, float4* __restrict__ Psi) {
-  const size_t total = static_cast<size_t>(F) * P * Kb2;
-  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t row = e / Kb2;  // f * P + p
-    const int k2 = static_cast<int>(e - row * Kb2);
-    const int f = static_cast<int>(row / P), p = static_cast<int>(row - static_cast<size_t>(f) * P);
-    const float4* yf = Y + static_cast<size_t>(f) * M * Kb2;
-    const float4 a = __ldg(yf + static_cast<size_t>(__ldg(pm + p)) * Kb2 + k2);
-    const float4 b = __ldg(yf + static_cast<size_t>(__ldg(pmp + p)) * Kb2 + k2);
-    const double fl = floors ? __ldg(floors + f) : const_floor;
+  const int row = blockIdx.x;  // f * P + p
+  const int f = row / P, p = row - f * P;
+  const float4* ya = Y + (static_cast<size_t>(f) * M + __ldg(pm + p)) * Kb2;
+  const float4* yb = Y + (static_cast<size_t>(f) * M + __ldg(pmp + p)) * Kb2;
+  const PhatFloor fl = make_phat_floor(floors ? __ldg(floors + f) : const_floor);
+  float4* out = Psi + static_cast<size_t>(row) * Kb2;
+  for (int k2 = threadIdx.x; k2 < Kb2; k2 += kPsiThreads) {
+    const float4 a = __ldg(ya + k2), b = __ldg(yb + k2);
     const float2 o0 = phat_one(make_float2(a.x, a.y), make_float2(b.x, b.y), weighting, fl);
     const float2 o1 = phat_one(make_float2(a.z, a.w), make_float2(b.z, b.w), weighting, fl);
-    Psi[e] = make_float4(o0.x, o0.y, o1.x, o1.y);
+    out[k2] = make_float4(o0.x, o0.y, o1.x, o1.y);
   }
 }
 
 // odd Kb or unaligned buffers: one bin per thread
-__global__ void __launch_bounds__(256)
-gcc_psi1_kernel(const float2* __restrict__ Y, int F, int M, int Kb, const int32_t* __restrict__ pm,
+__global__ void __launch_bounds__(kPsiThreads)
+gcc_psi1_kernel(const float2* __restrict__ Y, int M, int Kb, const int32_t* __restrict__ pm,
                 const int32_t* __restrict__ pmp, int P, int weighting,
                 const double* __restrict__ floors, double const_floor, float2* __restrict__ Psi) {
-  const size_t total = static_cast<size_t>(F) * P * Kb;
-  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t row = e / Kb;
-    const int k = static_cast<int>(e - row * Kb);
-    const int f = static_cast<int>(row / P), p = static_cast<int>(row - static_cast<size_t>(f) * P);
-    const float2* yf = Y + static_cast<size_t>(f) * M * Kb;
-    const double fl = floors ? floors[f] : const_floor;
-    Psi[e] = phat_one(yf[static_cast<size_t>(pm[p]) * Kb + k], yf[static_cast<size_t>(pmp[p]) * Kb + k],
-                      weighting, fl);
-  }
+  const int row = blockIdx.x;
+  const int f = row / P, p = row - f * P;
+  const float2* ya = Y + (static_cast<size_t>(f) * M + __ldg(pm + p)) * Kb;
+  const float2* yb = Y + (static_cast<size_t>(f) * M + __ldg(pmp + p)) * Kb;
+  const PhatFloor fl = make_phat_floor(floors ? __ldg(floors + f) : const_floor);
+  float2* out = Psi + static_cast<size_t>(row) * Kb;
+  for (int k = threadIdx.x; k < Kb; k += kPsiThreads)
+    out[k] = phat_one(__ldg(ya + k), __ldg(yb + k), weighting, fl);
 }
 
 cudaError_t launch_gcc_floor(const float* Y, int F, int M, int Kb, const int32_t* pm,
                              const int32_t* pmp, int P, double floor_rel, double* floor_out,
-                             cudaStream_t stream) {
+                             int32_t* clean_out, cudaStream_t stream) {
   if (F == 0) return cudaSuccess;
   gcc_floor_kernel<<<F, kFloorThreads, 0, stream>>>(reinterpret_cast<const float2*>(Y), M, Kb, pm,
-                                                     pmp, P, floor_rel, floor_out);
+                                                     pmp, P, floor_rel, floor_out, clean_out);
   return cudaGetLastError();
 }
 
@@ -143,7 +145,7 @@ cudaError_t launch_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t*
       if (e != cudaSuccess) return e;
     }
     gcc_floor_kernel<<<F, kFloorThreads, 0, stream>>>(reinterpret_cast<const float2*>(Y), M, Kb,
-                                                       pm, pmp, P, floor_rel, floors);
+                                                       pm, pmp, P, floor_rel, floors, nullptr);
   } else if (floor_out) {
     fill_kernel<<<(F + 255) / 256, 256, 0, stream>>>(floor_out, F, const_floor);
   }
@@ -151,16 +153,15 @@ cudaError_t launch_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t*
   if (e != cudaSuccess) return e;
   const bool vec = Kb % 2 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0 &&
                    (reinterpret_cast<uintptr_t>(Psi) & 15) == 0;
-  const size_t elems = static_cast<size_t>(F) * P * (vec ? Kb / 2 : Kb);
-  const int blocks = static_cast<int>(std::min<size_t>((elems + 255) / 256, 16 * kNumSMs));
+  const int rows = F * P;
   if (vec)
-    gcc_psi_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(Y), F, M, Kb / 2, pm,
-                                               pmp, P, weighting, floors, const_floor,
-                                               reinterpret_cast<float4*>(Psi));
+    gcc_psi_kernel<<<rows, kPsiThreads, 0, stream>>>(reinterpret_cast<const float4*>(Y), M, Kb / 2,
+                                                     pm, pmp, P, weighting, floors, const_floor,
+                                                     reinterpret_cast<float4*>(Psi));
   else
-    gcc_psi1_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float2*>(Y), F, M, Kb, pm,
-                                                pmp, P, weighting, floors, const_floor,
-                                                reinterpret_cast<float2*>(Psi));
+    gcc_psi1_kernel<<<rows, kPsiThreads, 0, stream>>>(reinterpret_cast<const float2*>(Y), M, Kb,
+                                                      pm, pmp, P, weighting, floors, const_floor,
+                                                      reinterpret_cast<float2*>(Psi));
   e = cudaGetLastError();
   if (per_frame && !floor_out) {
     const cudaError_t e2 = cudaFreeAsync(floors, stream);

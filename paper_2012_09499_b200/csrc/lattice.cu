@@ -16,35 +16,56 @@
 
 namespace srpb {
 
+__host__ __device__ constexpr int twiddle_stride(int L) { return (L + 1 + 15) / 16 * 16; }
+
 __global__ void lattice_twiddle_kernel(const double* __restrict__ omega, int Kb, double T,
                                        int L, float2* __restrict__ tw) {
-  const int row = blockIdx.y;  // lag n = row - L
-  const double lag = static_cast<double>(row - L) * T;  // offsets * sample_period (:235)
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < Kb; k += gridDim.x * blockDim.x) {
-    double s, c;
-    sincos(lag * omega[k], &s, &c);  // exp(1j * outer(lags, omega)) (:236)
-    tw[static_cast<size_t>(row) * Kb + k] = make_float2(static_cast<float>(c), static_cast<float>(s));
+  // tw [Kb, Hs]: half-lags n = 0..L of bin k contiguous (lag -n = conj),
+  // zero-padded to a multiple of 16 columns (whole 128-byte windows)
+  const int Hs = twiddle_stride(L);
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < Kb * Hs; e += gridDim.x * blockDim.x) {
+    const int k = e / Hs, n = e - k * Hs;
+    double sn = 0.0, cs = 0.0;
+    if (n <= L) sincos(static_cast<double>(n) * T * omega[k], &sn, &cs);  // (:235-236)
+    tw[e] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
   }
 }
 
-// Register-tiled SIMT GEMM per pair: Xi_p[f, n] = 2 Re sum_k psi[f,p,k] tw[n,k].
-// CTA = (pair p, 64 frames, 32 lags); 128 threads, each owning 4 consecutive
-// frames x 4 lags (n = ng + 8 i) in 16 fp32 accumulators.  Bins stream through
-// double-buffered shared memory in chunks of 32: s_psi[k][f] (row stride 66
-// complex -> 16-byte aligned LDS.128 of 2 frames) and s_tw[k][n] (odd row
-// stride 33 -> conflict-free transposed staging, 8 consecutive lags per
-// LDS.64 wavefront).  Per bin a thread issues 2 LDS.128 + 4 LDS.64 for 32 FFMA.
-// kFromY: psi is generated in the staging pass from the channel spectra Y and
-// the per-frame floors (K1's psi pass fused in: the cross-spectra never
-// round-trip through HBM); otherwise it is read from Psi.
-constexpr int kLatF = 64;      // frames per CTA
-constexpr int kLatN = 32;      // lags per CTA
-constexpr int kLatK = 32;      // bins per shared-memory chunk
-constexpr int kLatThreads = 128;
-constexpr int kLatPsiStride = kLatF + 2;
-constexpr int kLatTwStride = kLatN + 1;
-constexpr int kLatPsiPerThread = kLatF * kLatK / kLatThreads;  // 16
-constexpr int kLatTwPerThread = kLatN * kLatK / kLatThreads;   // 8
+// Half-lag SIMT GEMM per pair.  With c = cos(w_k n T), s = sin(w_k n T):
+//   A[n] = sum_k Re(psi_k) c,  B[n] = sum_k Im(psi_k) s,
+//   Xi[+n] = 2 (A - B),  Xi[-n] = 2 (A + B)
+// so only the R+1 non-negative lags are contracted (half the FMAs of the
+// direct form).  CTA = (pair p, 32 frames, up to 16 half-lags), 8 warps:
+// lane = frame, warp w = K-slice (bins 32c + 4w .. 32c + 4w + 3 of every
+// 32-bin chunk c), each thread accumulating A and B for its half-lags in
+// registers; the 8 slices are summed in a fixed order through shared memory
+// at the end (deterministic, independent of the frame batching).
+//
+// Staging: every warp runs its own 4-stage cp.async ring over its slice (no
+// CTA barrier until the final reduction, no registers held by loads in
+// flight).  Sources are read in 16-byte bin pairs and land as raw[ch][pair]
+// [f] (float4 = two bins of frame f), so the compute lane of frame f reads
+// two bins per conflict-free LDS.128.  kFromY: the two channel rows of Y are
+// staged and psi is formed in the compute loop (GCC-PHAT of K1 fused in: one
+// evaluation per (frame, pair, bin), the cross-spectra never touch HBM);
+// otherwise the psi row is staged.  All variants run the same arithmetic, so
+// fused and two-step results agree bitwise.
+constexpr int kLatF = 32;        // frames per CTA (lane = frame)
+constexpr int kLatWarps = 8;     // K-slices
+constexpr int kLatThreads = 32 * kLatWarps;
+constexpr int kLatBinsW = 4;     // bins per warp per stage
+constexpr int kLatChunk = kLatBinsW * kLatWarps;
+constexpr int kLatHl = 16;       // half-lags per CTA
+constexpr int kLatStages = 4;
+constexpr int kLatRow = 36;      // float4 per raw row (32 frames; 36 = 4 mod 8: conflict-free copies)
+constexpr int kLatRaw = 2 * (kLatBinsW / 2) * kLatRow;  // float4: [ch][pair][f]
+constexpr int kLatTwW = kLatBinsW * kLatHl / 2;          // float4: [bin][h/2]
+constexpr int kLatStageW = kLatRaw + kLatTwW;            // float4 per warp stage
+constexpr size_t kLatSmemBytes = sizeof(float4) * kLatWarps * kLatStages * kLatStageW;
+static_assert(sizeof(float4) * kLatWarps * kLatStages * kLatStageW >=
+                  sizeof(float) * kLatWarps * 2 * kLatHl * kLatF,
+              "reduction buffer aliases the stages");
+static_assert(kLatTwW == 32 && kLatBinsW == 4, "copy mapping: one twiddle float4 per lane");
 
 struct LatticeArgs {
   const float2* src;  // Psi [F, P, Kb] or Y [F, M, Kb]
@@ -54,14 +75,16 @@ struct LatticeArgs {
   int weighting;
   const double* floors;  // per-frame floor (kFromY) or NULL -> const_floor
   double const_floor;
-  const float2* tw;
-  int L;
+  const int32_t* clean;  // per-frame K1a range flags (kFromY) or NULL
+  const float2* tw;      // [Kb, Hs]: e^{j w_k n T}, n = 0..L, zero beyond
+  int Hs;                // row stride, multiple of 16
   const int32_t* off;
   const int32_t* reach;
   int T_pad;
   float* Xi;     // [F, T_pad] or NULL
   float* Xi_hi;  // optional tf32 split of Xi for the tensor-core K4 (or NULL)
   float* Xi_lo;
+  int vec16;     // 16-byte copies (Kb even, 16-byte aligned source)
 };
 
 __device__ __forceinline__ void lattice_store(const LatticeArgs& a, size_t idx, float v) {
@@ -73,8 +96,163 @@ __device__ __forceinline__ void lattice_store(const LatticeArgs& a, size_t idx, 
   }
 }
 
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(umma::smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(umma::smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// one warp's view of the CTA: its K-slice, its ring, its copy sources
+struct LatticeWarp {
+  float4* ring;             // [stage][kLatStageW]
+  const float2* src[2][2];  // [ch][half]: row of frame (lane/2 + 16 half), clamped
+  const float2* twsrc;      // this lane's twiddle column window at bin 0
+  int nch, kbase;           // channels staged; first bin of the slice in chunk 0
+};
+
+template <int kNch>
+__device__ __forceinline__ void lattice_issue(const LatticeArgs& a, const LatticeWarp& w, int c,
+                                              int st) {
+  const int lane = threadIdx.x & 31;
+  float4* base = w.ring + st * kLatStageW;
+  const int k0 = c * kLatChunk + w.kbase;
+  // raw: lane -> (bin pair pr = lane & 1, frame lane/2 + 16 half)
+  const int pr = lane & 1;
+  const int kp = min(k0 + 2 * pr, a.Kb - 1);  // first bin of the pair (clamped)
+#pragma unroll
+  for (int ch = 0; ch < kNch; ++ch)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float4* dst = base + (ch * 2 + pr) * kLatRow + (lane >> 1) + 16 * half;
+      const float2* s = w.src[ch][half] + kp;
+      if (a.vec16) {
+        cp_async16(dst, s);
+      } else {
+        cp_async8(dst, s);
+        cp_async8(reinterpret_cast<float2*>(dst) + 1, s + (kp + 1 < a.Kb ? 1 : 0));
+      }
+    }
+  // twiddles: lane -> (bin lane/8, half-lag pair lane%8)
+  const int kt = min(k0 + (lane >> 3), a.Kb - 1);
+  cp_async16(base + kLatRaw + lane, w.twsrc + static_cast<size_t>(kt) * a.Hs);
+}
+
+template <int HL>
+__device__ __forceinline__ void lattice_bin(float2 v, const float4* trow, float (&A)[kLatHl],
+                                            float (&B)[kLatHl]) {
+#pragma unroll
+  for (int q = 0; q < HL / 2; ++q) {
+    const float4 t = trow[q];  // (c, s) of half-lags 2q, 2q+1
+    A[2 * q] = fmaf(v.x, t.x, A[2 * q]);
+    B[2 * q] = fmaf(v.y, t.y, B[2 * q]);
+    A[2 * q + 1] = fmaf(v.x, t.z, A[2 * q + 1]);
+    B[2 * q + 1] = fmaf(v.y, t.w, B[2 * q + 1]);
+  }
+}
+
+template <int kMode, int HL>
+__device__ __forceinline__ void lattice_body(const LatticeArgs& a, const LatticeWarp& w,
+                                             PhatFloor fl, float (&A)[kLatHl],
+                                             float (&B)[kLatHl]) {
+  constexpr int kNch = kMode == kPsiStaged ? 1 : 2;
+  const int lane = threadIdx.x & 31;
+  const int n = (a.Kb + kLatChunk - 1) / kLatChunk;
+#pragma unroll
+  for (int c = 0; c < kLatStages - 1; ++c) {
+    if (c < n) lattice_issue<kNch>(a, w, c, c);
+    cp_async_commit();
+  }
+  for (int c = 0; c < n; ++c) {
+    cp_async_wait<kLatStages - 2>();  // this lane's copies of chunk c landed
+    __syncwarp();                     // the warp's; stage (c-1)%S is free
+    if (c + kLatStages - 1 < n)
+      lattice_issue<kNch>(a, w, c + kLatStages - 1, (c + kLatStages - 1) % kLatStages);
+    cp_async_commit();
+    const float4* stage = w.ring + (c % kLatStages) * kLatStageW;
+    const int kvalid = a.Kb - (c * kLatChunk + w.kbase);  // bins of the slice inside Kb
+#pragma unroll
+    for (int pr = 0; pr < kLatBinsW / 2; ++pr) {
+      const float4 ra = stage[pr * kLatRow + lane];
+      const float4 rb = kNch == 2 ? stage[(2 + pr) * kLatRow + lane] : ra;
+      float2 v0 = psi_warp<kMode>(make_float2(ra.x, ra.y), make_float2(rb.x, rb.y), fl);
+      float2 v1 = psi_warp<kMode>(make_float2(ra.z, ra.w), make_float2(rb.z, rb.w), fl);
+      if (2 * pr >= kvalid) v0 = make_float2(0.0f, 0.0f);  // clamped copies past Kb
+      if (2 * pr + 1 >= kvalid) v1 = make_float2(0.0f, 0.0f);
+      const float4* tw = stage + kLatRaw + (2 * pr) * (kLatHl / 2);
+      lattice_bin<HL>(v0, tw, A, B);
+      lattice_bin<HL>(v1, tw + kLatHl / 2, A, B);
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int HL>
+__device__ __forceinline__ void lattice_reduce_store(const LatticeArgs& a, float* red, int p,
+                                                     int f0, int fv, int hl0, int R,
+                                                     const float (&A)[kLatHl],
+                                                     const float (&B)[kLatHl]) {
+  // fixed-order reduction over the 8 K-slices: red[w][acc][frame]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();  // every warp is done with its ring (aliased by red)
+#pragma unroll
+  for (int h = 0; h < HL; ++h) {
+    red[(warp * 2 * kLatHl + h) * kLatF + lane] = A[h];
+    red[(warp * 2 * kLatHl + kLatHl + h) * kLatF + lane] = B[h];
+  }
+  __syncthreads();
+  const int col0 = __ldg(a.off + p) + R;  // column of lag 0
+  for (int o = threadIdx.x; o < kLatF * HL; o += kLatThreads) {
+    const int fl = o % kLatF, h = o / kLatF;
+    const int f = f0 + fl, n_lag = hl0 + h;
+    if (fl >= fv || n_lag > R) continue;
+    float sa = 0.0f, sb = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kLatWarps; ++w) {
+      sa += red[(w * 2 * kLatHl + h) * kLatF + fl];
+      sb += red[(w * 2 * kLatHl + kLatHl + h) * kLatF + fl];
+    }
+    const size_t row = static_cast<size_t>(f) * a.T_pad + col0;
+    lattice_store(a, row + n_lag, 2.0f * (sa - sb));
+    if (n_lag > 0) lattice_store(a, row - n_lag, 2.0f * (sa + sb));
+  }
+}
+
+template <int kMode, int HL>
+__device__ __forceinline__ void lattice_run(const LatticeArgs& a, const LatticeWarp& w,
+                                         PhatFloor fl, float* red, int p, int f0, int fv,
+                                         int hl0, int R) {
+  float A[kLatHl], B[kLatHl];
+#pragma unroll
+  for (int h = 0; h < kLatHl; ++h) A[h] = B[h] = 0.0f;
+  lattice_body<kMode, HL>(a, w, fl, A, B);
+  lattice_reduce_store<HL>(a, red, p, f0, fv, hl0, R, A, B);
+}
+
+template <int kMode>
+__device__ __forceinline__ void lattice_dispatch_hl(int hlc, const LatticeArgs& a,
+                                                    const LatticeWarp& w, PhatFloor fl,
+                                                    float* red, int p, int f0, int fv, int hl0,
+                                                    int R) {
+  if (hlc <= 8)
+    lattice_run<kMode, 8>(a, w, fl, red, p, f0, fv, hl0, R);
+  else if (hlc <= 12)
+    lattice_run<kMode, 12>(a, w, fl, red, p, f0, fv, hl0, R);
+  else
+    lattice_run<kMode, 16>(a, w, fl, red, p, f0, fv, hl0, R);
+}
+
 template <bool kFromY>
-__global__ void __launch_bounds__(kLatThreads)
+__global__ void __launch_bounds__(kLatThreads, 2)
 lattice_kernel(const LatticeArgs a) {
   const int p = blockIdx.x;
   const int f0 = blockIdx.y * kLatF;
@@ -90,136 +268,62 @@ lattice_kernel(const LatticeArgs a) {
     return;
   }
   const int R = __ldg(a.reach + p);
-  const int Tp = 2 * R + 1;
-  const int n_base = blockIdx.z * kLatN;  // local lag index (0 = lag -R)
-  if (n_base >= Tp) return;
+  const int hl0 = blockIdx.z * kLatHl;
+  if (hl0 > R) return;
 
-  extern __shared__ __align__(16) float2 s_lat[];
-  auto s_psi = reinterpret_cast<float2(*)[kLatK][kLatPsiStride]>(s_lat);
-  auto s_tw = reinterpret_cast<float2(*)[kLatK][kLatTwStride]>(s_lat + 2 * kLatK * kLatPsiStride);
-
-  // staging roles: psi item j -> (k = tid%8 + 8 (j%4), f = tid/8 + 16 (j/4)):
-  // per warp 4 frames x 8 consecutive bins per load; tw item j -> (k = tid%32,
-  // n = tid/32 + 4 j): one 256-byte row segment per warp
-  const int sk = tid & 7, sf = tid >> 3;
-  const int tk = tid & 31, tn = tid >> 5;
-  const float2* rowA[4];
-  const float2* rowB[4];
-  double fl[4];
-  bool fvalid[4];
+  extern __shared__ __align__(16) float4 s_lat[];
+  const int warp = tid >> 5, lane = tid & 31;
+  const int fv = min(kLatF, a.F - f0);
+  LatticeWarp w;
+  w.ring = s_lat + warp * kLatStages * kLatStageW;
+  w.kbase = warp * kLatBinsW;
+  w.twsrc = a.tw + hl0 + 2 * (lane & 7);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int f = f0 + sf + 16 * q;
-    fvalid[q] = f < a.F;
-    const int fc = fvalid[q] ? f : 0;
+  for (int half = 0; half < 2; ++half) {
+    const size_t f = static_cast<size_t>(f0 + min((lane >> 1) + 16 * half, fv - 1));
     if constexpr (kFromY) {
-      const float2* y = a.src + static_cast<size_t>(fc) * a.M * a.Kb;
-      rowA[q] = y + static_cast<size_t>(__ldg(a.pm + p)) * a.Kb;
-      rowB[q] = y + static_cast<size_t>(__ldg(a.pmp + p)) * a.Kb;
-      fl[q] = a.floors ? __ldg(a.floors + fc) : a.const_floor;
+      w.src[0][half] = a.src + (f * a.M + __ldg(a.pm + p)) * a.Kb;
+      w.src[1][half] = a.src + (f * a.M + __ldg(a.pmp + p)) * a.Kb;
     } else {
-      rowA[q] = a.src + (static_cast<size_t>(fc) * a.P + p) * a.Kb;
-      rowB[q] = nullptr;
-      fl[q] = 0.0;
+      w.src[0][half] = w.src[1][half] = a.src + (f * a.P + p) * a.Kb;
     }
   }
-  const float2* twrow[kLatTwPerThread];
-  bool nvalid[kLatTwPerThread];
-#pragma unroll
-  for (int j = 0; j < kLatTwPerThread; ++j) {
-    const int ni = n_base + tn + 4 * j;
-    nvalid[j] = ni < Tp;
-    twrow[j] = a.tw + static_cast<size_t>(a.L - R + (nvalid[j] ? ni : 0)) * a.Kb;
-  }
-
-  float2 ra[kLatPsiPerThread], rb[kFromY ? kLatPsiPerThread : 1];
-  float2 rt[kLatTwPerThread];
-  auto fetch = [&](int k0) {
-#pragma unroll
-    for (int j = 0; j < kLatPsiPerThread; ++j) {
-      const int k = k0 + sk + 8 * (j & 3);
-      const int q = j >> 2;
-      const bool ok = fvalid[q] && k < a.Kb;
-      ra[j] = ok ? __ldg(rowA[q] + k) : make_float2(0.0f, 0.0f);
-      if constexpr (kFromY) rb[j] = ok ? __ldg(rowB[q] + k) : make_float2(0.0f, 0.0f);
-    }
-#pragma unroll
-    for (int j = 0; j < kLatTwPerThread; ++j) {
-      const int k = k0 + tk;
-      rt[j] = (nvalid[j] && k < a.Kb) ? __ldg(twrow[j] + k) : make_float2(0.0f, 0.0f);
-    }
-  };
-  auto stage = [&](int buf) {
-#pragma unroll
-    for (int j = 0; j < kLatPsiPerThread; ++j) {
-      float2 v = ra[j];
-      if constexpr (kFromY) v = phat_one(ra[j], rb[j], a.weighting, fl[j >> 2]);
-      s_psi[buf][sk + 8 * (j & 3)][sf + 16 * (j >> 2)] = v;
-    }
-#pragma unroll
-    for (int j = 0; j < kLatTwPerThread; ++j) s_tw[buf][tk][tn + 4 * j] = rt[j];
-  };
-
-  // compute roles: frames 4 fg .. 4 fg + 3, lags ng + 8 i
-  const int ng = tid & 7, fg = tid >> 3;
-  float acc[4][4];
-#pragma unroll
-  for (int x = 0; x < 4; ++x)
-#pragma unroll
-    for (int y = 0; y < 4; ++y) acc[x][y] = 0.0f;
-
-  const int n_chunks = (a.Kb + kLatK - 1) / kLatK;
-  fetch(0);
-  stage(0);
-  __syncthreads();
-  for (int c = 0; c < n_chunks; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < n_chunks) fetch((c + 1) * kLatK);
-#pragma unroll 8
-    for (int kk = 0; kk < kLatK; ++kk) {
-      const float4 v01 = *reinterpret_cast<const float4*>(&s_psi[buf][kk][4 * fg]);
-      const float4 v23 = *reinterpret_cast<const float4*>(&s_psi[buf][kk][4 * fg + 2]);
-      const float2 v[4] = {make_float2(v01.x, v01.y), make_float2(v01.z, v01.w),
-                           make_float2(v23.x, v23.y), make_float2(v23.z, v23.w)};
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 t = s_tw[buf][kk][ng + 8 * i];
-#pragma unroll
-        for (int x = 0; x < 4; ++x) acc[x][i] = fmaf(v[x].x, t.x, fmaf(-v[x].y, t.y, acc[x][i]));
-      }
-    }
-    if (c + 1 < n_chunks) stage(buf ^ 1);
-    __syncthreads();
-  }
-  const int col0 = __ldg(a.off + p) + n_base;
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    const int f = f0 + 4 * fg + x;
-    if (f >= a.F) continue;
-    const size_t row = static_cast<size_t>(f) * a.T_pad + col0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (n_base + ng + 8 * i < Tp) lattice_store(a, row + ng + 8 * i, 2.0f * acc[x][i]);
+  const int hlc = min(kLatHl, R + 1 - hl0);  // half-lags this CTA owns
+  float* red = reinterpret_cast<float*>(s_lat);
+  if constexpr (kFromY) {
+    const int f = f0 + min(lane, fv - 1);  // lane = frame
+    const PhatFloor fl = make_phat_floor(a.floors ? __ldg(a.floors + f) : a.const_floor);
+    // CTA-uniform: every warp sees the same 32 frames
+    const bool clean = __all_sync(0xffffffffu, a.clean != nullptr && __ldg(a.clean + f) != 0);
+    if (a.weighting != 0)
+      lattice_dispatch_hl<kPsiIdentity>(hlc, a, w, fl, red, p, f0, fv, hl0, R);
+    else if (clean)
+      lattice_dispatch_hl<kPsiPhatClean>(hlc, a, w, fl, red, p, f0, fv, hl0, R);
+    else
+      lattice_dispatch_hl<kPsiPhatChecked>(hlc, a, w, fl, red, p, f0, fv, hl0, R);
+  } else {
+    lattice_dispatch_hl<kPsiStaged>(hlc, a, w, PhatFloor{0.0, 0.0f}, red, p, f0, fv, hl0, R);
   }
 }
 
 cudaError_t launch_lattice_twiddles(const double* omega, int Kb, double T, int L, float* tw,
                                     cudaStream_t stream) {
-  dim3 grid((Kb + 255) / 256, 2 * L + 1);
-  lattice_twiddle_kernel<<<grid, 256, 0, stream>>>(omega, Kb, T, L, reinterpret_cast<float2*>(tw));
+  const int blocks = (Kb * twiddle_stride(L) + 255) / 256;
+  lattice_twiddle_kernel<<<blocks, 256, 0, stream>>>(omega, Kb, T, L, reinterpret_cast<float2*>(tw));
   return cudaGetLastError();
 }
 
 static cudaError_t launch_lattice_args(const LatticeArgs& a, bool from_y, int max_Tp,
                                       cudaStream_t stream) {
-  constexpr int smem = static_cast<int>(sizeof(float2)) * 2 * kLatK * (kLatPsiStride + kLatTwStride);
+  constexpr int smem = static_cast<int>(kLatSmemBytes);
   // per launch: the attribute is per device, and setting it is cheap
   cudaError_t e = from_y ? cudaFuncSetAttribute(lattice_kernel<true>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
                          : cudaFuncSetAttribute(lattice_kernel<false>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(a.P + 1, (a.F + kLatF - 1) / kLatF, (max_Tp + kLatN - 1) / kLatN);
+  const int max_reach = (max_Tp - 1) / 2;
+  dim3 grid(a.P + 1, (a.F + kLatF - 1) / kLatF, max_reach / kLatHl + 1);
   if (from_y)
     lattice_kernel<true><<<grid, kLatThreads, smem, stream>>>(a);
   else
@@ -227,26 +331,31 @@ static cudaError_t launch_lattice_args(const LatticeArgs& a, bool from_y, int ma
   return cudaGetLastError();
 }
 
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 cudaError_t launch_lattice(const float* Psi, int F, int P, int Kb, const float* tw, int L,
                            const int32_t* off, const int32_t* reach, int max_Tp, int T_pad,
                            float* Xi, cudaStream_t stream) {
   if (F == 0) return cudaSuccess;
   LatticeArgs a{reinterpret_cast<const float2*>(Psi), F, P, Kb, 0, nullptr, nullptr, 1,
-                nullptr, 0.0, reinterpret_cast<const float2*>(tw), L, off, reach, T_pad, Xi,
-                nullptr, nullptr};
+                nullptr, 0.0, nullptr, reinterpret_cast<const float2*>(tw), twiddle_stride(L),
+                off, reach, T_pad, Xi, nullptr, nullptr, Kb % 2 == 0 && aligned16(Psi)};
   return launch_lattice_args(a, false, max_Tp, stream);
 }
 
 cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_t* pm,
                                         const int32_t* pmp, int P, int weighting,
-                                        const double* floors, double abs_floor, const float* tw,
+                                        const double* floors, double abs_floor,
+                                        const int32_t* clean, const float* tw,
                                         int L, const int32_t* off, const int32_t* reach,
                                         int max_Tp, int T_pad, float* Xi, float* Xi_hi,
                                         float* Xi_lo, cudaStream_t stream) {
   if (F == 0) return cudaSuccess;
   LatticeArgs a{reinterpret_cast<const float2*>(Y), F, P, Kb, M, pm, pmp, weighting,
                 weighting == 0 ? floors : nullptr, weighting == 0 ? abs_floor : 0.0,
-                reinterpret_cast<const float2*>(tw), L, off, reach, T_pad, Xi, Xi_hi, Xi_lo};
+                weighting == 0 ? clean : nullptr, reinterpret_cast<const float2*>(tw),
+                twiddle_stride(L), off, reach, T_pad, Xi, Xi_hi, Xi_lo,
+                Kb % 2 == 0 && aligned16(Y)};
   return launch_lattice_args(a, true, max_Tp, stream);
 }
 

@@ -147,7 +147,8 @@ class SrpPlan:
         self.off = torch.as_tensor(off, device=dev)
         self.L = int(reach.max())
         self.omega_dev = torch.as_tensor(self.omega, device=dev)
-        self.twiddles = torch.empty((2 * self.L + 1, self.Kb, 2), dtype=torch.float32, device=dev)
+        self.twiddles = torch.empty((self.Kb, (self.L + 16) // 16 * 16, 2), dtype=torch.float32,
+                                    device=dev)
         s = N.stream_handle(dev)
         N.call("srpb_lattice_twiddles", N.ptr(self.omega_dev), self.Kb, T, self.L,
                N.ptr(self.twiddles), s)
@@ -224,11 +225,14 @@ class SrpPlan:
             raise ValueError("plan was built without a lattice (sample_period)")
         F, wcode, abs_floor = self._check_spectra(Y, weighting, phat_floor)
         s = N.stream_handle(self.device)
-        floors = None
-        if wcode == 0 and abs_floor <= 0:
-            floors = torch.empty(F, dtype=torch.float64, device=self.device)
+        floors = clean = None
+        if wcode == 0:  # K1a: relative floors and per-frame range flags
+            clean = torch.empty(F, dtype=torch.int32, device=self.device)
+            if abs_floor <= 0:
+                floors = torch.empty(F, dtype=torch.float64, device=self.device)
             self._main("srpb_gcc_floor", N.ptr(Y), F, Y.shape[1], self.Kb, N.ptr(self.pair_m),
-                       N.ptr(self.pair_mp), self.P, DEFAULT_PHAT_FLOOR_REL, N.ptr(floors), s)
+                       N.ptr(self.pair_mp), self.P, DEFAULT_PHAT_FLOOR_REL, N.ptr(floors),
+                       N.ptr(clean), s)
         shape = (F, self.T_pad)
         if split:
             outs = (None, torch.empty(shape, dtype=torch.float32, device=self.device),
@@ -237,7 +241,7 @@ class SrpPlan:
             outs = (torch.empty(shape, dtype=torch.float32, device=self.device), None, None)
         self._main("srpb_lattice_from_spectra", N.ptr(Y), F, Y.shape[1], self.Kb,
                    N.ptr(self.pair_m), N.ptr(self.pair_mp), self.P, wcode, N.ptr(floors),
-                   abs_floor, N.ptr(self.twiddles), self.L, N.ptr(self.off), N.ptr(self.reach),
+                   abs_floor, N.ptr(clean), N.ptr(self.twiddles), self.L, N.ptr(self.off), N.ptr(self.reach),
                    self.T_pad, *(N.ptr(o) for o in outs), s)
         return outs[1:] if split else outs[0]
 

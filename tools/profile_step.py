@@ -32,7 +32,10 @@ def main():
     Y = torch.from_numpy(scene.Y).cuda()
     for path in args.paths.split(","):
         for _ in range(args.reps):
-            plan.run(Y, path)
+            if path == "approx2step":  # unfused K1 -> K3 -> K4
+                plan.approx(plan.lattice(plan.cross_spectra(Y)[0]))
+            else:
+                plan.run(Y, path)
     torch.cuda.synchronize()
     print("ok")
 
