@@ -206,25 +206,31 @@ def roofline_entry(kms, plan, F, J, P, Kb, peaks, path):
 
     Algorithmic work per unit: K4 2*sum(T_p) flops and K2
     4*P*Kb flops per frame.candidate; K3 4*sum(T_p)*Kb flops per frame.
-    Tensor-core kernels are rated against the 3xTF32 rate derived from the
-    measured bf16 peak (TF32 = bf16/2; 3 MMAs per fp32-accurate product).
+    Tensor-core kernels are rated against the fp32-accurate rate derived
+    from the measured bf16 peak: 3xFP16 = fp16 (= bf16) rate / 3 MMAs per
+    product, 3xTF32 = bf16 / 2 (TF32 rate) / 3.
     """
     bf16 = peaks.get("bf16_tflops") or 1590.0
-    tc_peak = bf16 / 2.0 / 3.0
-    names = {"approx": ("srpb_interp_tc", "srpb_interp", "srpb_interp_onthefly"),
-             "conventional": ("srpb_conventional_tc", "srpb_conventional",
-                              "srpb_conventional_general")}[path]
+    names = {"approx": ("srpb_interp_tc16", "srpb_interp_tc", "srpb_interp",
+                        "srpb_interp_onthefly"),
+             "conventional": ("srpb_conventional_tc16", "srpb_conventional_tc",
+                              "srpb_conventional", "srpb_conventional_general")}[path]
     name = next((n for n in names if n in kms), None)
     if name is None:
         return None
     per_unit = 2.0 * plan.total_samples if path == "approx" else 4.0 * P * Kb
     achieved = per_unit * F * J / (kms[name] * 1e-3) / 1e12
-    tc = name.endswith("_tc")
+    tc16 = name.endswith("_tc16")
+    tc = tc16 or name.endswith("_tc")
+    tc_peak = bf16 / 3.0 if tc16 else bf16 / 2.0 / 3.0
+    src = ("measured bf16 burst %.1f TF/s (MEASURED_PEAKS.json; fp16 rate = bf16 rate) / 3 "
+           "(3xFP16 passes)" % bf16) if tc16 else (
+           "measured bf16 burst %.1f TF/s (MEASURED_PEAKS.json) / 2 (TF32 rate) / 3 "
+           "(3xTF32 passes)" % bf16)
     entry = {
         "kernel": name, "bound": "tensor" if tc else "fp32", "achieved": achieved,
         "peak": tc_peak if tc else FP32_NOMINAL_TFLOPS, "unit": "TFLOP/s", "traffic": None,
-        "peak_source": ("measured bf16 burst %.1f TF/s (MEASURED_PEAKS.json) / 2 (TF32 rate) / 3 "
-                        "(3xTF32 passes)" % bf16) if tc else
+        "peak_source": src if tc else
                        "nominal FP32 SIMT 148 SM x 128 lanes x 2 x 1.965 GHz (none measured)",
         "flops_per_unit": per_unit, "units_per_launch": F * J, "kernel_ms": kms[name],
         "kernels_ms": kms,

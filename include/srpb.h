@@ -206,6 +206,36 @@ int srpb_interp_tc(const float* w_hi, const float* w_lo, const float* xi_hi, con
                    int kb_per_group, void* stream);
 
 /*
+ * 3xFP16 operand split: hi = fp16(scale x), lo = fp16(scale x - hi), scale a
+ * power of two keeping |scale x| < 65504 (fp16 has tf32's 11-bit
+ * significand: the split is as exact as the tf32 one).
+ *   x [n] float32; hi, lo [n] fp16 out
+ */
+int srpb_f16_split(const float* x, size_t n, float scale, void* hi, void* lo, void* stream);
+
+/*
+ * K2 on the tensor cores in 3xFP16 (kind::f16, twice the kind::tf32 rate);
+ * same maps as srpb_conventional_tc.  psi_hi/psi_lo [F, 2 P Kb] fp16 split of
+ * Psi prescaled by psi_scale (power of two, |psi_scale psi| < 65504: 2^14 for
+ * PHAT cross-spectra); the steering phases are generated prescaled by 2^14.
+ * Kb % 32 == 0.
+ */
+int srpb_conventional_tc16(const void* psi_hi, const void* psi_lo, float psi_scale, int F, int P,
+                           int Kb, int period, const int32_t* tau_i, const float* tau_f, int J,
+                           float* maps, unsigned long long* keys, int kb_per_group,
+                           void* stream);
+
+/*
+ * K4 on the tensor cores in 3xFP16; same maps as srpb_interp_tc.
+ *   w_hi/w_lo [J, T_pad] fp16 split of W prescaled by w_scale;
+ *   xi_hi/xi_lo [F, T_pad] fp16 split of Xi prescaled by xi_scale
+ *   (powers of two); T_pad % 8 == 0.
+ */
+int srpb_interp_tc16(const void* w_hi, const void* w_lo, float w_scale, const void* xi_hi,
+                     const void* xi_lo, float xi_scale, int F, int J, int T_pad, float* maps,
+                     unsigned long long* keys, int kb_per_group, void* stream);
+
+/*
  * K5 per-frame argmax, lowest index on ties (srp.argmax_candidate,
  * srp.py:107-109) over stored maps [F, J]: folds into keys [F].
  */

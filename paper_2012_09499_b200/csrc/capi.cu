@@ -3,6 +3,7 @@
 #include <cstdarg>
 #include <cstdio>
 
+#include <cmath>
 #include "../../include/srpb.h"
 #include "common.cuh"
 
@@ -38,6 +39,12 @@ cudaError_t launch_conventional_tc(const float*, const float*, int, int, int, in
 cudaError_t launch_interp_tc(const float*, const float*, const float*, const float*, int, int, int,
                              float*, unsigned long long*, int, cudaStream_t);
 cudaError_t launch_tf32_split(const float*, size_t, float*, float*, cudaStream_t);
+cudaError_t launch_f16_split(const float*, size_t, float, void*, void*, cudaStream_t);
+cudaError_t launch_conventional_tc16(const void*, const void*, float, int, int, int, int,
+                                     const int32_t*, const float*, int, float*,
+                                     unsigned long long*, int, cudaStream_t);
+cudaError_t launch_interp_tc16(const void*, const void*, float, const void*, const void*, float,
+                               int, int, int, float*, unsigned long long*, int, cudaStream_t);
 cudaError_t launch_argmax_f64(const double*, int, int, int32_t*, cudaStream_t);
 cudaError_t launch_keys_reset(unsigned long long*, int, cudaStream_t);
 cudaError_t launch_keys_to_index(const unsigned long long*, int, int32_t*, cudaStream_t);
@@ -225,6 +232,48 @@ int srpb_conventional_tc(const float* psi_hi, const float* psi_lo, int F, int P,
   return status(srpb::launch_conventional_tc(psi_hi, psi_lo, F, P, Kb, period, tau_i, tau_f, J,
                                              maps, keys, kb_per_group, S(stream)),
                 "srpb_conventional_tc");
+}
+
+static bool pow2_scale(float s) {
+  int e;
+  return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
+}
+
+int srpb_f16_split(const float* x, size_t n, float scale, void* hi, void* lo, void* stream) {
+  REQUIRE(n == 0 || (x && hi && lo), "srpb_f16_split: null pointer");
+  REQUIRE(pow2_scale(scale), "srpb_f16_split: scale must be a positive power of two");
+  return status(srpb::launch_f16_split(x, n, scale, hi, lo, S(stream)), "srpb_f16_split");
+}
+
+int srpb_conventional_tc16(const void* psi_hi, const void* psi_lo, float psi_scale, int F, int P,
+                           int Kb, int period, const int32_t* tau_i, const float* tau_f, int J,
+                           float* maps, unsigned long long* keys, int kb_per_group,
+                           void* stream) {
+  REQUIRE(F >= 0 && P >= 1 && Kb >= 1 && J >= 0, "srpb_conventional_tc16: bad shape");
+  REQUIRE(Kb % 32 == 0, "srpb_conventional_tc16: Kb must be a multiple of 32, got %d", Kb);
+  REQUIRE(period >= 1 && period <= 46340, "srpb_conventional_tc16: period %d out of range",
+          period);
+  REQUIRE(pow2_scale(psi_scale), "srpb_conventional_tc16: psi_scale must be a power of two");
+  REQUIRE(F == 0 || J == 0 || (psi_hi && psi_lo && tau_i && tau_f),
+          "srpb_conventional_tc16: null pointer");
+  REQUIRE(maps || keys, "srpb_conventional_tc16: need maps and/or keys output");
+  return status(srpb::launch_conventional_tc16(psi_hi, psi_lo, psi_scale, F, P, Kb, period, tau_i,
+                                               tau_f, J, maps, keys, kb_per_group, S(stream)),
+                "srpb_conventional_tc16");
+}
+
+int srpb_interp_tc16(const void* w_hi, const void* w_lo, float w_scale, const void* xi_hi,
+                     const void* xi_lo, float xi_scale, int F, int J, int T_pad, float* maps,
+                     unsigned long long* keys, int kb_per_group, void* stream) {
+  REQUIRE(F >= 0 && J >= 0 && T_pad >= 1, "srpb_interp_tc16: bad shape");
+  REQUIRE(T_pad % 8 == 0, "srpb_interp_tc16: T_pad must be a multiple of 8, got %d", T_pad);
+  REQUIRE(pow2_scale(w_scale) && pow2_scale(xi_scale),
+          "srpb_interp_tc16: scales must be powers of two");
+  REQUIRE(F == 0 || J == 0 || (w_hi && w_lo && xi_hi && xi_lo), "srpb_interp_tc16: null pointer");
+  REQUIRE(maps || keys, "srpb_interp_tc16: need maps and/or keys output");
+  return status(srpb::launch_interp_tc16(w_hi, w_lo, w_scale, xi_hi, xi_lo, xi_scale, F, J, T_pad,
+                                         maps, keys, kb_per_group, S(stream)),
+                "srpb_interp_tc16");
 }
 
 int srpb_interp_tc(const float* w_hi, const float* w_lo, const float* xi_hi, const float* xi_lo,

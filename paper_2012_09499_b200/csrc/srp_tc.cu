@@ -1,4 +1,5 @@
-// Tensor-core (tcgen05, kind::tf32, 3xTF32) SRP contractions for sm_100a.
+// Tensor-core (tcgen05; 3xFP16 kind::f16 or 3xTF32 kind::tf32) SRP
+// contractions for sm_100a.
 //
 //   maps[f, j] = scale * sum_kk A[j, kk] B[f, kk]
 //
@@ -9,9 +10,18 @@
 // K4 (approximate, srp.py:320-347): A = W [J, T_pad] sinc weights, B = Xi
 //    [F, T_pad] lattice samples, both streamed by TMA, scale 1.
 //
-// fp32 accuracy from TF32 tensor cores: every operand is pre-split into
-// hi = tf32(x), lo = tf32(x - hi) and each K step issues three MMAs
-// (lo*hi + hi*lo + hi*hi) into the same TMEM accumulator (residual ~2^-22).
+// fp32 accuracy from 16-bit-significand tensor cores: every operand is
+// pre-split into hi = r(x), lo = r(x - hi) and each K step issues three MMAs
+// (lo*hi + hi*lo + hi*hi) into the same TMEM accumulator (residual ~2^-22;
+// the hi*hi, hi*lo, lo*hi products are exact in fp32).  kF16: r = fp16 with
+// a power-of-two prescale that keeps every operand inside fp16's range
+// (steering phases and sinc weights |x| <= 1 -> 2^14; PHAT cross-spectra
+// |psi| <= 1 -> 2^14; lattice samples |xi| <= 2 Kb); fp16 has tf32's 11-bit
+// significand, so the split is as accurate as 3xTF32, but kind::f16 runs at
+// twice the kind::tf32 rate and moves half the operand bytes.  A 128-byte
+// swizzle row holds 64 fp16 (32 tf32) and each MMA consumes 32 bytes of K in
+// both kinds, so descriptors, stages and TMEM A tiles are byte-identical.
+// Otherwise (identity weighting: unbounded cross-spectra) r = tf32.
 // The tensor core's fp32 accumulation is not round-to-nearest: over a long
 // chain the accumulator drifts toward zero (measured: -1.4e-5 relative after
 // 384 K steps x 3 MMAs at C1).  The contraction is therefore cut into groups
@@ -37,6 +47,7 @@
 //   warps 4..11 epilogue: TMEM drains, map store, fused argmax; for K2 they
 //               also generate the A tiles (2 threads per candidate row)
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 
 #include <cstdlib>
 
@@ -51,19 +62,22 @@ constexpr int kTcThreads = 384;
 constexpr int kTcMaxStages = 4;
 constexpr int kTcM = 128;            // candidate rows per CTA
 constexpr int kTcMaxN = 160;
-constexpr int kTcKBlock = 32;        // fp32 elements per K block = one 128-B swizzle row
+constexpr int kTcKBlock = 32;        // tf32 elements per K block = one 128-B swizzle row
+constexpr int kTcKBlock16 = 64;      // fp16 elements per K block
+constexpr float kF16PhaseScale = 16384.0f;  // 2^14: steering phases / sinc weights
 constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 8;
 constexpr int kABytes = kTcM * 128;  // one of A_hi / A_lo per stage
 
 enum : int { kAFromTma = 0, kAPhase = 1 };
 
-template <int kAMode, bool kPair>
+template <int kAMode, bool kPair, bool kF16>
 struct TcCfg {
   // smem stages: K4 pairs fit 4 x (32 KB A + N/2 rows of B hi/lo); K2 is
   // bounded by its A stages in TMEM (2N + 64 S <= 512)
   static constexpr int kStages = (kAMode == kAFromTma && kPair) ? 4 : 3;
   static constexpr bool kASmem = kAMode == kAFromTma;
+  static constexpr int kKbElems = kF16 ? kTcKBlock16 : kTcKBlock;  // elements per K block
 };
 
 // Instrumentation build only (make prof -> libsrpb_prof.so, tools/tc_probe.py):
@@ -161,58 +175,101 @@ __device__ __forceinline__ void tc_drain(const TcParams& p, TcSmem* bar, bool re
 // (lowest j on ties), then reset the totals for the next tile.  The four
 // lane-quarter warps of a column half combine their warp maxima in shared
 // memory (tile_keys) so each tile issues one global 64-bit atomicMax per
-// frame instead of four.
+// frame instead of four.  Per column a warp issues one streaming 128-byte
+// store (predicated, pointer-increment addressing) and one CREDUX + VOTE for
+// the argmax; full tiles (every row and column valid) take a mask-free path.
+__device__ __forceinline__ void st_cs_pred(float* ptr, float v, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p st.global.cs.f32 [%0], %1;\n}" ::"l"(ptr),
+      "f"(v), "r"(static_cast<uint32_t>(pred))
+      : "memory");
+}
+
+template <bool kFull>
+__device__ __forceinline__ void tc_write_cols(const TcParams& p, unsigned long long* tk, int quarter,
+                                              int cbase, int ncols, int lim, uint32_t jbase,
+                                              int lane, float* ptr,
+                                              const float (&tot)[kTcMaxN / 2]) {
+  // lim: columns valid for this lane (0 when the row is past J)
+  const size_t J = static_cast<size_t>(p.J);
+  TCP_DECL(w_st);
+  TCP_DECL(w_am);
+  if (ptr != nullptr) {
+    TCP_T0();
+#pragma unroll
+    for (int i = 0; i < kTcMaxN / 2; ++i) {
+      if (kFull)
+        __stcs(ptr, tot[i]);
+      else
+        st_cs_pred(ptr, tot[i], i < lim);
+      ptr += J;
+    }
+    TCP_ACC(w_st);
+  }
+  if (p.keys) {
+    TCP_T0();
+    // per column, the warp's best (value, lowest row) as a 64-bit key
+    // (orderable value << 32 | ~j); a 32-column butterfly transpose-reduce
+    // leaves column c of each group in lane c (31 64-bit exchanges per 32
+    // columns instead of a CREDUX + VOTE chain per column)
+    const unsigned long long low = static_cast<unsigned long long>(0xFFFFFFFFu - (jbase + lane));
+#pragma unroll
+    for (int g = 0; g < (kTcMaxN / 2 + 31) / 32; ++g) {
+      if (kFull || 32 * g < ncols) {  // uniform
+        unsigned long long k[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int i = 32 * g + c;
+          k[c] = (i < kTcMaxN / 2 && (kFull || i < lim))
+                     ? (static_cast<unsigned long long>(orderable_bits(tot[i < kTcMaxN / 2 ? i : 0]))
+                        << 32) | low
+                     : 0ull;
+        }
+#pragma unroll
+        for (int o = 16, n = 16; o >= 1; o >>= 1, n >>= 1) {
+          const bool up = lane & o;
+#pragma unroll
+          for (int c = 0; c < n; ++c) {
+            const unsigned long long keep = up ? k[c + n] : k[c];
+            const unsigned long long send = up ? k[c] : k[c + n];
+            const unsigned long long recv = __shfl_xor_sync(0xffffffffu, send, o);
+            k[c] = keep > recv ? keep : recv;
+          }
+        }
+        const int col = 32 * g + lane;
+        if (col < ncols) tk[quarter * kTcMaxN + cbase + col] = k[0];  // 0 = none
+      }
+    }
+    TCP_ACC(w_am);
+  }
+  if (threadIdx.x == kEpiWarp0 * 32) {
+    TCP_FLUSH(14, w_st);
+    TCP_FLUSH(15, w_am);
+  }
+}
+
 __device__ __forceinline__ void tc_write_tile(const TcParams& p, TcSmem* bar, int m0, int n0,
                                               int quarter, int half, int lane,
                                               float (&tot)[kTcMaxN / 2]) {
-  // everything loop-invariant in registers; no per-column branches, so the
-  // compiler can overlap the columns' reduction chains
   const int J = p.J;
-  const int j = m0 + 32 * quarter + lane;
-  const bool jv = j < J;
+  const uint32_t jbase = static_cast<uint32_t>(m0 + 32 * quarter);
+  const int j = static_cast<int>(jbase) + lane;
   const int cbase = half * (p.N / 2);
   const int ncols = p.N / 2;
   const int nv = max(0, min(ncols, p.F - (n0 + cbase)));  // columns with f < F
-  const float scale = p.scale;
-  float* const mcol = p.maps + (static_cast<size_t>(n0 + cbase) * J + j);
-  const bool store = jv && p.maps != nullptr;
+  const int lim = j < J ? nv : 0;
+  float* ptr = p.maps ? p.maps + (static_cast<size_t>(n0 + cbase) * J + j) : nullptr;
   unsigned long long* tk = bar->tile_keys;  // [4 quarters][kTcMaxN columns]
   TCP_DECL(w_loop);
   TCP_DECL(w_flush);
   { TCP_T0();
 #pragma unroll
-  for (int i = 0; i < kTcMaxN / 2; ++i) tot[i] *= scale;
-#pragma unroll
-  for (int i = 0; i < kTcMaxN / 2; ++i)
-    if (store && i < nv) mcol[static_cast<size_t>(i) * J] = tot[i];
-  if (p.keys) {
-    const uint32_t jbase = static_cast<uint32_t>(m0 + 32 * quarter);
-#pragma unroll
-    for (int c0 = 0; c0 < kTcMaxN / 2; c0 += 16) {
-      if (c0 < nv) {
-        uint32_t bits[16], mx[16], hit[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          bits[i] = (jv && c0 + i < nv) ? orderable_bits(tot[c0 + i]) : 0u;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) mx[i] = __reduce_max_sync(0xffffffffu, bits[i]);
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          hit[i] = __ballot_sync(0xffffffffu, bits[i] == mx[i] && bits[i] != 0u);
-        if (lane == 0) {  // this quarter's best per column (0 = none)
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c0 + i < ncols)
-              tk[quarter * kTcMaxN + cbase + c0 + i] =
-                  hit[i] != 0u
-                      ? (static_cast<unsigned long long>(mx[i]) << 32) |
-                            static_cast<unsigned long long>(0xFFFFFFFFu -
-                                                            (jbase + __ffs(hit[i]) - 1))
-                      : 0ull;
-        }
-      }
-    }
-  }
+  for (int i = 0; i < kTcMaxN / 2; ++i) tot[i] *= p.scale;
+  // full: all 80 columns valid for every lane of the warp
+  if (__all_sync(0xffffffffu, lim == kTcMaxN / 2))
+    tc_write_cols<true>(p, tk, quarter, cbase, ncols, lim, jbase, lane, ptr, tot);
+  else
+    tc_write_cols<false>(p, tk, quarter, cbase, ncols, lim, jbase, lane, ptr, tot);
 #pragma unroll
   for (int i = 0; i < kTcMaxN / 2; ++i) tot[i] = 0.0f;
   TCP_ACC(w_loop); }
@@ -243,15 +300,20 @@ __device__ __forceinline__ uint32_t tf32_rna_bits(float x) {
 }
 
 // Steering-phase generator of one A row (candidate j) and one half of every
-// 32-column K block (8 bins).  Per pair: the one-bin and 16-bin rotations
-// e^{j2pi x/N}, e^{j2pi 16x/N} from exact turn arithmetic; per block: the
-// anchor phase, exact (integer-reduced turns + sincospif) every 4th block and
-// otherwise the previous anchor rotated by 16 bins; then 7 one-bin rotations.
-// Longest rotation chain: 3 x 16-bin + 7 x 1-bin, ~1e-6 relative phase error.
+// K block (kBins bins: 8 per 32-column tf32 block, 16 per 64-element fp16
+// block).  Per pair: the one-bin and one-block rotations e^{j2pi x/N},
+// e^{j2pi 2 kBins x/N} from exact turn arithmetic; per block: the anchor
+// phase, exact (integer-reduced turns + sincospif) every 64 bins and
+// otherwise the previous anchor rotated by one block; then kBins - 1 one-bin
+// rotations.  Longest rotation chain ~ 3 block + 15 one-bin rotations, ~1e-6
+// relative phase error.
+template <bool kF16>
 struct PhaseGen {
+  static constexpr int kBins = kF16 ? 16 : 8;                 // bins per half block
+  static constexpr int kAnchorBlocks = 64 / (2 * kBins);     // exact anchor every 64 bins
   int kbp, left;  // K blocks per pair, blocks left in the current pair
   int pair, ti;
-  float tf, sc, ss, s16c, s16s, ac, as;
+  float tf, sc, ss, sbc, sbs, ac, as;
   int since_exact;
 
   __device__ __forceinline__ void start_tile(const TcParams& p) {
@@ -272,17 +334,17 @@ struct PhaseGen {
         tf = p.tau_f[static_cast<size_t>(pair) * p.J + j];
       }
       sincospif(2.0f * (static_cast<float>(ti) + tf) * p.inv_period, &ss, &sc);
-      const float t16 = harmonic_turns(16, ti, tf, p.period, p.mask, p.inv_period);
-      sincospif(2.0f * t16, &s16s, &s16c);
-      since_exact = 4;
+      const float tb = harmonic_turns(2 * kBins, ti, tf, p.period, p.mask, p.inv_period);
+      sincospif(2.0f * tb, &sbs, &sbc);
+      since_exact = kAnchorBlocks;
     }
-    const int k = (kbp - left) * 16 + 8 * half;
-    if (since_exact >= 4) {
+    const int k = (kbp - left) * (2 * kBins) + kBins * half;
+    if (since_exact >= kAnchorBlocks) {
       harmonic_phase(k, ti, tf, p.period, p.mask, p.inv_period, &ac, &as);
       since_exact = 0;
     } else {
-      const float cn = ac * s16c - as * s16s;
-      as = fmaf(ac, s16s, as * s16c);
+      const float cn = ac * sbc - as * sbs;
+      as = fmaf(ac, sbs, as * sbc);
       ac = cn;
     }
     ++since_exact;
@@ -290,13 +352,22 @@ struct PhaseGen {
     float c = ac, s = as;
     uint32_t hi[16], lo[16];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
+    for (int m = 0; m < kBins; ++m) {
       const float ns = -s;
-      const uint32_t hc = tf32_rna_bits(c), hs = tf32_rna_bits(ns);
-      hi[2 * m] = hc;
-      hi[2 * m + 1] = hs;
-      lo[2 * m] = __float_as_uint(c - __uint_as_float(hc));
-      lo[2 * m + 1] = __float_as_uint(ns - __uint_as_float(hs));
+      if constexpr (kF16) {
+        // one 32-bit TMEM column = half2 (cos, -sin) of one bin, prescaled
+        const float xc = c * kF16PhaseScale, xs = ns * kF16PhaseScale;
+        const __half2 h = __floats2half2_rn(xc, xs);
+        const __half2 l = __floats2half2_rn(xc - __low2float(h), xs - __high2float(h));
+        hi[m] = *reinterpret_cast<const uint32_t*>(&h);
+        lo[m] = *reinterpret_cast<const uint32_t*>(&l);
+      } else {
+        const uint32_t hc = tf32_rna_bits(c), hs = tf32_rna_bits(ns);
+        hi[2 * m] = hc;
+        hi[2 * m + 1] = hs;
+        lo[2 * m] = __float_as_uint(c - __uint_as_float(hc));
+        lo[2 * m + 1] = __float_as_uint(ns - __uint_as_float(hs));
+      }
       const float cn = c * sc - s * ss;  // rotate by one bin
       s = fmaf(c, ss, s * sc);
       c = cn;
@@ -306,14 +377,15 @@ struct PhaseGen {
   }
 };
 
-template <int kAMode, bool kPair>
+template <int kAMode, bool kPair, bool kF16>
 __global__ void __launch_bounds__(kTcThreads, 1)
 srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
               const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
               const TcParams p) {
-  using Cfg = TcCfg<kAMode, kPair>;
+  using Cfg = TcCfg<kAMode, kPair, kF16>;
   constexpr int S = Cfg::kStages;
   constexpr bool kASmem = Cfg::kASmem;
+  constexpr int KBE = Cfg::kKbElems;
   constexpr int kCta = kPair ? 2 : 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align by pointer arithmetic on the shared array (keeps the shared
@@ -408,19 +480,19 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
               mbar_expect_tx(&bar->full[s], tx);
             else
               mbar_arrive_cluster_relaxed(fb);
-            tma_load_2d_pair(b_hi(s), &tmB_hi, fb, kb * kTcKBlock, nb);
-            tma_load_2d_pair(b_lo(s), &tmB_lo, fb, kb * kTcKBlock, nb);
+            tma_load_2d_pair(b_hi(s), &tmB_hi, fb, kb * KBE, nb);
+            tma_load_2d_pair(b_lo(s), &tmB_lo, fb, kb * KBE, nb);
             if (kASmem) {
-              tma_load_2d_pair(a_hi(s), &tmA_hi, fb, kb * kTcKBlock, m0);
-              tma_load_2d_pair(a_lo(s), &tmA_lo, fb, kb * kTcKBlock, m0);
+              tma_load_2d_pair(a_hi(s), &tmA_hi, fb, kb * KBE, m0);
+              tma_load_2d_pair(a_lo(s), &tmA_lo, fb, kb * KBE, m0);
             }
           } else {
             mbar_expect_tx(&bar->full[s], tx);
-            tma_load_2d(b_hi(s), &tmB_hi, &bar->full[s], kb * kTcKBlock, nb);
-            tma_load_2d(b_lo(s), &tmB_lo, &bar->full[s], kb * kTcKBlock, nb);
+            tma_load_2d(b_hi(s), &tmB_hi, &bar->full[s], kb * KBE, nb);
+            tma_load_2d(b_lo(s), &tmB_lo, &bar->full[s], kb * KBE, nb);
             if (kASmem) {
-              tma_load_2d(a_hi(s), &tmA_hi, &bar->full[s], kb * kTcKBlock, m0);
-              tma_load_2d(a_lo(s), &tmA_lo, &bar->full[s], kb * kTcKBlock, m0);
+              tma_load_2d(a_hi(s), &tmA_hi, &bar->full[s], kb * KBE, m0);
+              tma_load_2d(a_lo(s), &tmA_lo, &bar->full[s], kb * KBE, m0);
             }
           }
         }
@@ -440,7 +512,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // byte-offset>>4 arithmetic on uniform values; one elected lane issues
     // the MMAs and their commits.
     if (leader) {
-      const uint32_t idesc = idesc_tf32(kTcM * kCta, p.N);
+      const uint32_t idesc = kF16 ? idesc_f16(kTcM * kCta, p.N) : idesc_tf32(kTcM * kCta, p.N);
       const uint64_t db0 = sw128_kmajor_desc(smem_u32(b_hi(0)));  // stage 0 B_hi
       const uint64_t da0 = sw128_kmajor_desc(smem_u32(a_hi(0)));  // stage 0 A_hi (K4)
       const uint32_t stage16 = static_cast<uint32_t>(stage_bytes >> 4);
@@ -474,13 +546,21 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
               const uint64_t ah = da0 + static_cast<uint64_t>(s * stage16);
               const uint64_t al = ah + a16;
 #pragma unroll
-              for (int ks = 0; ks < kTcKBlock / 8; ++ks) {
-                const uint32_t o = 2 * ks;  // 32 bytes along K, in 16-byte units
+              for (int ks = 0; ks < 4; ++ks) {  // 4 MMAs x 32 bytes of K
+                const uint32_t o = 2 * ks;      // in 16-byte units
                 const uint32_t acc0 = (in_group > 0 || ks > 0) ? 1u : 0u;
-                if (kPair) {
+                if constexpr (kPair && kF16) {
+                  mma_f16_pair(d, al + o, bh + o, idesc, acc0);
+                  mma_f16_pair(d, ah + o, bl + o, idesc, 1u);
+                  mma_f16_pair(d, ah + o, bh + o, idesc, 1u);
+                } else if constexpr (kPair) {
                   mma_tf32_pair(d, al + o, bh + o, idesc, acc0);
                   mma_tf32_pair(d, ah + o, bl + o, idesc, 1u);
                   mma_tf32_pair(d, ah + o, bh + o, idesc, 1u);
+                } else if constexpr (kF16) {
+                  mma_f16(d, al + o, bh + o, idesc, acc0);
+                  mma_f16(d, ah + o, bl + o, idesc, 1u);
+                  mma_f16(d, ah + o, bh + o, idesc, 1u);
                 } else {
                   mma_tf32(d, al + o, bh + o, idesc, acc0);
                   mma_tf32(d, ah + o, bl + o, idesc, 1u);
@@ -491,13 +571,21 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
               const uint32_t ah = tmem + static_cast<uint32_t>(tc_a_tmem_col(p.N, s));
               const uint32_t al = ah + 32;
 #pragma unroll
-              for (int ks = 0; ks < kTcKBlock / 8; ++ks) {
+              for (int ks = 0; ks < 4; ++ks) {  // 8 TMEM columns (32 bytes) of K each
                 const uint32_t o = 2 * ks;
                 const uint32_t acc0 = (in_group > 0 || ks > 0) ? 1u : 0u;
-                if (kPair) {
+                if constexpr (kPair && kF16) {
+                  mma_f16_ts_pair(d, al + 8 * ks, bh + o, idesc, acc0);
+                  mma_f16_ts_pair(d, ah + 8 * ks, bl + o, idesc, 1u);
+                  mma_f16_ts_pair(d, ah + 8 * ks, bh + o, idesc, 1u);
+                } else if constexpr (kPair) {
                   mma_tf32_ts_pair(d, al + 8 * ks, bh + o, idesc, acc0);
                   mma_tf32_ts_pair(d, ah + 8 * ks, bl + o, idesc, 1u);
                   mma_tf32_ts_pair(d, ah + 8 * ks, bh + o, idesc, 1u);
+                } else if constexpr (kF16) {
+                  mma_f16_ts(d, al + 8 * ks, bh + o, idesc, acc0);
+                  mma_f16_ts(d, ah + 8 * ks, bl + o, idesc, 1u);
+                  mma_f16_ts(d, ah + 8 * ks, bh + o, idesc, 1u);
                 } else {
                   mma_tf32_ts(d, al + 8 * ks, bh + o, idesc, acc0);
                   mma_tf32_ts(d, ah + 8 * ks, bl + o, idesc, 1u);
@@ -567,7 +655,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       // [16*half, +16) of each 32-column A block
       const int r = 32 * quarter + lane;
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
-      PhaseGen gen;
+      PhaseGen<kF16> gen;
       int kg = 0, s = 0, ph = 0;  // stage ring position
       for (int it = 0; it < my_tiles; ++it) {
         const int j = tile_m0(it) + r;
@@ -637,17 +725,21 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// Row-major fp32 matrix [rows, cols] -> tensor map with a (32 x box_rows)
-// box and 128-byte swizzle (K-major UMMA operand tiles).
-cudaError_t make_map(CUtensorMap* m, const float* base, int rows, int cols, int box_rows) {
+// Row-major fp32 / fp16 matrix [rows, cols] -> tensor map with a 128-byte
+// (32 fp32 or 64 fp16) x box_rows box and 128-byte swizzle (K-major UMMA
+// operand tiles); columns past `cols` read as zero.
+cudaError_t make_map(CUtensorMap* m, const void* base, int rows, int cols, int box_rows,
+                     bool f16) {
   auto fn = encode_fn();
   if (fn == nullptr) return cudaErrorNotSupported;
+  const size_t esz = f16 ? 2 : 4;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * sizeof(float)};
-  cuuint32_t box[2] = {kTcKBlock, static_cast<cuuint32_t>(box_rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * esz};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = fn(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -674,13 +766,13 @@ bool use_pair(int m_tiles, bool default_on) {
   return env == 1 || default_on;
 }
 
-void finish_params(TcParams& p, int kb_per_group, bool pair) {
+void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16) {
   p.N = pick_n(p.F);
   p.n_tiles = (p.F + p.N - 1) / p.N;
   const int m_tiles = (p.J + kTcM - 1) / kTcM;
   const int cta = pair ? 2 : 1;
   p.num_items = p.n_tiles * ((m_tiles + cta - 1) / cta);
-  p.kb_per_group = max(4, kb_per_group);
+  p.kb_per_group = max(f16 ? 2 : 4, kb_per_group);
   p.groups_per_tile = (p.num_kb + p.kb_per_group - 1) / p.kb_per_group;
 }
 
@@ -695,12 +787,12 @@ int num_sms() {
   return n;
 }
 
-template <int kAMode, bool kPair>
+template <int kAMode, bool kPair, bool kF16>
 cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                       const CUtensorMap& bl, const TcParams& p, cudaStream_t stream) {
-  using Cfg = TcCfg<kAMode, kPair>;
+  using Cfg = TcCfg<kAMode, kPair, kF16>;
   const size_t smem = tc_smem_bytes(p.N, Cfg::kASmem, kPair, Cfg::kStages);
-  auto kern = srp_tc_kernel<kAMode, kPair>;
+  auto kern = srp_tc_kernel<kAMode, kPair, kF16>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -725,19 +817,21 @@ cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtens
 
 }  // namespace
 
-cudaError_t launch_conventional_tc(const float* psi_hi, const float* psi_lo, int F, int P, int Kb,
-                                   int period, const int32_t* tau_i, const float* tau_f, int J,
-                                   float* maps, unsigned long long* keys, int kb_per_group,
+// K2: B = psi split (fp32 tf32-split or fp16 prescaled by psi_scale)
+static cudaError_t conventional_tc(const void* psi_hi, const void* psi_lo, bool f16, float psi_scale,
+                                   int F, int P, int Kb, int period, const int32_t* tau_i,
+                                   const float* tau_f, int J, float* maps,
+                                   unsigned long long* keys, int kb_per_group,
                                    cudaStream_t stream) {
   if (F == 0 || J == 0) return cudaSuccess;
   TcParams p{};
   p.F = F;
   p.J = J;
-  p.kb_per_pair = Kb / 16;
+  p.kb_per_pair = Kb / (f16 ? 32 : 16);  // K blocks per pair: 2 Kb elements
   p.num_kb = P * p.kb_per_pair;
   const bool pair = use_pair((J + kTcM - 1) / kTcM, false);
-  finish_params(p, kb_per_group, pair);
-  p.scale = 2.0f;
+  finish_params(p, kb_per_group, pair, f16);
+  p.scale = f16 ? 2.0f / (kF16PhaseScale * psi_scale) : 2.0f;
   p.maps = maps;
   p.keys = keys;
   p.tau_i = tau_i;
@@ -748,35 +842,76 @@ cudaError_t launch_conventional_tc(const float* psi_hi, const float* psi_lo, int
   CUtensorMap bh, bl;
   const int cols = 2 * P * Kb;
   const int brows = pair ? p.N / 2 : p.N;  // B rows per CTA
-  cudaError_t e = make_map(&bh, psi_hi, F, cols, brows);
-  if (e == cudaSuccess) e = make_map(&bl, psi_lo, F, cols, brows);
+  cudaError_t e = make_map(&bh, psi_hi, F, cols, brows, f16);
+  if (e == cudaSuccess) e = make_map(&bl, psi_lo, F, cols, brows, f16);
   if (e != cudaSuccess) return e;
-  return pair ? launch_tc<kAPhase, true>(bh, bl, bh, bl, p, stream)
-              : launch_tc<kAPhase, false>(bh, bl, bh, bl, p, stream);
+  if (f16)
+    return pair ? launch_tc<kAPhase, true, true>(bh, bl, bh, bl, p, stream)
+                : launch_tc<kAPhase, false, true>(bh, bl, bh, bl, p, stream);
+  return pair ? launch_tc<kAPhase, true, false>(bh, bl, bh, bl, p, stream)
+              : launch_tc<kAPhase, false, false>(bh, bl, bh, bl, p, stream);
+}
+
+// K4: A = W split, B = Xi split; maps = (W_hi + W_lo)(Xi_hi + Xi_lo)^T * scale
+static cudaError_t interp_tc(const void* w_hi, const void* w_lo, const void* xi_hi,
+                             const void* xi_lo, bool f16, float scale, int F, int J, int T_pad,
+                             float* maps, unsigned long long* keys, int kb_per_group,
+                             cudaStream_t stream) {
+  if (F == 0 || J == 0) return cudaSuccess;
+  TcParams p{};
+  p.F = F;
+  p.J = J;
+  const int kbe = f16 ? kTcKBlock16 : kTcKBlock;
+  p.num_kb = (T_pad + kbe - 1) / kbe;  // partial last block: TMA zero-fills
+  const bool pair = use_pair((J + kTcM - 1) / kTcM, true);
+  finish_params(p, kb_per_group, pair, f16);
+  p.scale = scale;
+  p.maps = maps;
+  p.keys = keys;
+  CUtensorMap ah, al, bh, bl;
+  const int brows = pair ? p.N / 2 : p.N;
+  cudaError_t e = make_map(&ah, w_hi, J, T_pad, kTcM, f16);
+  if (e == cudaSuccess) e = make_map(&al, w_lo, J, T_pad, kTcM, f16);
+  if (e == cudaSuccess) e = make_map(&bh, xi_hi, F, T_pad, brows, f16);
+  if (e == cudaSuccess) e = make_map(&bl, xi_lo, F, T_pad, brows, f16);
+  if (e != cudaSuccess) return e;
+  if (f16)
+    return pair ? launch_tc<kAFromTma, true, true>(ah, al, bh, bl, p, stream)
+                : launch_tc<kAFromTma, false, true>(ah, al, bh, bl, p, stream);
+  return pair ? launch_tc<kAFromTma, true, false>(ah, al, bh, bl, p, stream)
+              : launch_tc<kAFromTma, false, false>(ah, al, bh, bl, p, stream);
+}
+
+cudaError_t launch_conventional_tc(const float* psi_hi, const float* psi_lo, int F, int P, int Kb,
+                                   int period, const int32_t* tau_i, const float* tau_f, int J,
+                                   float* maps, unsigned long long* keys, int kb_per_group,
+                                   cudaStream_t stream) {
+  return conventional_tc(psi_hi, psi_lo, false, 1.0f, F, P, Kb, period, tau_i, tau_f, J, maps,
+                         keys, kb_per_group, stream);
+}
+
+cudaError_t launch_conventional_tc16(const void* psi_hi, const void* psi_lo, float psi_scale, int F,
+                                     int P, int Kb, int period, const int32_t* tau_i,
+                                     const float* tau_f, int J, float* maps,
+                                     unsigned long long* keys, int kb_per_group,
+                                     cudaStream_t stream) {
+  return conventional_tc(psi_hi, psi_lo, true, psi_scale, F, P, Kb, period, tau_i, tau_f, J, maps,
+                         keys, kb_per_group, stream);
 }
 
 cudaError_t launch_interp_tc(const float* w_hi, const float* w_lo, const float* xi_hi,
                              const float* xi_lo, int F, int J, int T_pad, float* maps,
                              unsigned long long* keys, int kb_per_group, cudaStream_t stream) {
-  if (F == 0 || J == 0) return cudaSuccess;
-  TcParams p{};
-  p.F = F;
-  p.J = J;
-  p.num_kb = T_pad / kTcKBlock;
-  const bool pair = use_pair((J + kTcM - 1) / kTcM, true);
-  finish_params(p, kb_per_group, pair);
-  p.scale = 1.0f;
-  p.maps = maps;
-  p.keys = keys;
-  CUtensorMap ah, al, bh, bl;
-  const int brows = pair ? p.N / 2 : p.N;
-  cudaError_t e = make_map(&ah, w_hi, J, T_pad, kTcM);
-  if (e == cudaSuccess) e = make_map(&al, w_lo, J, T_pad, kTcM);
-  if (e == cudaSuccess) e = make_map(&bh, xi_hi, F, T_pad, brows);
-  if (e == cudaSuccess) e = make_map(&bl, xi_lo, F, T_pad, brows);
-  if (e != cudaSuccess) return e;
-  return pair ? launch_tc<kAFromTma, true>(ah, al, bh, bl, p, stream)
-              : launch_tc<kAFromTma, false>(ah, al, bh, bl, p, stream);
+  return interp_tc(w_hi, w_lo, xi_hi, xi_lo, false, 1.0f, F, J, T_pad, maps, keys, kb_per_group,
+                   stream);
+}
+
+cudaError_t launch_interp_tc16(const void* w_hi, const void* w_lo, float w_scale,
+                               const void* xi_hi, const void* xi_lo, float xi_scale, int F, int J,
+                               int T_pad, float* maps, unsigned long long* keys, int kb_per_group,
+                               cudaStream_t stream) {
+  return interp_tc(w_hi, w_lo, xi_hi, xi_lo, true, 1.0f / (w_scale * xi_scale), F, J, T_pad, maps,
+                   keys, kb_per_group, stream);
 }
 
 // hi = tf32(x), lo = tf32(x - hi): operand split for 3xTF32
@@ -797,6 +932,29 @@ __global__ void tf32_split_kernel(const float4* __restrict__ x, size_t n4, float
     hi[i] = h;
     lo[i] = l;
   }
+}
+
+// hi = fp16(s x), lo = fp16(s x - hi): operand split for 3xFP16 (s a power
+// of two chosen so that |s x| < 65504)
+__global__ void f16_split_kernel(const float* __restrict__ x, size_t n, float scale,
+                                 __half* __restrict__ hi, __half* __restrict__ lo) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x) {
+    const float v = x[i] * scale;
+    const __half h = __float2half_rn(v);
+    hi[i] = h;
+    lo[i] = __float2half_rn(v - __half2float(h));
+  }
+}
+
+cudaError_t launch_f16_split(const float* x, size_t n, float scale, void* hi, void* lo,
+                             cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const size_t want = (n + 255) / 256;
+  const int blocks = static_cast<int>(want < size_t(8 * kNumSMs) ? want : size_t(8 * kNumSMs));
+  f16_split_kernel<<<blocks, 256, 0, stream>>>(x, n, scale, static_cast<__half*>(hi),
+                                               static_cast<__half*>(lo));
+  return cudaGetLastError();
 }
 
 cudaError_t launch_tf32_split(const float* x, size_t n, float* hi, float* lo, cudaStream_t stream) {

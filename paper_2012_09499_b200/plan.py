@@ -77,13 +77,19 @@ class SrpPlan:
     sample_period, n_aux : lattice spacing and guard samples (approximate
         path); ``None`` builds the conventional path only
     weights : ``"auto"`` | ``"stored"`` | ``"onthefly"``
+    precision : tensor-core operand split, ``"auto"`` (3xFP16 wherever the
+        operand bounds are proven -- ``run`` with PHAT weighting -- else
+        3xTF32) or ``"tf32"`` (always 3xTF32)
     """
 
     def __init__(self, tdoa_table, pair_m, pair_mp, tdoa_bounds, bin_frequencies,
                  sample_period=None, n_aux=None, weights="auto", device=None,
                  max_weight_bytes=DEFAULT_MAX_WEIGHT_BYTES, conventional=True, backend="auto",
-                 kb_per_group=4, interp_kb_per_group=10):
+                 kb_per_group=4, interp_kb_per_group=10, precision="auto"):
         self.device = N.require_cuda(device)
+        if precision not in ("auto", "tf32"):
+            raise ValueError(f"precision must be auto|tf32, got {precision!r}")
+        self.precision = precision
         if backend not in ("auto", "simt", "tc"):
             raise ValueError(f"backend must be auto|simt|tc, got {backend!r}")
         self.backend = backend
@@ -93,7 +99,12 @@ class SrpPlan:
         # K4's short K (C2: 19 blocks) folds every 10 (120 steps, ~1.5e-6).
         self.kb_per_group = int(kb_per_group)
         self.interp_kb_per_group = int(interp_kb_per_group)
+        # 3xFP16 blocks hold 64 elements but the same 12 MMA accumulations as
+        # a tf32 block, and the drift grows with accumulations: same periods
+        self.kb_per_group16 = self.kb_per_group
+        self.interp_kb_per_group16 = self.interp_kb_per_group
         self.W_hi = self.W_lo = None
+        self.W16 = None
         table = np.asarray(tdoa_table, dtype=np.float64)
         omega = np.asarray(bin_frequencies, dtype=np.float64)
         if table.ndim != 2 or table.shape[0] == 0:
@@ -280,7 +291,32 @@ class SrpPlan:
                N.stream_handle(self.device))
         return hi, lo
 
-    def conventional(self, psi, maps=True, maps_out=None):
+    # 3xFP16 prescales (powers of two): |phase|, |W|, PHAT |psi| <= 1; PHAT
+    # lattice samples |xi| <= 2 sum_k |psi_k| <= 2 Kb
+    F16_UNIT_SCALE = 2.0 ** 14
+
+    @property
+    def xi_scale16(self):
+        return 2.0 ** math.floor(math.log2(60000.0 / (2.0 * self.Kb)))
+
+    def split_f16(self, x, scale):
+        """(hi, lo) fp16 split of scale * x (float32/complex64 tensor)."""
+        xf = torch.view_as_real(x) if x.is_complex() else x
+        hi = torch.empty(xf.shape, dtype=torch.float16, device=self.device)
+        lo = torch.empty_like(hi)
+        N.call("srpb_f16_split", N.ptr(xf), xf.numel(), float(scale), N.ptr(hi), N.ptr(lo),
+               N.stream_handle(self.device))
+        return hi, lo
+
+    def _f16_ok(self, kind, bounded):
+        """3xFP16 tensor-core path for this contraction?"""
+        if self.precision != "auto" or not bounded:
+            return False
+        if kind == "conv":
+            return self.harmonic and self.Kb % 32 == 0
+        return self.W is not None
+
+    def conventional(self, psi, maps=True, maps_out=None, _bounded=False):
         """K2 (+ fused K5): Psi [F, P, Kb] -> (maps [F, J] fp32 | None,
         argmax [F] int32)."""
         if not self._conv_ready:
@@ -293,7 +329,12 @@ class SrpPlan:
                 (F, self.J), dtype=torch.float32, device=self.device)
         keys = self._keys(F)
         s = N.stream_handle(self.device)
-        if self._use_tc(F, "conv"):
+        if self._use_tc(F, "conv") and self._f16_ok("conv", _bounded):
+            hi, lo = self.split_f16(psi, self.F16_UNIT_SCALE)
+            self._main("srpb_conventional_tc16", N.ptr(hi), N.ptr(lo), self.F16_UNIT_SCALE, F,
+                       self.P, self.Kb, self.period, N.ptr(self.conv_ti), N.ptr(self.conv_tf),
+                       self.J, N.ptr(out), N.ptr(keys), self.kb_per_group16, s)
+        elif self._use_tc(F, "conv"):
             hi, lo = self.split_tf32(psi)
             self._main("srpb_conventional_tc", N.ptr(hi), N.ptr(lo), F, self.P, self.Kb, self.period,
                    N.ptr(self.conv_ti), N.ptr(self.conv_tf), self.J, N.ptr(out), N.ptr(keys),
@@ -342,6 +383,17 @@ class SrpPlan:
                    N.ptr(out), N.ptr(keys), s)
         return out, self.keys_to_index(keys)
 
+    def _approx_tc16(self, xi, out, keys):
+        if self.W16 is None:
+            self.W16 = self.split_f16(self.W, self.F16_UNIT_SCALE)
+        xs = self.xi_scale16
+        xh, xl = self.split_f16(xi, xs)
+        self._main("srpb_interp_tc16", N.ptr(self.W16[0]), N.ptr(self.W16[1]),
+                   self.F16_UNIT_SCALE, N.ptr(xh), N.ptr(xl), xs, xh.shape[0], self.J, self.T_pad,
+                   N.ptr(out), N.ptr(keys), self.interp_kb_per_group16,
+                   N.stream_handle(self.device))
+        return out, self.keys_to_index(keys)
+
     def _approx_tc(self, xh, xl, out, keys):
         if self.W_hi is None:
             self.W_hi, self.W_lo = self.split_tf32(self.W)
@@ -361,16 +413,21 @@ class SrpPlan:
 
     def run(self, Y, path="approx", maps=True, weighting="phat", phat_floor=None):
         """Y [F, M, Kb] complex64 -> (maps | None, argmax) along ``path``.
-        The approximate path fuses K1's cross-spectra into K3."""
+        The approximate path fuses K1's cross-spectra into K3; with PHAT
+        weighting the contractions run in 3xFP16 (bounded operands)."""
+        bounded = weighting == "phat"
         if path == "conventional":
             psi, _ = self.cross_spectra(Y, weighting, phat_floor)
-            return self.conventional(psi, maps)
+            return self.conventional(psi, maps, _bounded=bounded)
         if path == "approx":
             F = Y.shape[0]
             if self.sample_period is not None and self._use_tc(F, "interp"):
-                xh, xl = self.lattice_from_spectra(Y, weighting, phat_floor, split=True)
                 out = torch.empty((F, self.J), dtype=torch.float32,
                                   device=self.device) if maps else None
+                if self._f16_ok("interp", bounded):
+                    xi = self.lattice_from_spectra(Y, weighting, phat_floor)
+                    return self._approx_tc16(xi, out, self._keys(F))
+                xh, xl = self.lattice_from_spectra(Y, weighting, phat_floor, split=True)
                 return self._approx_tc(xh, xl, out, self._keys(F))
             return self.approx(self.lattice_from_spectra(Y, weighting, phat_floor), maps)
         raise ValueError(f"unknown path {path!r}")

@@ -201,6 +201,31 @@ def test_end_to_end_from_stft(path):
     assert list(am.cpu().numpy()) == list(refam)
 
 
+@pytest.mark.parametrize("precision", ["auto", "tf32"])
+@pytest.mark.parametrize("name", ["c1", "c2_subset", "random_small", "on_lattice"])
+def test_run_tensor_core_precisions(name, precision):
+    """Y -> maps through the tensor-core engine in 3xFP16 (PHAT-bounded
+    operands, default) and 3xTF32, both paths, vs the reference."""
+    g = load_golden(name)
+    Y = dev(g["Y"])
+    if g["omega"].size % 32:
+        pytest.skip("3xFP16 conventional kernel needs Kb % 32 == 0")
+    for n_aux in g["n_aux"]:
+        plan = SrpPlan(g["tdoa"], g["pair_m"], g["pair_mp"], g["bounds"], g["omega"],
+                       sample_period=T, n_aux=int(n_aux), weights="stored", backend="tc",
+                       precision=precision)
+        maps, am = plan.run(Y, "approx")
+        assert_maps_match(maps.cpu().numpy(), g[f"approx_{n_aux}"], am.cpu().numpy(),
+                          what=f"{name} n_aux={n_aux} {precision} approx")
+        if name in ("c1", "c2_subset"):
+            assert list(am.cpu().numpy()) == list(g[f"argmax_approx_{n_aux}"])
+    maps, am = plan.run(Y, "conventional")
+    assert_maps_match(maps.cpu().numpy(), g["conv"], am.cpu().numpy(),
+                      what=f"{name} {precision} conventional")
+    if name in ("c1", "c2_subset"):
+        assert list(am.cpu().numpy()) == list(g["argmax_conv"])
+
+
 def test_argmax_only_mode_matches_maps_mode():
     g = load_golden("c2_subset")
     plan = plan_from_golden(g, 4)
