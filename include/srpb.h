@@ -136,14 +136,16 @@ int srpb_lattice(const float* Psi, int F, int P, int Kb, const float* tw, int L,
  *   NULL with abs_floor > 0 (explicit floor); ignored for identity weighting.
  *   clean [F] int32 (srpb_gcc_floor) or NULL (every bin range-tested).
  *   tw 16-byte aligned.
- *   Xi [F, T_pad] float32 out and/or Xi_hi, Xi_lo [F, T_pad]: its tf32
- *   operand split (hi = rna(Xi), lo = rna(Xi - hi)) for srpb_interp_tc.
+ *   Xi [F, T_pad] float32 out and/or Xi_hi, Xi_lo [F, T_pad]: its operand
+ *   split for the tensor-core K4 -- split_scale == 0: tf32 floats
+ *   (hi = rna(Xi), lo = rna(Xi - hi), srpb_interp_tc); split_scale a power
+ *   of two: fp16 of split_scale * Xi (srpb_interp_tc16).
  */
 int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
                               const int32_t* pair_mp, int P, int weighting, const double* floors,
                               double abs_floor, const int32_t* clean, const float* tw, int L,
                               const int32_t* off, const int32_t* reach, int T_pad, float* Xi,
-                              float* Xi_hi, float* Xi_lo, void* stream);
+                              void* Xi_hi, void* Xi_lo, float split_scale, void* stream);
 
 /*
  * Sinc interpolation table W[j, off[p] + n + reach[p]] = sinc(x[j,p] - n),

@@ -21,7 +21,8 @@ from .geometry import (
     tdoa_farfield,
     tdoa_nearfield,
 )
-from .plan import SrpPlan, lattice_layout, standalone_argmax
+from .pipeline import ChunkedRunner, chunk_bounds
+from .plan import CapturedStep, SrpPlan, lattice_layout, standalone_argmax
 from .spectral import (
     DEFAULT_PHAT_FLOOR_REL,
     CrossSpectra,
@@ -53,6 +54,9 @@ from .srp import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "CapturedStep",
+    "ChunkedRunner",
+    "chunk_bounds",
     "CandidateGrid", "MicArray", "MicPair", "build_tdoa_table", "circular_array",
     "enumerate_pairs", "tdoa_farfield", "tdoa_nearfield",
     "SrpPlan", "lattice_layout", "standalone_argmax",

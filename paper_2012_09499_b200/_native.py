@@ -34,7 +34,8 @@ _SIGNATURES = {
                        c_void_p, c_void_p, c_void_p],
     "srpb_lattice_from_spectra": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
                                   c_void_p, c_double, c_void_p, c_void_p, c_int, c_void_p,
-                                  c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p],
+                                  c_void_p, c_int, c_void_p, c_void_p, c_void_p, ctypes.c_float,
+                                  c_void_p],
     "srpb_sinc_table": [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p,
                         c_void_p],
     "srpb_interp": [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],

@@ -15,7 +15,7 @@ cudaError_t launch_gcc_floor(const float*, int, int, int, const int32_t*, const 
 cudaError_t launch_lattice_from_spectra(const float*, int, int, int, const int32_t*,
                                         const int32_t*, int, int, const double*, double,
                                         const int32_t*, const float*, int, const int32_t*,
-                                        const int32_t*, int, int, float*, float*, float*,
+                                        const int32_t*, int, int, float*, void*, void*, float,
                                         cudaStream_t);
 cudaError_t launch_conventional(const float*, int, int, int, int, const int32_t*, const float*,
                                 int, float*, unsigned long long*, cudaStream_t);
@@ -80,7 +80,12 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 extern "C" {
 
-int srpb_abi_version(void) { return 2; }
+static bool pow2_scale(float s) {
+  int e;
+  return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
+}
+
+int srpb_abi_version(void) { return 3; }
 
 const char* srpb_last_error(void) { return g_err; }
 
@@ -159,8 +164,8 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
                               const int32_t* pair_mp, int P, int weighting, const double* floors,
                               double abs_floor, const int32_t* clean, const float* tw, int L,
                               const int32_t* off,
-                              const int32_t* reach, int T_pad, float* Xi, float* Xi_hi,
-                              float* Xi_lo, void* stream) {
+                              const int32_t* reach, int T_pad, float* Xi, void* Xi_hi,
+                              void* Xi_lo, float split_scale, void* stream) {
   REQUIRE(F >= 0 && M >= 1 && P >= 1 && Kb >= 1 && L >= 0 && T_pad >= 1,
           "srpb_lattice_from_spectra: bad shape");
   REQUIRE(weighting == SRPB_WEIGHT_PHAT || weighting == SRPB_WEIGHT_IDENTITY,
@@ -170,6 +175,8 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
   REQUIRE((Xi_hi == nullptr) == (Xi_lo == nullptr),
           "srpb_lattice_from_spectra: Xi_hi and Xi_lo go together");
   REQUIRE(Xi || Xi_hi, "srpb_lattice_from_spectra: need Xi and/or Xi_hi/Xi_lo output");
+  REQUIRE(split_scale == 0.0f || pow2_scale(split_scale),
+          "srpb_lattice_from_spectra: split_scale must be 0 (tf32) or a power of two (fp16)");
   REQUIRE(F == 0 || (Y && pair_m && pair_mp && tw && off && reach),
           "srpb_lattice_from_spectra: null pointer");
   REQUIRE((reinterpret_cast<uintptr_t>(tw) & 15) == 0,
@@ -177,7 +184,7 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
   return status(srpb::launch_lattice_from_spectra(Y, F, M, Kb, pair_m, pair_mp, P, weighting,
                                                   floors, abs_floor, clean, tw, L, off, reach,
                                                   2 * L + 1,
-                                                  T_pad, Xi, Xi_hi, Xi_lo, S(stream)),
+                                                  T_pad, Xi, Xi_hi, Xi_lo, split_scale, S(stream)),
                 "srpb_lattice_from_spectra");
 }
 
@@ -234,10 +241,6 @@ int srpb_conventional_tc(const float* psi_hi, const float* psi_lo, int F, int P,
                 "srpb_conventional_tc");
 }
 
-static bool pow2_scale(float s) {
-  int e;
-  return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
-}
 
 int srpb_f16_split(const float* x, size_t n, float scale, void* hi, void* lo, void* stream) {
   REQUIRE(n == 0 || (x && hi && lo), "srpb_f16_split: null pointer");

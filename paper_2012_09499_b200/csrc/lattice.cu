@@ -14,6 +14,8 @@
 #include "common.cuh"
 #include "umma.cuh"
 
+#include <cuda_fp16.h>
+
 namespace srpb {
 
 __host__ __device__ constexpr int twiddle_stride(int L) { return (L + 1 + 15) / 16 * 16; }
@@ -82,17 +84,25 @@ struct LatticeArgs {
   const int32_t* reach;
   int T_pad;
   float* Xi;     // [F, T_pad] or NULL
-  float* Xi_hi;  // optional tf32 split of Xi for the tensor-core K4 (or NULL)
-  float* Xi_lo;
+  void* Xi_hi;   // optional operand split of Xi for the tensor-core K4 (or NULL):
+  void* Xi_lo;   //   split_scale == 0: tf32 hi/lo floats; else fp16 hi/lo of split_scale * Xi
+  float split_scale;
   int vec16;     // 16-byte copies (Kb even, 16-byte aligned source)
 };
 
 __device__ __forceinline__ void lattice_store(const LatticeArgs& a, size_t idx, float v) {
   if (a.Xi) a.Xi[idx] = v;
   if (a.Xi_hi) {
-    const float h = umma::to_tf32(v);
-    a.Xi_hi[idx] = h;
-    a.Xi_lo[idx] = umma::to_tf32(v - h);
+    if (a.split_scale == 0.0f) {
+      const float h = umma::to_tf32(v);
+      static_cast<float*>(a.Xi_hi)[idx] = h;
+      static_cast<float*>(a.Xi_lo)[idx] = umma::to_tf32(v - h);
+    } else {
+      const float x = v * a.split_scale;
+      const __half h = __float2half_rn(x);
+      static_cast<__half*>(a.Xi_hi)[idx] = h;
+      static_cast<__half*>(a.Xi_lo)[idx] = __float2half_rn(x - __half2float(h));
+    }
   }
 }
 
@@ -339,7 +349,7 @@ cudaError_t launch_lattice(const float* Psi, int F, int P, int Kb, const float* 
   if (F == 0) return cudaSuccess;
   LatticeArgs a{reinterpret_cast<const float2*>(Psi), F, P, Kb, 0, nullptr, nullptr, 1,
                 nullptr, 0.0, nullptr, reinterpret_cast<const float2*>(tw), twiddle_stride(L),
-                off, reach, T_pad, Xi, nullptr, nullptr, Kb % 2 == 0 && aligned16(Psi)};
+                off, reach, T_pad, Xi, nullptr, nullptr, 0.0f, Kb % 2 == 0 && aligned16(Psi)};
   return launch_lattice_args(a, false, max_Tp, stream);
 }
 
@@ -348,13 +358,13 @@ cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, co
                                         const double* floors, double abs_floor,
                                         const int32_t* clean, const float* tw,
                                         int L, const int32_t* off, const int32_t* reach,
-                                        int max_Tp, int T_pad, float* Xi, float* Xi_hi,
-                                        float* Xi_lo, cudaStream_t stream) {
+                                        int max_Tp, int T_pad, float* Xi, void* Xi_hi,
+                                        void* Xi_lo, float split_scale, cudaStream_t stream) {
   if (F == 0) return cudaSuccess;
   LatticeArgs a{reinterpret_cast<const float2*>(Y), F, P, Kb, M, pm, pmp, weighting,
                 weighting == 0 ? floors : nullptr, weighting == 0 ? abs_floor : 0.0,
                 weighting == 0 ? clean : nullptr, reinterpret_cast<const float2*>(tw),
-                twiddle_stride(L), off, reach, T_pad, Xi, Xi_hi, Xi_lo,
+                twiddle_stride(L), off, reach, T_pad, Xi, Xi_hi, Xi_lo, split_scale,
                 Kb % 2 == 0 && aligned16(Y)};
   return launch_lattice_args(a, true, max_Tp, stream);
 }

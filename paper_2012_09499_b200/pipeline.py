@@ -1,0 +1,86 @@
+"""End-to-end host -> device -> host pipeline over frame chunks.
+
+``ChunkedRunner`` splits a batch of F frames into chunks, each with its own
+graph-captured step (``CapturedStep``), and runs chunk c's host->device copy,
+compute and device->host copy on three CUDA streams, so the copy engines
+overlap compute of the neighbouring chunks (the maps' device->host transfer
+of the C2 workload, 62 MB, is the longest leg).  Cross-call dependencies
+keep a chunk's static buffers from being overwritten while the previous call
+still reads them.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native as N
+from .plan import CapturedStep
+
+MIN_CHUNK_FRAMES = 32  # one tensor-core frame tile
+
+
+def chunk_bounds(F: int, chunks: int):
+    chunks = max(1, min(chunks, F // MIN_CHUNK_FRAMES or 1))
+    base, rem = divmod(F, chunks)
+    out, lo = [], 0
+    for c in range(chunks):
+        hi = lo + base + (1 if c < rem else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+class ChunkedRunner:
+    """Pipelined ``plan.run`` over host buffers (pinned for async copies)."""
+
+    def __init__(self, plan, F, M=None, path="approx", chunks=4, maps=True, weighting="phat",
+                 phat_floor=None):
+        self.plan, self.F, self.path, self.want_maps = plan, F, path, maps
+        self.bounds = chunk_bounds(F, chunks)
+        dev = plan.device
+        self.steps = [CapturedStep(plan, hi - lo, M if M is not None else plan.M, path, maps,
+                                   weighting, phat_floor) for lo, hi in self.bounds]
+        self.s_in = torch.cuda.Stream(dev)
+        self.s_comp = torch.cuda.Stream(dev)
+        self.s_out = torch.cuda.Stream(dev)
+        n = len(self.bounds)
+        self.ev_in = [torch.cuda.Event() for _ in range(n)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(n)]
+        self.ev_out = [torch.cuda.Event() for _ in range(n)]
+        self._first = True
+
+    @property
+    def launches(self):
+        """Kernels per call (all chunks)."""
+        return sum(s.launches for s in self.steps)
+
+    def run(self, Y_host, maps_host=None, argmax_host=None):
+        """Enqueue one pass: Y_host [F, M, Kb] complex64 (pinned) -> maps_host
+        [F, J] float32 and argmax_host [F] int32 (pinned).  Asynchronous with
+        respect to the host; the caller's current stream waits for the last
+        device->host copy."""
+        for c, (lo, hi) in enumerate(self.bounds):
+            st = self.steps[c]
+            with torch.cuda.stream(self.s_in):
+                if not self._first:  # previous call's compute has read st.Y
+                    self.s_in.wait_event(self.ev_comp[c])
+                st.Y.copy_(Y_host[lo:hi], non_blocking=True)
+                self.ev_in[c].record(self.s_in)
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(self.ev_in[c])
+                if not self._first:  # previous call's copy-out has read the outputs
+                    self.s_comp.wait_event(self.ev_out[c])
+                st.graph.replay()
+                self.ev_comp[c].record(self.s_comp)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(self.ev_comp[c])
+                if maps_host is not None and st.maps is not None:
+                    maps_host[lo:hi].copy_(st.maps, non_blocking=True)
+                if argmax_host is not None:
+                    argmax_host[lo:hi].copy_(st.argmax, non_blocking=True)
+                self.ev_out[c].record(self.s_out)
+        self._first = False
+        torch.cuda.current_stream(self.plan.device).wait_stream(self.s_out)
+
+
+__all__ = ["ChunkedRunner", "chunk_bounds"]

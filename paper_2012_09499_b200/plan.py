@@ -230,11 +230,18 @@ class SrpPlan:
 
     def lattice_from_spectra(self, Y, weighting="phat", phat_floor=None, split=False):
         """K1a + fused K1b/K3: ``Y`` [F, M, Kb] -> Xi [F, T_pad] fp32, or its
-        tf32 split (Xi_hi, Xi_lo) with ``split=True``; the cross-spectra are
-        formed inside the lattice kernel and never stored."""
+        tensor-core operand split (Xi_hi, Xi_lo): ``split=True`` / ``"tf32"``
+        tf32 floats, ``"f16"`` fp16 of ``xi_scale16 * Xi`` (PHAT only).  The
+        cross-spectra are formed inside the lattice kernel and never stored."""
         if self.sample_period is None:
             raise ValueError("plan was built without a lattice (sample_period)")
         F, wcode, abs_floor = self._check_spectra(Y, weighting, phat_floor)
+        if split is True:
+            split = "tf32"
+        if split not in (False, "tf32", "f16"):
+            raise ValueError(f"split must be False|'tf32'|'f16', got {split!r}")
+        if split == "f16" and wcode != 0:
+            raise ValueError("the fp16 split needs PHAT-bounded lattice samples")
         s = N.stream_handle(self.device)
         floors = clean = None
         if wcode == 0:  # K1a: relative floors and per-frame range flags
@@ -245,15 +252,18 @@ class SrpPlan:
                        N.ptr(self.pair_mp), self.P, DEFAULT_PHAT_FLOOR_REL, N.ptr(floors),
                        N.ptr(clean), s)
         shape = (F, self.T_pad)
+        scale = 0.0
         if split:
-            outs = (None, torch.empty(shape, dtype=torch.float32, device=self.device),
-                    torch.empty(shape, dtype=torch.float32, device=self.device))
+            dt = torch.float16 if split == "f16" else torch.float32
+            outs = (None, torch.empty(shape, dtype=dt, device=self.device),
+                    torch.empty(shape, dtype=dt, device=self.device))
+            scale = self.xi_scale16 if split == "f16" else 0.0
         else:
             outs = (torch.empty(shape, dtype=torch.float32, device=self.device), None, None)
         self._main("srpb_lattice_from_spectra", N.ptr(Y), F, Y.shape[1], self.Kb,
                    N.ptr(self.pair_m), N.ptr(self.pair_mp), self.P, wcode, N.ptr(floors),
-                   abs_floor, N.ptr(clean), N.ptr(self.twiddles), self.L, N.ptr(self.off), N.ptr(self.reach),
-                   self.T_pad, *(N.ptr(o) for o in outs), s)
+                   abs_floor, N.ptr(clean), N.ptr(self.twiddles), self.L, N.ptr(self.off),
+                   N.ptr(self.reach), self.T_pad, *(N.ptr(o) for o in outs), float(scale), s)
         return outs[1:] if split else outs[0]
 
     def _use_tc(self, F, kind):
@@ -383,11 +393,11 @@ class SrpPlan:
                    N.ptr(out), N.ptr(keys), s)
         return out, self.keys_to_index(keys)
 
-    def _approx_tc16(self, xi, out, keys):
+    def _approx_tc16(self, xh, xl, out, keys):
+        """K4 in 3xFP16 from the fp16 split of xi_scale16 * Xi."""
         if self.W16 is None:
             self.W16 = self.split_f16(self.W, self.F16_UNIT_SCALE)
         xs = self.xi_scale16
-        xh, xl = self.split_f16(xi, xs)
         self._main("srpb_interp_tc16", N.ptr(self.W16[0]), N.ptr(self.W16[1]),
                    self.F16_UNIT_SCALE, N.ptr(xh), N.ptr(xl), xs, xh.shape[0], self.J, self.T_pad,
                    N.ptr(out), N.ptr(keys), self.interp_kb_per_group16,
@@ -425,12 +435,18 @@ class SrpPlan:
                 out = torch.empty((F, self.J), dtype=torch.float32,
                                   device=self.device) if maps else None
                 if self._f16_ok("interp", bounded):
-                    xi = self.lattice_from_spectra(Y, weighting, phat_floor)
-                    return self._approx_tc16(xi, out, self._keys(F))
+                    xh, xl = self.lattice_from_spectra(Y, weighting, phat_floor, split="f16")
+                    return self._approx_tc16(xh, xl, out, self._keys(F))
                 xh, xl = self.lattice_from_spectra(Y, weighting, phat_floor, split=True)
                 return self._approx_tc(xh, xl, out, self._keys(F))
             return self.approx(self.lattice_from_spectra(Y, weighting, phat_floor), maps)
         raise ValueError(f"unknown path {path!r}")
+
+    def capture(self, F, M=None, path="approx", maps=True, weighting="phat", phat_floor=None):
+        """Capture ``run`` for F frames of M channels into a CUDA graph
+        (``CapturedStep``: static input ``Y``, ``replay()``)."""
+        return CapturedStep(self, F, M if M is not None else self.M, path, maps, weighting,
+                            phat_floor)
 
 
 def standalone_argmax(maps: torch.Tensor) -> torch.Tensor:
@@ -447,3 +463,42 @@ def standalone_argmax(maps: torch.Tensor) -> torch.Tensor:
     idx = torch.empty(F, dtype=torch.int32, device=maps.device)
     N.call("srpb_keys_to_index", N.ptr(keys), F, N.ptr(idx), s)
     return idx
+
+
+class CapturedStep:
+    """One ``SrpPlan.run`` step captured in a CUDA graph.
+
+    The step's kernels (K1a floor, fused K1b/K3 lattice, K4/K2 tensor-core
+    contraction with the fused argmax, argmax key reset/decode) replay with a
+    single graph launch, so host-side work (argument marshalling, tensor-map
+    encoding) leaves the critical path.  ``Y`` is the static input buffer;
+    ``maps`` / ``argmax`` the static outputs, overwritten by each replay.
+    """
+
+    def __init__(self, plan, F, M, path="approx", maps=True, weighting="phat", phat_floor=None):
+        dev = plan.device
+        self.plan, self.path = plan, path
+        self.Y = torch.zeros((F, M, plan.Kb), dtype=torch.complex64, device=dev)
+        timer, plan.kernel_timer = plan.kernel_timer, None
+        try:
+            # warm-up outside capture: lazily built operands (fp16 W split),
+            # kernel attributes, allocator pools
+            plan.run(self.Y, path, maps, weighting, phat_floor)
+            torch.cuda.synchronize(dev)
+            self.graph = torch.cuda.CUDAGraph()
+            n0 = N.launch_count()
+            with torch.cuda.graph(self.graph):
+                self.maps, self.argmax = plan.run(self.Y, path, maps, weighting, phat_floor)
+            #: kernels launched by one replay
+            self.launches = N.launch_count() - n0
+        finally:
+            plan.kernel_timer = timer
+
+    def replay(self, Y=None):
+        """Run the step (on the current stream); ``Y`` (optional) is copied
+        into the static input first.  Returns the static (maps, argmax)."""
+        if Y is not None:
+            self.Y.copy_(Y, non_blocking=True)
+        self.graph.replay()
+        return self.maps, self.argmax
+

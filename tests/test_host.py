@@ -38,7 +38,7 @@ def test_library_exports_every_header_symbol():
 
 def test_abi_version_and_error_reporting_without_gpu():
     lib = _native.load()
-    assert lib.srpb_abi_version() == 2
+    assert lib.srpb_abi_version() == 3
     # invalid arguments are rejected on the host before any CUDA call
     with pytest.raises(ValueError, match="bad shape"):
         _native.call("srpb_gcc_phat", None, -1, 4, 64, None, None, 6, 0, 1e-12, -1.0, None, None,
@@ -216,3 +216,13 @@ def test_scene_shapes_match_baseline_configs():
     assert c5.Y.shape == (2, 8, 512) and c5.Y.dtype == np.complex64
     # seeded: identical on regeneration
     assert np.array_equal(scenes.make_c1(num_frames=2).Y, scenes.make_c1(num_frames=2).Y)
+
+
+def test_chunk_bounds():
+    from paper_2012_09499_b200.pipeline import chunk_bounds
+
+    assert chunk_bounds(311, 4) == [(0, 78), (78, 156), (156, 234), (234, 311)]
+    assert chunk_bounds(40, 4) == [(0, 40)]  # chunks keep >= 32 frames
+    assert chunk_bounds(100, 3) == [(0, 34), (34, 67), (67, 100)]
+    b = chunk_bounds(1000, 7)
+    assert b[0][0] == 0 and b[-1][1] == 1000 and all(x[1] == y[0] for x, y in zip(b, b[1:]))

@@ -226,6 +226,31 @@ def test_run_tensor_core_precisions(name, precision):
         assert list(am.cpu().numpy()) == list(g["argmax_conv"])
 
 
+def test_captured_step_and_chunked_runner_match_eager():
+    """CUDA-graph replay (CapturedStep) and the 3-stream chunked host
+    pipeline give bitwise the same maps/argmax as the eager plan.run."""
+    g = load_golden("c2_subset")
+    Y = np.concatenate([g["Y"]] * 40)  # 120 frames: 3 chunks of >= 32
+    plan = plan_from_golden(g, 4, weights="stored", backend="tc")
+    for path in ("approx", "conventional"):
+        ref_maps, ref_am = plan.run(dev(Y), path)
+        cap = plan.capture(Y.shape[0], Y.shape[1], path)
+        m, a = cap.replay(dev(Y))
+        assert cap.launches >= 3
+        assert torch.equal(m, ref_maps) and torch.equal(a, ref_am)
+        m2, a2 = cap.replay()  # replays are repeatable
+        assert torch.equal(m2, ref_maps) and torch.equal(a2, ref_am)
+        runner = B.ChunkedRunner(plan, Y.shape[0], Y.shape[1], path, chunks=3)
+        assert len(runner.bounds) == 3
+        Yh = torch.from_numpy(Y).pin_memory()
+        mh = torch.empty(tuple(ref_maps.shape), dtype=torch.float32).pin_memory()
+        ah = torch.empty(Y.shape[0], dtype=torch.int32).pin_memory()
+        for _ in range(2):  # back-to-back calls reuse the static buffers safely
+            runner.run(Yh, mh, ah)
+        torch.cuda.synchronize()
+        assert torch.equal(mh, ref_maps.cpu()) and torch.equal(ah, ref_am.cpu())
+
+
 def test_argmax_only_mode_matches_maps_mode():
     g = load_golden("c2_subset")
     plan = plan_from_golden(g, 4)
