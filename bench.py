@@ -238,6 +238,15 @@ def roofline_entry(kms, plan, F, J, P, Kb, peaks, path):
         "kernels_ms": kms,
     }
     entry["frac"] = achieved / entry["peak"]
+    # DRAM bytes per launch from the committed ncu --set full capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+            tr = json.load(fh)
+        if name in tr:
+            entry["traffic"] = tr[name]
+            entry["traffic_unit"] = "bytes/launch (profiles/r1_traffic.json)"
+    except (OSError, ValueError):
+        pass
     return entry
 
 
