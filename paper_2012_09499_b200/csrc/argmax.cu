@@ -18,25 +18,39 @@ argmax_kernel(const float* __restrict__ maps, int J, int slice, unsigned long lo
   const int j_begin = blockIdx.x * slice;
   const int j_end = min(J, j_begin + slice);
   const float* row = maps + static_cast<size_t>(f) * J;
-  unsigned long long best = 0ull;
+  // per thread: best orderable bits and its (lowest, ascending scan) index;
+  // strict > keeps the first maximum; keys combine across threads
+  uint32_t bb = 0u;
+  int bj = 0;
   // scalar head until 16-byte alignment of the row pointer
   int j = j_begin;
   while (j < j_end && (reinterpret_cast<uintptr_t>(row + j) & 15u) != 0) {
-    if (threadIdx.x == 0) best = key_max(best, make_key(row[j], j));
+    if (threadIdx.x == 0) {
+      const uint32_t b = orderable_bits(row[j]);
+      if (b > bb) { bb = b; bj = j; }
+    }
     ++j;
   }
   const int nvec = (j_end - j) / 4;
   const float4* v4 = reinterpret_cast<const float4*>(row + j);
+#pragma unroll 4
   for (int e = threadIdx.x; e < nvec; e += blockDim.x) {
-    const float4 v = v4[e];
+    const float4 v = __ldcs(v4 + e);
     const int jj = j + 4 * e;
-    best = key_max(best, make_key(v.x, jj));
-    best = key_max(best, make_key(v.y, jj + 1));
-    best = key_max(best, make_key(v.z, jj + 2));
-    best = key_max(best, make_key(v.w, jj + 3));
+    const uint32_t b0 = orderable_bits(v.x), b1 = orderable_bits(v.y);
+    const uint32_t b2 = orderable_bits(v.z), b3 = orderable_bits(v.w);
+    if (b0 > bb) { bb = b0; bj = jj; }
+    if (b1 > bb) { bb = b1; bj = jj + 1; }
+    if (b2 > bb) { bb = b2; bj = jj + 2; }
+    if (b3 > bb) { bb = b3; bj = jj + 3; }
   }
-  for (int jj = j + 4 * nvec + threadIdx.x; jj < j_end; jj += blockDim.x)
-    best = key_max(best, make_key(row[jj], jj));
+  for (int jj = j + 4 * nvec + threadIdx.x; jj < j_end; jj += blockDim.x) {
+    const uint32_t b = orderable_bits(row[jj]);
+    if (b > bb) { bb = b; bj = jj; }
+  }
+  unsigned long long best =
+      bb != 0u ? (static_cast<unsigned long long>(bb) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(bj))
+               : 0ull;
   best = warp_key_max(best);
   __shared__ unsigned long long s_best[kArgThreads / 32];
   if ((threadIdx.x & 31) == 0) s_best[threadIdx.x >> 5] = best;
@@ -95,8 +109,8 @@ __global__ void keys_to_index_kernel(const unsigned long long* __restrict__ keys
 cudaError_t launch_argmax(const float* maps, int F, int J, unsigned long long* keys,
                           cudaStream_t stream) {
   if (F == 0 || J == 0) return cudaSuccess;
-  // about 4 CTAs per SM in total, slices of >= 4096 candidates
-  int slices = (4 * kNumSMs + F - 1) / F;
+  // about 8 CTAs per SM in total, slices of >= 4096 candidates
+  int slices = (8 * kNumSMs + F - 1) / F;
   int slice = (J + slices - 1) / slices;
   slice = max(4096, (slice + 3) & ~3);
   slices = (J + slice - 1) / slice;

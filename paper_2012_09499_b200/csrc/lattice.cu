@@ -12,6 +12,7 @@
 //
 // Roofline: FP32 pipe, 4 sum_p T_p Kb flops per frame.
 #include "common.cuh"
+#include "tmap.cuh"
 #include "umma.cuh"
 
 #include <cuda_fp16.h>
@@ -62,10 +63,28 @@ constexpr int kLatStages = 4;
 constexpr int kLatRow = 36;      // float4 per raw row (32 frames; 36 = 4 mod 8: conflict-free copies)
 constexpr int kLatRaw = 2 * (kLatBinsW / 2) * kLatRow;  // float4: [ch][pair][f]
 constexpr int kLatTwW = kLatBinsW * kLatHl / 2;          // float4: [bin][h/2]
-constexpr int kLatStageW = kLatRaw + kLatTwW;            // float4 per warp stage
-constexpr size_t kLatSmemBytes = sizeof(float4) * kLatWarps * kLatStages * kLatStageW;
-static_assert(sizeof(float4) * kLatWarps * kLatStages * kLatStageW >=
-                  sizeof(float) * kLatWarps * 2 * kLatHl * kLatF,
+constexpr int kLatStageW = kLatRaw + kLatTwW;            // float4 per cp.async warp stage
+// psi rows: per bin, FG/2 planes of 32/FG frame pairs; planes padded by 64
+// bytes so the two planes' 8-byte stores land on different banks
+constexpr int kPsiRow = 48;                               // float2 per bin row
+constexpr int kLatPsiW = kLatBinsW * kPsiRow;             // float2: one chunk's psi rows
+// TMA staging: per stage [raw_a 32 frames x 4 bins][raw_b][tw 4 bins x 16] in bytes
+constexpr int kTmaRaw = 32 * 4 * 8;            // 1024 B per channel tile (32-byte rows, SW32)
+constexpr int kTmaTwOff = 2 * kTmaRaw;         // 2048
+constexpr int kTmaStageBytes = kTmaTwOff + 4 * kLatHl * 8;  // 2560
+static_assert(kTmaStageBytes % 256 == 0, "stages keep the 32B-swizzle alignment");
+
+// shared-memory geometry of the two staging variants
+template <bool kTma>
+struct LatGeom {
+  static constexpr int kStageW = kTma ? kTmaStageBytes / 16 : kLatStageW;  // float4 per stage
+  static constexpr int kRing = kLatWarps * kLatStages * kStageW;            // float4, all warps
+  static constexpr size_t kSmem = 1024 /* alignment slack */ + sizeof(float4) * kRing +
+                                  sizeof(float2) * kLatWarps * 2 * kLatPsiW +  // double buffered
+                                  sizeof(uint64_t) * kLatWarps * kLatStages;   // TMA barriers
+};
+static_assert(sizeof(float4) * kLatWarps * kLatStages * (kTmaStageBytes / 16) >=
+                  sizeof(float) * kLatWarps * 2 * kLatHl * 32,
               "reduction buffer aliases the stages");
 static_assert(kLatTwW == 32 && kLatBinsW == 4, "copy mapping: one twiddle float4 per lane");
 
@@ -125,16 +144,59 @@ __device__ __forceinline__ void cp_async_wait() {
 // one warp's view of the CTA: its K-slice, its ring, its copy sources
 struct LatticeWarp {
   float4* ring;             // [stage][kLatStageW]
-  const float2* src[2][2];  // [ch][half]: row of frame (lane/2 + 16 half), clamped
-  const float2* twsrc;      // this lane's twiddle column window at bin 0
+  const float2* src[2][2];  // [ch][half]: row of frame (lane/2 + 16 half), clamped (cp.async)
+  const float2* twsrc;      // this lane's twiddle column window at bin 0 (cp.async)
   int nch, kbase;           // channels staged; first bin of the slice in chunk 0
+  uint64_t* full;           // [stage] TMA completion barriers of this warp
+  int row_c[2];             // TMA: channel (Y) or pair (Psi) coordinate per staged row set
+  int f0, hl0;
+  const CUtensorMap* tm_src;
+  const CUtensorMap* tm_tw;
 };
+
+// TMA staging of chunk c into stage st: lane 0 issues the channel tiles
+// (32 frames x 4 bins, 32-byte rows, 32-byte swizzle) and the twiddle window
+// (4 bins x 16 half-lags); out-of-range frames / bins are zero-filled
+template <int kNch>
+__device__ __forceinline__ void lattice_issue_tma(const LatticeWarp& w, int c, int st) {
+  // warp-uniform operands, one elected lane issues (no per-issue register
+  // broadcasts into the uniform datapath)
+  uint8_t* base = reinterpret_cast<uint8_t*>(w.ring + st * LatGeom<true>::kStageW);
+  const int k0 = c * kLatChunk + w.kbase;
+  if (umma::elect_one()) {
+    umma::fence_proxy_async_smem();  // generic reads of this stage precede the async writes
+    umma::mbar_expect_tx(&w.full[st], kNch * kTmaRaw + 4 * kLatHl * 8);
+#pragma unroll
+    for (int ch = 0; ch < kNch; ++ch)
+      umma::tma_load_3d(base + ch * kTmaRaw, w.tm_src, &w.full[st], k0, w.row_c[ch], w.f0);
+    umma::tma_load_2d(base + kTmaTwOff, w.tm_tw, &w.full[st], w.hl0, k0);
+  }
+  __syncwarp();
+}
+
+// raw value (two bins 2pr, 2pr+1 of frame f, channel ch) of a stage
+template <bool kTma>
+__device__ __forceinline__ float4 lattice_raw(const float4* stage, int ch, int pr, int f) {
+  if constexpr (kTma) {
+    // 32-byte swizzle: the 16-byte chunk index flips with bit 7 of the address
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(stage) + ch * kTmaRaw + f * 32 +
+                       ((pr ^ ((f >> 2) & 1)) << 4);
+    return *reinterpret_cast<const float4*>(b);
+  } else {
+    return stage[(ch * 2 + pr) * kLatRow + f];
+  }
+}
+template <bool kTma>
+__device__ __forceinline__ const float2* lattice_tw(const float4* stage) {
+  return kTma ? reinterpret_cast<const float2*>(reinterpret_cast<const uint8_t*>(stage) + kTmaTwOff)
+              : reinterpret_cast<const float2*>(stage + kLatRaw);
+}
 
 template <int kNch>
 __device__ __forceinline__ void lattice_issue(const LatticeArgs& a, const LatticeWarp& w, int c,
                                               int st) {
   const int lane = threadIdx.x & 31;
-  float4* base = w.ring + st * kLatStageW;
+  float4* base = w.ring + st * LatGeom<false>::kStageW;
   const int k0 = c * kLatChunk + w.kbase;
   // raw: lane -> (bin pair pr = lane & 1, frame lane/2 + 16 half)
   const int pr = lane & 1;
@@ -157,67 +219,144 @@ __device__ __forceinline__ void lattice_issue(const LatticeArgs& a, const Lattic
   cp_async16(base + kLatRaw + lane, w.twsrc + static_cast<size_t>(kt) * a.Hs);
 }
 
-template <int HL>
-__device__ __forceinline__ void lattice_bin(float2 v, const float4* trow, float (&A)[kLatHl],
-                                            float (&B)[kLatHl]) {
-#pragma unroll
-  for (int q = 0; q < HL / 2; ++q) {
-    const float4 t = trow[q];  // (c, s) of half-lags 2q, 2q+1
-    A[2 * q] = fmaf(v.x, t.x, A[2 * q]);
-    B[2 * q] = fmaf(v.y, t.y, B[2 * q]);
-    A[2 * q + 1] = fmaf(v.x, t.z, A[2 * q + 1]);
-    B[2 * q + 1] = fmaf(v.y, t.w, B[2 * q + 1]);
-  }
+// Compute tiling: each lane owns FG frames x HG half-lags (HL = FG * HG per
+// CTA, (32 / FG) frame groups x FG half-lag groups = 32 lanes), so per bin a
+// lane loads FG psi values (FG/2 LDS.128) and HG twiddles (2 LDS.128 or 3
+// LDS.64) for 2 * FG * HG FFMA -- the shared-memory issue rate no longer
+// bounds the loop.  Each lane still forms exactly one psi per bin (its own
+// frame = lane) and shares it through a per-warp buffer laid out
+// psi_w[bin][plane][frame group][2] so the LDS.128 of a frame pair is
+// conflict-free.
+template <int FG>
+__device__ __forceinline__ int psi_slot(int f) {  // float2 offset of frame f in a bin row
+  constexpr int NFG = 32 / FG;
+  return ((f % FG) >> 1) * (2 * NFG + 8) + (f / FG) * 2 + (f & 1);
 }
 
-template <int kMode, int HL>
-__device__ __forceinline__ void lattice_body(const LatticeArgs& a, const LatticeWarp& w,
-                                             PhatFloor fl, float (&A)[kLatHl],
-                                             float (&B)[kLatHl]) {
-  constexpr int kNch = kMode == kPsiStaged ? 1 : 2;
+// psi of this lane's frame for the warp's 4 bins of chunk c -> psi_w row set
+template <int kMode, int kNch, bool kTma>
+__device__ __forceinline__ void lattice_psi(const LatticeArgs& a, const LatticeWarp& w, int c,
+                                            float2* psi_dst, int my_slot, PhatFloor fl) {
   const int lane = threadIdx.x & 31;
-  const int n = (a.Kb + kLatChunk - 1) / kLatChunk;
+  const float4* stage = w.ring + (c % kLatStages) * LatGeom<kTma>::kStageW;
+  const int kvalid = a.Kb - (c * kLatChunk + w.kbase);  // bins of the slice inside Kb
 #pragma unroll
-  for (int c = 0; c < kLatStages - 1; ++c) {
-    if (c < n) lattice_issue<kNch>(a, w, c, c);
-    cp_async_commit();
-  }
-  for (int c = 0; c < n; ++c) {
-    cp_async_wait<kLatStages - 2>();  // this lane's copies of chunk c landed
-    __syncwarp();                     // the warp's; stage (c-1)%S is free
-    if (c + kLatStages - 1 < n)
-      lattice_issue<kNch>(a, w, c + kLatStages - 1, (c + kLatStages - 1) % kLatStages);
-    cp_async_commit();
-    const float4* stage = w.ring + (c % kLatStages) * kLatStageW;
-    const int kvalid = a.Kb - (c * kLatChunk + w.kbase);  // bins of the slice inside Kb
-#pragma unroll
-    for (int pr = 0; pr < kLatBinsW / 2; ++pr) {
-      const float4 ra = stage[pr * kLatRow + lane];
-      const float4 rb = kNch == 2 ? stage[(2 + pr) * kLatRow + lane] : ra;
-      float2 v0 = psi_warp<kMode>(make_float2(ra.x, ra.y), make_float2(rb.x, rb.y), fl);
-      float2 v1 = psi_warp<kMode>(make_float2(ra.z, ra.w), make_float2(rb.z, rb.w), fl);
-      if (2 * pr >= kvalid) v0 = make_float2(0.0f, 0.0f);  // clamped copies past Kb
+  for (int pr = 0; pr < kLatBinsW / 2; ++pr) {
+    const float4 ra = lattice_raw<kTma>(stage, 0, pr, lane);
+    const float4 rb = kNch == 2 ? lattice_raw<kTma>(stage, 1, pr, lane) : ra;
+    float2 v0 = psi_warp<kMode>(make_float2(ra.x, ra.y), make_float2(rb.x, rb.y), fl);
+    float2 v1 = psi_warp<kMode>(make_float2(ra.z, ra.w), make_float2(rb.z, rb.w), fl);
+    if (!kTma) {  // clamped copies past Kb (TMA zero-fills them, twiddles included)
+      if (2 * pr >= kvalid) v0 = make_float2(0.0f, 0.0f);
       if (2 * pr + 1 >= kvalid) v1 = make_float2(0.0f, 0.0f);
-      const float4* tw = stage + kLatRaw + (2 * pr) * (kLatHl / 2);
-      lattice_bin<HL>(v0, tw, A, B);
-      lattice_bin<HL>(v1, tw + kLatHl / 2, A, B);
     }
+    psi_dst[(2 * pr) * kPsiRow + my_slot] = v0;
+    psi_dst[(2 * pr + 1) * kPsiRow + my_slot] = v1;
   }
-  cp_async_wait<0>();
 }
 
-template <int HL>
+// FFMA of chunk c: FG frames x HG half-lags per lane, 4 bins
+template <int FG, int HG, bool kTma>
+__device__ __forceinline__ void lattice_fma(const LatticeWarp& w, int c, const float2* psi_src,
+                                            int fgi, int hgi, float (&A)[FG * HG],
+                                            float (&B)[FG * HG]) {
+  const float2* twb = lattice_tw<kTma>(w.ring + (c % kLatStages) * LatGeom<kTma>::kStageW);
+#pragma unroll
+  for (int b = 0; b < kLatBinsW; ++b) {
+    float2 v[FG];
+#pragma unroll
+    for (int q = 0; q < FG / 2; ++q) {
+      const float4 t = *reinterpret_cast<const float4*>(psi_src + b * kPsiRow +
+                                                        q * (2 * (32 / FG) + 8) + fgi * 2);
+      v[2 * q] = make_float2(t.x, t.y);
+      v[2 * q + 1] = make_float2(t.z, t.w);
+    }
+    float2 t[HG];
+    const float2* trow = twb + b * kLatHl + HG * hgi;
+    if constexpr (HG == 4) {
+      const float4 t01 = *reinterpret_cast<const float4*>(trow);
+      const float4 t23 = *reinterpret_cast<const float4*>(trow + 2);
+      t[0] = make_float2(t01.x, t01.y);
+      t[1] = make_float2(t01.z, t01.w);
+      t[2] = make_float2(t23.x, t23.y);
+      t[3] = make_float2(t23.z, t23.w);
+    } else {
+#pragma unroll
+      for (int j = 0; j < HG; ++j) t[j] = trow[j];
+    }
+#pragma unroll
+    for (int i = 0; i < FG; ++i)
+#pragma unroll
+      for (int j = 0; j < HG; ++j) {
+        A[i * HG + j] = fmaf(v[i].x, t[j].x, A[i * HG + j]);
+        B[i * HG + j] = fmaf(v[i].y, t[j].y, B[i * HG + j]);
+      }
+  }
+}
+
+// Software-pipelined over chunks: iteration c forms psi of chunk c+1 (MUFU /
+// LDS latency) while the FFMAs of chunk c run; psi rows are double buffered.
+template <int kMode, int FG, int HG, bool kTma>
+__device__ __forceinline__ void lattice_body(const LatticeArgs& a, const LatticeWarp& w,
+                                             float2* psi_w, PhatFloor fl,
+                                             float (&A)[FG * HG], float (&B)[FG * HG]) {
+  constexpr int kNch = kMode == kPsiStaged ? 1 : 2;
+  constexpr int NHG = FG;  // half-lag groups
+  constexpr int S = kLatStages;
+  static_assert(S >= 4, "pipeline depth");
+  const int lane = threadIdx.x & 31;
+  const int fgi = lane / NHG, hgi = lane % NHG;
+  const int my_slot = psi_slot<FG>(lane);
+  const int n = (a.Kb + kLatChunk - 1) / kLatChunk;
+  auto issue = [&](int c) {
+    if constexpr (kTma)
+      lattice_issue_tma<kNch>(w, c, c % S);
+    else
+      lattice_issue<kNch>(a, w, c, c % S);
+  };
+  auto wait_chunk = [&](int c) {  // chunk c landed and is visible to the warp
+    if constexpr (kTma)
+      umma::mbar_wait(&w.full[c % S], (c / S) & 1);
+    else
+      cp_async_wait<S - 3>();  // all but the newest group: chunks <= c
+  };
+#pragma unroll
+  for (int c = 0; c < S - 1; ++c) {
+    if (c < n) issue(c);
+    if (!kTma) cp_async_commit();
+  }
+  if (kTma)
+    umma::mbar_wait(&w.full[0], 0);
+  else
+    cp_async_wait<S - 2>();  // chunk 0
+  __syncwarp();
+  lattice_psi<kMode, kNch, kTma>(a, w, 0, psi_w, my_slot, fl);
+  for (int c = 0; c < n; ++c) {
+    // chunk c+1 landed, psi_w[c&1] written, stage (c-1)%S fully consumed
+    if (c + 1 < n || !kTma) wait_chunk(c + 1);
+    __syncwarp();
+    if (c + S - 1 < n) issue(c + S - 1);
+    if (!kTma) cp_async_commit();
+    if (c + 1 < n)
+      lattice_psi<kMode, kNch, kTma>(a, w, c + 1, psi_w + ((c + 1) & 1) * kLatPsiW, my_slot, fl);
+    lattice_fma<FG, HG, kTma>(w, c, psi_w + (c & 1) * kLatPsiW, fgi, hgi, A, B);
+  }
+  if (!kTma) cp_async_wait<0>();
+}
+
+template <int FG, int HG>
 __device__ __forceinline__ void lattice_reduce_store(const LatticeArgs& a, float* red, int p,
                                                      int f0, int fv, int hl0, int R,
-                                                     const float (&A)[kLatHl],
-                                                     const float (&B)[kLatHl]) {
-  // fixed-order reduction over the 8 K-slices: red[w][acc][frame]
+                                                     const float (&A)[FG * HG],
+                                                     const float (&B)[FG * HG]) {
+  // fixed-order reduction over the 8 K-slices: red[w][acc][lane]
+  constexpr int HL = FG * HG, NHG = FG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   __syncthreads();  // every warp is done with its ring (aliased by red)
 #pragma unroll
-  for (int h = 0; h < HL; ++h) {
-    red[(warp * 2 * kLatHl + h) * kLatF + lane] = A[h];
-    red[(warp * 2 * kLatHl + kLatHl + h) * kLatF + lane] = B[h];
+  for (int e = 0; e < HL; ++e) {
+    red[(warp * 2 * HL + e) * 32 + lane] = A[e];
+    red[(warp * 2 * HL + HL + e) * 32 + lane] = B[e];
   }
   __syncthreads();
   const int col0 = __ldg(a.off + p) + R;  // column of lag 0
@@ -225,11 +364,13 @@ __device__ __forceinline__ void lattice_reduce_store(const LatticeArgs& a, float
     const int fl = o % kLatF, h = o / kLatF;
     const int f = f0 + fl, n_lag = hl0 + h;
     if (fl >= fv || n_lag > R) continue;
+    const int src = (fl / FG) * NHG + h / HG;       // lane holding (fl, h)
+    const int e = (fl % FG) * HG + h % HG;          // its accumulator
     float sa = 0.0f, sb = 0.0f;
 #pragma unroll
     for (int w = 0; w < kLatWarps; ++w) {
-      sa += red[(w * 2 * kLatHl + h) * kLatF + fl];
-      sb += red[(w * 2 * kLatHl + kLatHl + h) * kLatF + fl];
+      sa += red[(w * 2 * HL + e) * 32 + src];
+      sb += red[(w * 2 * HL + HL + e) * 32 + src];
     }
     const size_t row = static_cast<size_t>(f) * a.T_pad + col0;
     lattice_store(a, row + n_lag, 2.0f * (sa - sb));
@@ -237,33 +378,34 @@ __device__ __forceinline__ void lattice_reduce_store(const LatticeArgs& a, float
   }
 }
 
-template <int kMode, int HL>
+template <int kMode, int FG, int HG, bool kTma>
 __device__ __forceinline__ void lattice_run(const LatticeArgs& a, const LatticeWarp& w,
-                                         PhatFloor fl, float* red, int p, int f0, int fv,
-                                         int hl0, int R) {
-  float A[kLatHl], B[kLatHl];
+                                            float2* psi_w, PhatFloor fl, float* red, int p,
+                                            int f0, int fv, int hl0, int R) {
+  float A[FG * HG], B[FG * HG];
 #pragma unroll
-  for (int h = 0; h < kLatHl; ++h) A[h] = B[h] = 0.0f;
-  lattice_body<kMode, HL>(a, w, fl, A, B);
-  lattice_reduce_store<HL>(a, red, p, f0, fv, hl0, R, A, B);
+  for (int e = 0; e < FG * HG; ++e) A[e] = B[e] = 0.0f;
+  lattice_body<kMode, FG, HG, kTma>(a, w, psi_w, fl, A, B);
+  lattice_reduce_store<FG, HG>(a, red, p, f0, fv, hl0, R, A, B);
 }
 
-template <int kMode>
+template <int kMode, bool kTma>
 __device__ __forceinline__ void lattice_dispatch_hl(int hlc, const LatticeArgs& a,
-                                                    const LatticeWarp& w, PhatFloor fl,
-                                                    float* red, int p, int f0, int fv, int hl0,
-                                                    int R) {
+                                                    const LatticeWarp& w, float2* psi_w,
+                                                    PhatFloor fl, float* red, int p, int f0,
+                                                    int fv, int hl0, int R) {
   if (hlc <= 8)
-    lattice_run<kMode, 8>(a, w, fl, red, p, f0, fv, hl0, R);
+    lattice_run<kMode, 2, 4, kTma>(a, w, psi_w, fl, red, p, f0, fv, hl0, R);
   else if (hlc <= 12)
-    lattice_run<kMode, 12>(a, w, fl, red, p, f0, fv, hl0, R);
+    lattice_run<kMode, 4, 3, kTma>(a, w, psi_w, fl, red, p, f0, fv, hl0, R);
   else
-    lattice_run<kMode, 16>(a, w, fl, red, p, f0, fv, hl0, R);
+    lattice_run<kMode, 4, 4, kTma>(a, w, psi_w, fl, red, p, f0, fv, hl0, R);
 }
 
-template <bool kFromY>
+template <bool kFromY, bool kTma>
 __global__ void __launch_bounds__(kLatThreads, 2)
-lattice_kernel(const LatticeArgs a) {
+lattice_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_tw,
+               const LatticeArgs a) {
   const int p = blockIdx.x;
   const int f0 = blockIdx.y * kLatF;
   const int tid = threadIdx.x;
@@ -281,38 +423,61 @@ lattice_kernel(const LatticeArgs a) {
   const int hl0 = blockIdx.z * kLatHl;
   if (hl0 > R) return;
 
-  extern __shared__ __align__(16) float4 s_lat[];
+  extern __shared__ __align__(1024) uint8_t s_lat_raw[];
+  // 1024-align (32-byte-swizzled TMA tiles need 256-byte aligned stages)
+  float4* s_lat = reinterpret_cast<float4*>(
+      s_lat_raw + ((1024u - (umma::smem_u32(s_lat_raw) & 1023u)) & 1023u));
   const int warp = tid >> 5, lane = tid & 31;
   const int fv = min(kLatF, a.F - f0);
   LatticeWarp w;
-  w.ring = s_lat + warp * kLatStages * kLatStageW;
+  using G = LatGeom<kTma>;
+  w.ring = s_lat + warp * kLatStages * G::kStageW;
   w.kbase = warp * kLatBinsW;
-  w.twsrc = a.tw + hl0 + 2 * (lane & 7);
+  w.f0 = f0;
+  w.hl0 = hl0;
+  w.tm_src = &tm_src;
+  w.tm_tw = &tm_tw;
+  w.full = reinterpret_cast<uint64_t*>(reinterpret_cast<float2*>(s_lat + G::kRing) +
+                                       kLatWarps * 2 * kLatPsiW) +
+           warp * kLatStages;
+  if constexpr (kTma) {
+    if (lane == 0) {
+      for (int st = 0; st < kLatStages; ++st) umma::mbar_init(&w.full[st], 1);
+      umma::fence_mbar_init();
+    }
+    __syncwarp();
+    w.row_c[0] = kFromY ? __ldg(a.pm + p) : p;
+    w.row_c[1] = kFromY ? __ldg(a.pmp + p) : p;
+  } else {
+    w.twsrc = a.tw + hl0 + 2 * (lane & 7);
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const size_t f = static_cast<size_t>(f0 + min((lane >> 1) + 16 * half, fv - 1));
-    if constexpr (kFromY) {
-      w.src[0][half] = a.src + (f * a.M + __ldg(a.pm + p)) * a.Kb;
-      w.src[1][half] = a.src + (f * a.M + __ldg(a.pmp + p)) * a.Kb;
-    } else {
-      w.src[0][half] = w.src[1][half] = a.src + (f * a.P + p) * a.Kb;
+    for (int half = 0; half < 2; ++half) {
+      const size_t f = static_cast<size_t>(f0 + min((lane >> 1) + 16 * half, fv - 1));
+      if constexpr (kFromY) {
+        w.src[0][half] = a.src + (f * a.M + __ldg(a.pm + p)) * a.Kb;
+        w.src[1][half] = a.src + (f * a.M + __ldg(a.pmp + p)) * a.Kb;
+      } else {
+        w.src[0][half] = w.src[1][half] = a.src + (f * a.P + p) * a.Kb;
+      }
     }
   }
   const int hlc = min(kLatHl, R + 1 - hl0);  // half-lags this CTA owns
   float* red = reinterpret_cast<float*>(s_lat);
+  float2* psi_w = reinterpret_cast<float2*>(s_lat + G::kRing) + warp * 2 * kLatPsiW;
   if constexpr (kFromY) {
     const int f = f0 + min(lane, fv - 1);  // lane = frame
     const PhatFloor fl = make_phat_floor(a.floors ? __ldg(a.floors + f) : a.const_floor);
     // CTA-uniform: every warp sees the same 32 frames
     const bool clean = __all_sync(0xffffffffu, a.clean != nullptr && __ldg(a.clean + f) != 0);
     if (a.weighting != 0)
-      lattice_dispatch_hl<kPsiIdentity>(hlc, a, w, fl, red, p, f0, fv, hl0, R);
+      lattice_dispatch_hl<kPsiIdentity, kTma>(hlc, a, w, psi_w, fl, red, p, f0, fv, hl0, R);
     else if (clean)
-      lattice_dispatch_hl<kPsiPhatClean>(hlc, a, w, fl, red, p, f0, fv, hl0, R);
+      lattice_dispatch_hl<kPsiPhatClean, kTma>(hlc, a, w, psi_w, fl, red, p, f0, fv, hl0, R);
     else
-      lattice_dispatch_hl<kPsiPhatChecked>(hlc, a, w, fl, red, p, f0, fv, hl0, R);
+      lattice_dispatch_hl<kPsiPhatChecked, kTma>(hlc, a, w, psi_w, fl, red, p, f0, fv, hl0, R);
   } else {
-    lattice_dispatch_hl<kPsiStaged>(hlc, a, w, PhatFloor{0.0, 0.0f}, red, p, f0, fv, hl0, R);
+    lattice_dispatch_hl<kPsiStaged, kTma>(hlc, a, w, psi_w, PhatFloor{0.0, 0.0f}, red, p, f0, fv,
+                                          hl0, R);
   }
 }
 
@@ -323,22 +488,47 @@ cudaError_t launch_lattice_twiddles(const double* omega, int Kb, double T, int L
   return cudaGetLastError();
 }
 
+template <bool kFromY, bool kTma>
+static cudaError_t launch_lattice_kernel(const CUtensorMap& tm_src, const CUtensorMap& tm_tw,
+                                         const LatticeArgs& a, dim3 grid, cudaStream_t stream) {
+  constexpr int smem = static_cast<int>(LatGeom<kTma>::kSmem);
+  static_assert(2 * LatGeom<kTma>::kSmem <= 227 * 1024, "two CTAs per SM");
+  // per launch: the attribute is per device, and setting it is cheap
+  cudaError_t e = cudaFuncSetAttribute(lattice_kernel<kFromY, kTma>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  lattice_kernel<kFromY, kTma><<<grid, kLatThreads, smem, stream>>>(tm_src, tm_tw, a);
+  return cudaGetLastError();
+}
+
 static cudaError_t launch_lattice_args(const LatticeArgs& a, bool from_y, int max_Tp,
                                       cudaStream_t stream) {
-  constexpr int smem = static_cast<int>(kLatSmemBytes);
-  // per launch: the attribute is per device, and setting it is cheap
-  cudaError_t e = from_y ? cudaFuncSetAttribute(lattice_kernel<true>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
-                         : cudaFuncSetAttribute(lattice_kernel<false>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
   const int max_reach = (max_Tp - 1) / 2;
   dim3 grid(a.P + 1, (a.F + kLatF - 1) / kLatF, max_reach / kLatHl + 1);
+  // TMA staging: 3-D map over the source rows [F][rows][Kb] of 8-byte
+  // complex elements (box 4 bins x 1 row x 32 frames, 32-byte swizzle) and a
+  // 2-D map over the twiddles [Kb][Hs] (box 16 half-lags x 4 bins); needs
+  // even Kb and 16-byte aligned bases, else the cp.async path stages
+  CUtensorMap tm_src{}, tm_tw{};
+  bool tma = a.vec16 && (reinterpret_cast<uintptr_t>(a.tw) & 15) == 0;
+  if (tma) {
+    const cuuint64_t rows = from_y ? a.M : a.P;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(a.Kb), rows, static_cast<cuuint64_t>(a.F)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(a.Kb) * 8, rows * a.Kb * 8};
+    cuuint32_t box[3] = {4, 1, kLatF};
+    tma = encode_tensor_map(&tm_src, CU_TENSOR_MAP_DATA_TYPE_INT64, 3, a.src, dims, strides, box,
+                            CU_TENSOR_MAP_SWIZZLE_32B) == cudaSuccess;
+    cuuint64_t tdims[2] = {static_cast<cuuint64_t>(a.Hs), static_cast<cuuint64_t>(a.Kb)};
+    cuuint64_t tstrides[1] = {static_cast<cuuint64_t>(a.Hs) * 8};
+    cuuint32_t tbox[2] = {kLatHl, 4};
+    tma = tma && encode_tensor_map(&tm_tw, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, a.tw, tdims, tstrides,
+                                   tbox, CU_TENSOR_MAP_SWIZZLE_NONE) == cudaSuccess;
+  }
   if (from_y)
-    lattice_kernel<true><<<grid, kLatThreads, smem, stream>>>(a);
-  else
-    lattice_kernel<false><<<grid, kLatThreads, smem, stream>>>(a);
-  return cudaGetLastError();
+    return tma ? launch_lattice_kernel<true, true>(tm_src, tm_tw, a, grid, stream)
+               : launch_lattice_kernel<true, false>(tm_src, tm_tw, a, grid, stream);
+  return tma ? launch_lattice_kernel<false, true>(tm_src, tm_tw, a, grid, stream)
+             : launch_lattice_kernel<false, false>(tm_src, tm_tw, a, grid, stream);
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }

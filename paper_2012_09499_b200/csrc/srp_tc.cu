@@ -52,6 +52,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tmap.cuh"
 #include "umma.cuh"
 
 namespace srpb {
@@ -712,36 +713,18 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
 // --------------------------------------------------------------------- host
 namespace {
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (fn == nullptr) {
-    cudaDriverEntryPointQueryResult q;
-    void* ptr = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
-  return fn;
-}
-
 // Row-major fp32 / fp16 matrix [rows, cols] -> tensor map with a 128-byte
 // (32 fp32 or 64 fp16) x box_rows box and 128-byte swizzle (K-major UMMA
 // operand tiles); columns past `cols` read as zero.
 cudaError_t make_map(CUtensorMap* m, const void* base, int rows, int cols, int box_rows,
                      bool f16) {
-  auto fn = encode_fn();
-  if (fn == nullptr) return cudaErrorNotSupported;
   const size_t esz = f16 ? 2 : 4;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * esz};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esz), static_cast<cuuint32_t>(box_rows)};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                  const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+  return encode_tensor_map(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                           2, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
 }
 
 // Frames per tile: N-tiles of <= 160 frames, multiple of 32.
@@ -852,7 +835,9 @@ static cudaError_t conventional_tc(const void* psi_hi, const void* psi_lo, bool 
               : launch_tc<kAPhase, false, false>(bh, bl, bh, bl, p, stream);
 }
 
-// K4: A = W split, B = Xi split; maps = (W_hi + W_lo)(Xi_hi + Xi_lo)^T * scale
+// K4: A = W split, B = Xi split; maps = (W_hi + W_lo)(Xi_hi + Xi_lo)^T * scale.
+// (Measured: splitting the argmax into a K5 pass over the stored maps saves
+// 6 us of K4 epilogue but costs 16 us of K5, so it stays fused.)
 static cudaError_t interp_tc(const void* w_hi, const void* w_lo, const void* xi_hi,
                              const void* xi_lo, bool f16, float scale, int F, int J, int T_pad,
                              float* maps, unsigned long long* keys, int kb_per_group,
