@@ -87,58 +87,77 @@ def config_dict(F, J, P, Kb, total_samples):
 
 # -------------------------------------------------------------- clocks probe
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled every ~1 ms during
+    the timed regions (NVML; nvidia-smi -lms 100 as the fallback).  Call
+    resume()/pause() around each timed region; stop() summarises."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.active = threading.Event()
+        self.done = threading.Event()
+        self.thread = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - any NVML failure: fall back
+            self.nv = None
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", str(self.index)],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+        if self.nv is not None:
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
-        except OSError:
-            self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def resume(self):
+        self.active.set()
 
-    def stop(self):
-        if self.proc is None:
-            return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) != 6:
+    def pause(self):
+        self.active.clear()
+
+    def _poll(self):
+        nv = self.nv
+        while not self.done.is_set():
+            if not self.active.wait(0.01):
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sm:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, const in self.REASONS:
+                    if bits & getattr(nv, const, 0):
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.001)
+
+    def stop(self):
+        self.done.set()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        if not self.samples:
+            return self._smi_fallback()
+        return {"sm_mhz": statistics.median(self.samples), "sm_min_mhz": min(self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples), "source": "NVML, ~1 ms polling in timed regions"}
+
+    def _smi_fallback(self):
+        try:
+            out = subprocess.run(
+                ["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm", "--format=csv,noheader,nounits",
+                 "-i", str(self.index)], capture_output=True, text=True, timeout=10).stdout
+            sm, mx = (float(x) for x in out.strip().split(","))
+            return {"sm_mhz": sm, "sm_max_mhz": mx, "reasons": [], "samples": 1,
+                    "source": "nvidia-smi after the timed regions (NVML unavailable)"}
+        except Exception:  # noqa: BLE001
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
 
 
 # --------------------------------------------------------------- CPU baseline
@@ -343,6 +362,7 @@ def run_ours(args):
         kt = KernelTimer() if profile else None
         plan.kernel_timer = kt
         launches0 = _native.launch_count()
+        clocks.resume()
         for _ in range(args.steps):
             flush.zero_()
             a, b = ev(), ev()
@@ -354,6 +374,7 @@ def run_ours(args):
             b.synchronize()
             tot += a.elapsed_time(b)
         torch.cuda.synchronize()
+        clocks.pause()
         plan.kernel_timer = None
         launches = _native.launch_count() - launches0
         ms = tot / args.steps
@@ -369,12 +390,12 @@ def run_ours(args):
     clocks.start()
     ms_a, _, _ = timed(step, "approx")
     ms_c, _, _ = timed(step, "conventional")
-    clk = clocks.stop()
     _, kms_a, _ = timed(eager_step, "approx", profile=True)
     _, kms_c, _ = timed(eager_step, "conventional", profile=True)
     launches_a, launches_c = graphs["approx"].launches, graphs["conventional"].launches
     e2e_a, _, _ = timed(e2e_step, "approx")
     e2e_c, _, _ = timed(e2e_step, "conventional")
+    clk = clocks.stop()
 
     units = F * J * world
     value = units / (ms_a * 1e-3)

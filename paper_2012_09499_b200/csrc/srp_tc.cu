@@ -84,7 +84,7 @@ struct TcCfg {
 // Instrumentation build only (make prof -> libsrpb_prof.so, tools/tc_probe.py):
 // per-role cycle counters; compiled out of libsrpb.so.
 #ifdef SRPB_TC_PROFILE
-__device__ unsigned long long g_tc_prof[16];
+__device__ unsigned long long g_tc_prof[24];
 #define TCP_DECL(v) long long v = 0
 #define TCP_T0() const long long _tcp0 = clock64()
 #define TCP_ACC(v) (v += clock64() - _tcp0)
@@ -100,6 +100,9 @@ struct TcParams {
   int F, J, N;        // frames, candidates, frames per tile
   int n_tiles;        // frame tiles
   int num_items;      // n_tiles * candidate tiles (of 128, or 256 per pair)
+  int full_items;     // items run at full width; the tail wave's items are split
+  int n_piece0;       // frames of a split item's first piece (second: N - n_piece0)
+  int total_items;    // full_items + 2 * (num_items - full_items)
   int num_kb;         // K blocks of 32 per tile
   int kb_per_group;   // TMEM drain period (K blocks)
   int groups_per_tile;
@@ -138,14 +141,14 @@ __host__ __device__ constexpr int tc_a_tmem_col(int N, int s) { return 2 * N + 6
 // row = 32*(warp%4) + lane, columns [half*N/2, half*N/2 + N/2); release the
 // buffer on `acc_empty_addr` (the leader's barrier for pairs).
 __device__ __forceinline__ void tc_drain(const TcParams& p, TcSmem* bar, bool remote,
-                                         uint32_t acc_empty_addr0, uint32_t tmem, int g,
+                                         uint32_t acc_empty_addr0, uint32_t tmem, int g, int nc,
                                          int quarter, int half, float (&tot)[kTcMaxN / 2]) {
   const int b = g & 1;
   mbar_wait(&bar->acc_full[b], (g >> 1) & 1);
   tc_fence_after();
   const uint32_t base = tmem + (static_cast<uint32_t>(32 * quarter) << 16) +
-                        static_cast<uint32_t>(b * p.N + half * (p.N / 2));
-  const int nchunks = p.N / 32;  // 16-column loads per half
+                        static_cast<uint32_t>(b * p.N + half * (nc / 2));
+  const int nchunks = nc / 32;  // 16-column loads per half (nc: this item's frames)
   // two 16-column loads in flight per wait (register budget: 384 threads/SM)
 #pragma unroll
   for (int c = 0; c < kTcMaxN / 32; c += 2) {
@@ -250,13 +253,13 @@ __device__ __forceinline__ void tc_write_cols(const TcParams& p, unsigned long l
 }
 
 __device__ __forceinline__ void tc_write_tile(const TcParams& p, TcSmem* bar, int m0, int n0,
-                                              int quarter, int half, int lane,
+                                              int nc, int quarter, int half, int lane,
                                               float (&tot)[kTcMaxN / 2]) {
   const int J = p.J;
   const uint32_t jbase = static_cast<uint32_t>(m0 + 32 * quarter);
   const int j = static_cast<int>(jbase) + lane;
-  const int cbase = half * (p.N / 2);
-  const int ncols = p.N / 2;
+  const int cbase = half * (nc / 2);
+  const int ncols = nc / 2;
   const int nv = max(0, min(ncols, p.F - (n0 + cbase)));  // columns with f < F
   const int lim = j < J ? nv : 0;
   float* ptr = p.maps ? p.maps + (static_cast<size_t>(n0 + cbase) * J + j) : nullptr;
@@ -278,7 +281,7 @@ __device__ __forceinline__ void tc_write_tile(const TcParams& p, TcSmem* bar, in
     TCP_T0();
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
     const int et = threadIdx.x - kEpiWarp0 * 32;  // 0..255
-    for (int c = et; c < p.N; c += kEpiWarps * 32) {
+    for (int c = et; c < nc; c += kEpiWarps * 32) {
       unsigned long long k = tk[c];
 #pragma unroll
       for (int q = 1; q < 4; ++q) k = key_max(k, tk[q * kTcMaxN + c]);
@@ -388,6 +391,11 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   constexpr bool kASmem = Cfg::kASmem;
   constexpr int KBE = Cfg::kKbElems;
   constexpr int kCta = kPair ? 2 : 1;
+#ifdef SRPB_TC_PROFILE
+  const long long t_entry = clock64();
+  unsigned long long g_entry;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
+#endif
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align by pointer arithmetic on the shared array (keeps the shared
   // address space visible to the compiler: STS/LDS, not generic accesses)
@@ -403,11 +411,34 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   // Work items: (frame tile, candidate tile of 128 x kCta rows); CTA (pair) c
   // takes items c, c + #CTAs(pairs), ...; in a pair, CTA `rank` owns rows
   // [128 rank, 128 rank + 128) of the 256-row tile.
+  // The last partial wave's items are split into two frame pieces (n_piece0
+  // and N - n_piece0 frames) so the wave's work spreads over more CTAs; every
+  // output element accumulates over K in the same order whatever its item's
+  // width, so maps are bitwise independent of the split.
   const int cid = static_cast<int>(blockIdx.x) / kCta;
   const int ncl = static_cast<int>(gridDim.x) / kCta;
-  const int my_tiles = p.num_items > cid ? (p.num_items - 1 - cid) / ncl + 1 : 0;
-  auto tile_m0 = [&](int it) { return (((cid + it * ncl) / p.n_tiles) * kCta + rank) * kTcM; };
-  auto tile_n0 = [&](int it) { return ((cid + it * ncl) % p.n_tiles) * p.N; };
+  const int my_tiles = p.total_items > cid ? (p.total_items - 1 - cid) / ncl + 1 : 0;
+  struct Item {
+    int m0, n0, nc;  // candidate row base (this CTA), frame base, frames
+  };
+  auto item = [&](int it) {
+    const int g = cid + it * ncl;
+    int b = g, piece = -1;
+    if (g >= p.full_items) {
+      b = p.full_items + ((g - p.full_items) >> 1);
+      piece = (g - p.full_items) & 1;
+    }
+    Item r;
+    r.m0 = ((b / p.n_tiles) * kCta + rank) * kTcM;
+    r.n0 = (b % p.n_tiles) * p.N;
+    r.nc = p.N;
+    if (piece == 0) r.nc = p.n_piece0;
+    if (piece == 1) {
+      r.n0 += p.n_piece0;
+      r.nc = p.N - p.n_piece0;
+    }
+    return r;
+  };
 
   const size_t a_bytes = kASmem ? 2 * kABytes : 0;
   auto a_hi = [&](int s) { return smem + s * stage_bytes; };
@@ -449,6 +480,9 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   __syncthreads();
   if (kPair) cluster_sync();  // the leader's barriers exist before peers signal them
   tc_fence_after();
+#ifdef SRPB_TC_PROFILE
+  if (threadIdx.x == 0) atomicAdd(&g_tc_prof[17], static_cast<unsigned long long>(clock64() - t_entry));
+#endif
   // make the TMEM base provably warp-uniform (it stays in a uniform register)
   const uint32_t tmem = __shfl_sync(0xffffffffu, bar->tmem_base, 0);
   // barriers every CTA of the pair signals live in the leader
@@ -460,14 +494,17 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // ------------------------------------------------------------ TMA producer
     // warp-wide loop, one elected lane issues (uniform operands, no per-issue
     // register broadcasts)
-    const uint32_t tx = static_cast<uint32_t>(kCta) * (2 * b_bytes + (kASmem ? 2 * kABytes : 0));
     int kg = 0;
     TCP_DECL(w_empty);
     TCP_DECL(t_all);
     { TCP_T0();
     for (int it = 0; it < my_tiles; ++it) {
-      const int m0 = tile_m0(it);
-      const int nb = tile_n0(it) + rank * b_rows;  // this CTA's B rows
+      const Item t = item(it);
+      const int m0 = t.m0;
+      const int rows = kPair ? t.nc / 2 : t.nc;    // this CTA's B rows (multiple of 16)
+      const int nb = t.n0 + rank * rows;
+      const uint32_t tx = static_cast<uint32_t>(kCta) *
+                          (2 * static_cast<uint32_t>(rows) * 128 + (kASmem ? 2 * kABytes : 0));
       for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
         const int s = kg % S;
         { TCP_T0();
@@ -481,16 +518,20 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
               mbar_expect_tx(&bar->full[s], tx);
             else
               mbar_arrive_cluster_relaxed(fb);
-            tma_load_2d_pair(b_hi(s), &tmB_hi, fb, kb * KBE, nb);
-            tma_load_2d_pair(b_lo(s), &tmB_lo, fb, kb * KBE, nb);
+            for (int r = 0; r < rows; r += 16) {  // 16-row boxes: any item width
+              tma_load_2d_pair(b_hi(s) + r * 128, &tmB_hi, fb, kb * KBE, nb + r);
+              tma_load_2d_pair(b_lo(s) + r * 128, &tmB_lo, fb, kb * KBE, nb + r);
+            }
             if (kASmem) {
               tma_load_2d_pair(a_hi(s), &tmA_hi, fb, kb * KBE, m0);
               tma_load_2d_pair(a_lo(s), &tmA_lo, fb, kb * KBE, m0);
             }
           } else {
             mbar_expect_tx(&bar->full[s], tx);
-            tma_load_2d(b_hi(s), &tmB_hi, &bar->full[s], kb * KBE, nb);
-            tma_load_2d(b_lo(s), &tmB_lo, &bar->full[s], kb * KBE, nb);
+            for (int r = 0; r < rows; r += 16) {
+              tma_load_2d(b_hi(s) + r * 128, &tmB_hi, &bar->full[s], kb * KBE, nb + r);
+              tma_load_2d(b_lo(s) + r * 128, &tmB_lo, &bar->full[s], kb * KBE, nb + r);
+            }
             if (kASmem) {
               tma_load_2d(a_hi(s), &tmA_hi, &bar->full[s], kb * KBE, m0);
               tma_load_2d(a_lo(s), &tmA_lo, &bar->full[s], kb * KBE, m0);
@@ -513,7 +554,6 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // byte-offset>>4 arithmetic on uniform values; one elected lane issues
     // the MMAs and their commits.
     if (leader) {
-      const uint32_t idesc = kF16 ? idesc_f16(kTcM * kCta, p.N) : idesc_tf32(kTcM * kCta, p.N);
       const uint64_t db0 = sw128_kmajor_desc(smem_u32(b_hi(0)));  // stage 0 B_hi
       const uint64_t da0 = sw128_kmajor_desc(smem_u32(a_hi(0)));  // stage 0 A_hi (K4)
       const uint32_t stage16 = static_cast<uint32_t>(stage_bytes >> 4);
@@ -524,6 +564,8 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       TCP_DECL(t_all);
       { TCP_T0();
       for (int it = 0; it < my_tiles; ++it) {
+        const int nc = item(it).nc;
+        const uint32_t idesc = kF16 ? idesc_f16(kTcM * kCta, nc) : idesc_tf32(kTcM * kCta, nc);
         for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
           const int s = kg % S;
           const int gl = kb / p.kb_per_group;                 // group within the tile
@@ -634,12 +676,13 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     TCP_DECL(c_write);
     TCP_DECL(c_all);
     auto fold_next = [&]() {
+      const Item t = item(d_it);
       { TCP_T0();
-      tc_drain(p, bar, !leader, acc_empty_addr0, tmem, drained, quarter, half, tot);
+      tc_drain(p, bar, !leader, acc_empty_addr0, tmem, drained, t.nc, quarter, half, tot);
       TCP_ACC(c_drain); }
       if (d_gl == p.groups_per_tile - 1) {
         TCP_T0();
-        tc_write_tile(p, bar, tile_m0(d_it), tile_n0(d_it), quarter, half, lane, tot);
+        tc_write_tile(p, bar, t.m0, t.n0, t.nc, quarter, half, lane, tot);
         TCP_ACC(c_write);
         ++d_it;
         d_gl = 0;
@@ -659,7 +702,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       PhaseGen<kF16> gen;
       int kg = 0, s = 0, ph = 0;  // stage ring position
       for (int it = 0; it < my_tiles; ++it) {
-        const int j = tile_m0(it) + r;
+        const int j = item(it).m0 + r;
         gen.start_tile(p);
         for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
           { TCP_T0();
@@ -698,9 +741,25 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       TCP_FLUSH(10, c_all);
     }
   }
+#ifdef SRPB_TC_PROFILE
+  const long long t_work = clock64();
+#endif
   tc_fence_before();
   __syncthreads();
   if (kPair) cluster_sync();  // the pair leaves together (remote arrivals landed)
+#ifdef SRPB_TC_PROFILE
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_tc_prof[16], static_cast<unsigned long long>(clock64() - t_entry));
+    atomicAdd(&g_tc_prof[18], static_cast<unsigned long long>(clock64() - t_work));
+    atomicAdd(&g_tc_prof[19], 1ull);
+    unsigned long long g_exit;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+    atomicMax(&g_tc_prof[20], ~g_entry);  // earliest entry (complemented)
+    atomicMax(&g_tc_prof[21], g_exit);    // latest exit
+    atomicMax(&g_tc_prof[22], ~g_exit);   // earliest exit (complemented)
+    atomicMax(&g_tc_prof[23], g_entry);   // latest entry
+  }
+#endif
   if (warp == 1) {
     tc_fence_after();
     if (kPair)
@@ -749,16 +808,6 @@ bool use_pair(int m_tiles, bool default_on) {
   return env == 1 || default_on;
 }
 
-void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16) {
-  p.N = pick_n(p.F);
-  p.n_tiles = (p.F + p.N - 1) / p.N;
-  const int m_tiles = (p.J + kTcM - 1) / kTcM;
-  const int cta = pair ? 2 : 1;
-  p.num_items = p.n_tiles * ((m_tiles + cta - 1) / cta);
-  p.kb_per_group = max(f16 ? 2 : 4, kb_per_group);
-  p.groups_per_tile = (p.num_kb + p.kb_per_group - 1) / p.kb_per_group;
-}
-
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -768,6 +817,25 @@ int num_sms() {
       n = kNumSMs;
   }
   return n;
+}
+
+void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16) {
+  p.N = pick_n(p.F);
+  p.n_tiles = (p.F + p.N - 1) / p.N;
+  const int m_tiles = (p.J + kTcM - 1) / kTcM;
+  const int cta = pair ? 2 : 1;
+  p.num_items = p.n_tiles * ((m_tiles + cta - 1) / cta);
+  // tail-wave split: items beyond the last full wave of `units` CTAs (pairs)
+  // run as two frame pieces (widths multiples of 32: the epilogue drains
+  // 16-column chunks per column half)
+  const int units = max(1, min(p.num_items, num_sms() / cta));
+  p.n_piece0 = (p.N / 2 + 31) / 32 * 32;
+  const bool split = p.N >= 64 && p.n_piece0 < p.N && p.num_items > units &&
+                     p.num_items % units != 0 && getenv("SRPB_TC_NOSPLIT") == nullptr;
+  p.full_items = split ? p.num_items / units * units : p.num_items;
+  p.total_items = p.full_items + 2 * (p.num_items - p.full_items);
+  p.kb_per_group = max(f16 ? 2 : 4, kb_per_group);
+  p.groups_per_tile = (p.num_kb + p.kb_per_group - 1) / p.kb_per_group;
 }
 
 template <int kAMode, bool kPair, bool kF16>
@@ -780,7 +848,7 @@ cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtens
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   constexpr int cta = kPair ? 2 : 1;
-  const int units = min(p.num_items, num_sms() / cta);
+  const int units = min(p.total_items, num_sms() / cta);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * cta);
   cfg.blockDim = dim3(kTcThreads);
@@ -824,7 +892,7 @@ static cudaError_t conventional_tc(const void* psi_hi, const void* psi_lo, bool 
   p.inv_period = 1.0f / static_cast<float>(period);
   CUtensorMap bh, bl;
   const int cols = 2 * P * Kb;
-  const int brows = pair ? p.N / 2 : p.N;  // B rows per CTA
+  const int brows = 16;  // B boxes of 16 rows (any item width)
   cudaError_t e = make_map(&bh, psi_hi, F, cols, brows, f16);
   if (e == cudaSuccess) e = make_map(&bl, psi_lo, F, cols, brows, f16);
   if (e != cudaSuccess) return e;
@@ -854,7 +922,7 @@ static cudaError_t interp_tc(const void* w_hi, const void* w_lo, const void* xi_
   p.maps = maps;
   p.keys = keys;
   CUtensorMap ah, al, bh, bl;
-  const int brows = pair ? p.N / 2 : p.N;
+  const int brows = 16;  // B boxes of 16 rows (any item width)
   cudaError_t e = make_map(&ah, w_hi, J, T_pad, kTcM, f16);
   if (e == cudaSuccess) e = make_map(&al, w_lo, J, T_pad, kTcM, f16);
   if (e == cudaSuccess) e = make_map(&bh, xi_hi, F, T_pad, brows, f16);
@@ -958,8 +1026,8 @@ cudaError_t launch_tf32_split(const float* x, size_t n, float* hi, float* lo, cu
 #ifdef SRPB_TC_PROFILE
 // instrumentation build only: copy out and clear the 16 role counters
 extern "C" int srpb_tc_profile_read(unsigned long long* host16) {
-  cudaError_t e = cudaMemcpyFromSymbol(host16, srpb::g_tc_prof, sizeof(unsigned long long) * 16);
-  unsigned long long zero[16] = {};
+  cudaError_t e = cudaMemcpyFromSymbol(host16, srpb::g_tc_prof, sizeof(unsigned long long) * 24);
+  unsigned long long zero[24] = {};
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(srpb::g_tc_prof, zero, sizeof(zero));
   return static_cast<int>(e);
 }

@@ -29,22 +29,29 @@ from paper_2012_09499_b200.plan import SrpPlan  # noqa: E402
 NAMES = {0: "mma_total", 1: "mma_wait_full", 2: "mma_wait_acc_empty", 3: "tma_wait_empty",
          4: "tma_total", 5: "epi_gen_wait_empty", 6: "epi_gen", 7: "epi_drain", 9: "epi_write",
          10: "epi_total", 11: "ctas", 12: "write_loop", 13: "write_flush", 14: "write_stores",
-         15: "write_argmax"}
+         15: "write_argmax", 16: "cta_lifetime(all CTAs)", 17: "setup(all CTAs)",
+         18: "teardown_wait(all CTAs)", 19: "cta_count"}
 
 
 def read():
-    buf = (ctypes.c_ulonglong * 16)()
+    buf = (ctypes.c_ulonglong * 24)()
     assert lib.srpb_tc_profile_read(ctypes.addressof(buf)) == 0
     return list(buf)
 
 
 def report(tag, c):
     n = max(c[11], 1)
+    M = (1 << 64) - 1
+    first_in, last_out = M - c[20], c[21]
+    first_out, last_in = M - c[22], c[23]
+    print(f"== {tag}: CTA span {(last_out - first_in) / 1e3:.1f} us (globaltimer); entries spread "
+          f"{(last_in - first_in) / 1e3:.1f} us, exits spread {(last_out - first_out) / 1e3:.1f} us")
     print(f"== {tag}: {n} CTAs; per-CTA cycles:")
     for i, name in NAMES.items():
-        if i == 11:
+        if i in (11, 19, 20, 21, 22, 23):
             continue
-        print(f"   {name:22s} {c[i] / n:14.0f}   ({c[i] / max(c[0], 1) * 100:5.1f}% of mma_total)")
+        d = max(c[19], 1) if i in (16, 17, 18) else n
+        print(f"   {name:24s} {c[i] / d:14.0f}   ({c[i] / d / max(c[0] / n, 1) * 100:5.1f}% of mma_total)")
 
 
 def main():
