@@ -43,6 +43,20 @@ int srpb_abi_version(void);
 const char* srpb_last_error(void);
 
 /*
+ * K0 STFT on the device.  Replaces spectral.stft_analyze (spectral.py:185-215)
+ * with FrameSpec's framing and window (:35-99): frame f covers samples
+ * [f hop, f hop + N), periodic sqrt-Hann (window 0) or rectangular (1),
+ * one-sided bins 0..N/2-1 (DC kept, Nyquist dropped).
+ *   x [M, L] float32 audio; N = frame_length even: powers of two <= 8192
+ *   take a shared-memory FFT, other N <= 4096 a direct DFT;
+ *   F = (L - N) / hop + 1 (trailing samples dropped)
+ *   Y [F, M, N/2] complex64 out (the layout srpb_gcc_phat / srpb_gcc_floor /
+ *   srpb_lattice_from_spectra read)
+ */
+int srpb_stft(const float* x, int M, int L, int frame_length, int hop, int window, int F,
+              float* Y, void* stream);
+
+/*
  * K1 GCC-PHAT cross-spectra for F frames.
  * Replaces spectral.cross_spectrum (pkg/src/srpfast/spectral.py:218-285),
  * batched over frames.

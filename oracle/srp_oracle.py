@@ -73,6 +73,26 @@ def cross_spectrum(spectra, pair_m, pair_mp, weighting="phat", phat_floor=None):
     return out, floor
 
 
+def stft(signals, frame_length, hop_length=None, window="sqrt_hann"):
+    """Framed, windowed one-sided spectra [F, M, K] complex128
+    (``spectral.stft_analyze`` ``spectral.py:185-215``; window
+    ``FrameSpec.window_samples`` ``:85-90``; frame count ``num_frames``
+    ``:92-99``).  Frame f covers samples [f hop, f hop + N); DC kept, Nyquist
+    dropped; trailing samples that do not fill a frame are dropped."""
+    x = np.atleast_2d(np.asarray(signals, dtype=float))
+    n = int(frame_length)
+    hop = n // 2 if hop_length is None else int(hop_length)
+    if window == "rectangular":
+        w = np.ones(n)
+    else:
+        w = np.sqrt(0.5 - 0.5 * np.cos(2.0 * np.pi * np.arange(n) / n))
+    num = (x.shape[1] - n) // hop + 1
+    out = np.empty((num, x.shape[0], n // 2), dtype=np.complex128)
+    for f in range(num):
+        out[f] = np.fft.rfft(x[:, f * hop: f * hop + n] * w[None, :], axis=1)[:, : n // 2]
+    return out
+
+
 def bin_frequencies(sample_rate, frame_length):
     """``w_k = 2 pi k fs / N`` for ``k < N/2`` (``spectral.py:80-83``)."""
     k = np.arange(frame_length // 2)

@@ -31,6 +31,7 @@ from .spectral import (
     cross_spectrum,
     cross_spectrum_frames,
     stft_analyze,
+    stft_frames,
 )
 from .srp import (
     ComplexityReport,
@@ -61,7 +62,7 @@ __all__ = [
     "enumerate_pairs", "tdoa_farfield", "tdoa_nearfield",
     "SrpPlan", "lattice_layout", "standalone_argmax",
     "DEFAULT_PHAT_FLOOR_REL", "CrossSpectra", "FrameSpec", "SpectralFrame", "cross_spectrum",
-    "cross_spectrum_frames", "stft_analyze",
+    "cross_spectrum_frames", "stft_analyze", "stft_frames",
     "ComplexityReport", "GccLattice", "MultCounter", "SincTable", "SrpMap",
     "argmax_candidate", "build_gcc_lattice", "build_gcc_lattice_frames", "complexity_report",
     "gcc_at_lag", "lattice_half_counts", "precompute_sinc_table", "srp_approx",

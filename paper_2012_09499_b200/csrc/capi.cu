@@ -10,6 +10,7 @@
 namespace srpb {
 cudaError_t launch_gcc_phat(const float*, int, int, int, const int32_t*, const int32_t*, int, int,
                             double, double, float*, double*, cudaStream_t);
+cudaError_t launch_stft(const float*, int, int, int, int, int, int, float*, cudaStream_t);
 cudaError_t launch_gcc_floor(const float*, int, int, int, const int32_t*, const int32_t*, int,
                              double, double*, int32_t*, cudaStream_t);
 cudaError_t launch_lattice_from_spectra(const float*, int, int, int, const int32_t*,
@@ -85,9 +86,28 @@ static bool pow2_scale(float s) {
   return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
 }
 
-int srpb_abi_version(void) { return 3; }
+int srpb_abi_version(void) { return 4; }
 
 const char* srpb_last_error(void) { return g_err; }
+
+int srpb_stft(const float* x, int M, int L, int frame_length, int hop, int window, int F,
+              float* Y, void* stream) {
+  REQUIRE(M >= 1 && L >= 1, "srpb_stft: bad shape M=%d L=%d", M, L);
+  REQUIRE(frame_length >= 2 && frame_length % 2 == 0,
+          "srpb_stft: frame_length must be an even integer >= 2, got %d", frame_length);
+  REQUIRE((frame_length & (frame_length - 1)) == 0 ? frame_length <= 8192 : frame_length <= 4096,
+          "srpb_stft: frame_length %d too large (power of two <= 8192, else <= 4096)",
+          frame_length);
+  REQUIRE(hop >= 1, "srpb_stft: hop_length must be >= 1, got %d", hop);
+  REQUIRE(window == 0 || window == 1, "srpb_stft: unknown window %d", window);
+  REQUIRE(L >= frame_length, "srpb_stft: signal of %d samples is shorter than one frame (%d)", L,
+          frame_length);
+  REQUIRE(F == (L - frame_length) / hop + 1, "srpb_stft: F=%d, expected %d frames", F,
+          (L - frame_length) / hop + 1);
+  REQUIRE(x && Y, "srpb_stft: null pointer");
+  return status(srpb::launch_stft(x, M, L, frame_length, hop, window, F, Y, S(stream)),
+                "srpb_stft");
+}
 
 int srpb_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
                   const int32_t* pair_mp, int P, int weighting, double floor_rel,

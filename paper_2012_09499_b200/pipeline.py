@@ -34,12 +34,26 @@ class ChunkedRunner:
     """Pipelined ``plan.run`` over host buffers (pinned for async copies)."""
 
     def __init__(self, plan, F, M=None, path="approx", chunks=4, maps=True, weighting="phat",
-                 phat_floor=None):
+                 phat_floor=None, audio=None):
+        """``audio=(frame_length, hop_length, window)``: inputs are [M, L]
+        audio (F = its frame count); each chunk's graph runs K0 on the chunk's
+        sample span (spans of neighbouring chunks overlap by N - hop)."""
         self.plan, self.F, self.path, self.want_maps = plan, F, path, maps
         self.bounds = chunk_bounds(F, chunks)
         dev = plan.device
-        self.steps = [CapturedStep(plan, hi - lo, M if M is not None else plan.M, path, maps,
-                                   weighting, phat_floor) for lo, hi in self.bounds]
+        M = M if M is not None else plan.M
+        self.audio = None
+        if audio is not None:
+            n, hop, window = audio
+            hop = n // 2 if hop is None else int(hop)
+            self.audio = (n, hop, window)
+            self.spans = [(lo * hop, (hi - 1) * hop + n) for lo, hi in self.bounds]
+            self.steps = [CapturedStep(plan, hi - lo, M, path, maps, weighting, phat_floor,
+                                       audio=(b - a, n, hop, window))
+                          for (lo, hi), (a, b) in zip(self.bounds, self.spans)]
+        else:
+            self.steps = [CapturedStep(plan, hi - lo, M, path, maps, weighting, phat_floor)
+                          for lo, hi in self.bounds]
         self.s_in = torch.cuda.Stream(dev)
         self.s_comp = torch.cuda.Stream(dev)
         self.s_out = torch.cuda.Stream(dev)
@@ -55,16 +69,21 @@ class ChunkedRunner:
         return sum(s.launches for s in self.steps)
 
     def run(self, Y_host, maps_host=None, argmax_host=None):
-        """Enqueue one pass: Y_host [F, M, Kb] complex64 (pinned) -> maps_host
-        [F, J] float32 and argmax_host [F] int32 (pinned).  Asynchronous with
-        respect to the host; the caller's current stream waits for the last
-        device->host copy."""
+        """Enqueue one pass: Y_host [F, M, Kb] complex64 (or [M, L] float32
+        audio) in pinned memory -> maps_host [F, J] float32 and argmax_host
+        [F] int32 (pinned).  Asynchronous with respect to the host; the
+        caller's current stream waits for the last device->host copy."""
         for c, (lo, hi) in enumerate(self.bounds):
             st = self.steps[c]
             with torch.cuda.stream(self.s_in):
-                if not self._first:  # previous call's compute has read st.Y
+                if not self._first:  # previous call's compute has read the input
                     self.s_in.wait_event(self.ev_comp[c])
-                st.Y.copy_(Y_host[lo:hi], non_blocking=True)
+                if self.audio is not None:
+                    a, b = self.spans[c]
+                    for m in range(st.x.shape[0]):  # contiguous pinned rows
+                        st.x[m].copy_(Y_host[m, a:b], non_blocking=True)
+                else:
+                    st.Y.copy_(Y_host[lo:hi], non_blocking=True)
                 self.ev_in[c].record(self.s_in)
             with torch.cuda.stream(self.s_comp):
                 self.s_comp.wait_event(self.ev_in[c])

@@ -442,11 +442,42 @@ class SrpPlan:
             return self.approx(self.lattice_from_spectra(Y, weighting, phat_floor), maps)
         raise ValueError(f"unknown path {path!r}")
 
-    def capture(self, F, M=None, path="approx", maps=True, weighting="phat", phat_floor=None):
+    def stft(self, x, frame_length, hop_length=None, window="sqrt_hann", out=None):
+        """K0: audio ``x`` [M, L] float32 (CUDA) -> Y [F, M, frame_length/2]
+        complex64 (``spectral.stft_analyze`` framing and window)."""
+        hop = frame_length // 2 if hop_length is None else int(hop_length)
+        if frame_length // 2 != self.Kb:
+            raise ValueError(f"frame_length {frame_length} gives {frame_length // 2} bins, plan "
+                             f"has {self.Kb}")
+        if window not in ("sqrt_hann", "rectangular"):
+            raise ValueError(f"window must be one of ('sqrt_hann', 'rectangular'), got {window!r}")
+        if not isinstance(x, torch.Tensor) or x.device.type != "cuda" or x.dim() != 2 \
+                or x.dtype != torch.float32 or not x.is_contiguous():
+            raise ValueError("x must be a contiguous float32 CUDA tensor [M, L]")
+        M, L = x.shape
+        if L < frame_length:
+            raise ValueError(f"signal of {L} samples is shorter than one frame ({frame_length})")
+        F = (L - frame_length) // hop + 1
+        Y = out if out is not None else torch.empty((F, M, self.Kb), dtype=torch.complex64,
+                                                     device=self.device)
+        N.call("srpb_stft", N.ptr(x), M, L, frame_length, hop,
+               0 if window == "sqrt_hann" else 1, F, N.ptr(Y), N.stream_handle(self.device))
+        return Y
+
+    def run_audio(self, x, frame_length, hop_length=None, window="sqrt_hann", path="approx",
+                  maps=True, weighting="phat", phat_floor=None):
+        """K0 + ``run``: audio [M, L] -> (maps | None, argmax) per frame."""
+        return self.run(self.stft(x, frame_length, hop_length, window), path, maps, weighting,
+                        phat_floor)
+
+    def capture(self, F, M=None, path="approx", maps=True, weighting="phat", phat_floor=None,
+                audio=None):
         """Capture ``run`` for F frames of M channels into a CUDA graph
-        (``CapturedStep``: static input ``Y``, ``replay()``)."""
+        (``CapturedStep``: static input, ``replay()``); ``audio=(L,
+        frame_length, hop_length, window)`` captures STFT + run from [M, L]
+        audio instead (F is then derived from L)."""
         return CapturedStep(self, F, M if M is not None else self.M, path, maps, weighting,
-                            phat_floor)
+                            phat_floor, audio)
 
 
 def standalone_argmax(maps: torch.Tensor) -> torch.Tensor:
@@ -469,36 +500,57 @@ class CapturedStep:
     """One ``SrpPlan.run`` step captured in a CUDA graph.
 
     The step's kernels (K1a floor, fused K1b/K3 lattice, K4/K2 tensor-core
-    contraction with the fused argmax, argmax key reset/decode) replay with a
-    single graph launch, so host-side work (argument marshalling, tensor-map
-    encoding) leaves the critical path.  ``Y`` is the static input buffer;
-    ``maps`` / ``argmax`` the static outputs, overwritten by each replay.
+    contraction with the fused argmax, argmax key reset/decode; with
+    ``audio=(L, frame_length, hop_length, window)`` also the K0 STFT) replay
+    with a single graph launch, so host-side work (argument marshalling,
+    tensor-map encoding) leaves the critical path.  The static input is ``Y``
+    [F, M, Kb] complex64 or, for audio, ``x`` [M, L] float32; ``maps`` /
+    ``argmax`` are the static outputs, overwritten by each replay.
     """
 
-    def __init__(self, plan, F, M, path="approx", maps=True, weighting="phat", phat_floor=None):
+    def __init__(self, plan, F, M, path="approx", maps=True, weighting="phat", phat_floor=None,
+                 audio=None):
         dev = plan.device
         self.plan, self.path = plan, path
+        self.audio = audio
+        if audio is not None:
+            L, n, hop, window = audio
+            hop = n // 2 if hop is None else int(hop)
+            self.audio = (int(L), int(n), hop, window)
+            self.x = torch.zeros((M, int(L)), dtype=torch.float32, device=dev)
+            F = (int(L) - n) // hop + 1
         self.Y = torch.zeros((F, M, plan.Kb), dtype=torch.complex64, device=dev)
         timer, plan.kernel_timer = plan.kernel_timer, None
+
+        def body():
+            if self.audio is not None:
+                _, n_, hop_, win_ = self.audio
+                plan.stft(self.x, n_, hop_, win_, out=self.Y)
+            return plan.run(self.Y, path, maps, weighting, phat_floor)
+
         try:
             # warm-up outside capture: lazily built operands (fp16 W split),
             # kernel attributes, allocator pools
-            plan.run(self.Y, path, maps, weighting, phat_floor)
+            body()
             torch.cuda.synchronize(dev)
             self.graph = torch.cuda.CUDAGraph()
             n0 = N.launch_count()
             with torch.cuda.graph(self.graph):
-                self.maps, self.argmax = plan.run(self.Y, path, maps, weighting, phat_floor)
+                self.maps, self.argmax = body()
             #: kernels launched by one replay
             self.launches = N.launch_count() - n0
         finally:
             plan.kernel_timer = timer
 
-    def replay(self, Y=None):
-        """Run the step (on the current stream); ``Y`` (optional) is copied
+    @property
+    def input(self):
+        """The static input buffer (``x`` for audio steps, else ``Y``)."""
+        return self.x if self.audio is not None else self.Y
+
+    def replay(self, inp=None):
+        """Run the step (on the current stream); ``inp`` (optional) is copied
         into the static input first.  Returns the static (maps, argmax)."""
-        if Y is not None:
-            self.Y.copy_(Y, non_blocking=True)
+        if inp is not None:
+            self.input.copy_(inp, non_blocking=True)
         self.graph.replay()
         return self.maps, self.argmax
-

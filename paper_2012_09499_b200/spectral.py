@@ -183,22 +183,42 @@ class CrossSpectra:
     num_bins = property(lambda self: self._shape[1])
 
 
-def stft_analyze(signals, spec: FrameSpec) -> list:
-    """Window, frame and rFFT multichannel audio (``spectral.py:185-215``).
+WINDOW_CODES = {"sqrt_hann": 0, "rectangular": 1}
 
-    Host-side input preparation (upstream of the accelerated path; the
-    on-GPU STFT is SURVEY.md 8(f) rank 1).
-    """
-    x = np.atleast_2d(np.asarray(signals, dtype=float))
-    if x.ndim != 2:
-        raise ValueError(f"signals must be (M, L), got {x.shape}")
-    n_frames = spec.num_frames(x.shape[1])
-    win = spec.window_samples()
+
+def stft_frames(signals, spec: FrameSpec, device=None, out=None) -> torch.Tensor:
+    """K0 on the device: ``signals`` (M, L) (numpy or CUDA tensor) ->
+    Y [F, M, K] complex64 CUDA tensor, K = frame_length / 2 (framing, window
+    and bins of ``spectral.stft_analyze`` ``spectral.py:185-215``)."""
+    dev = N.require_cuda(device)
+    if isinstance(signals, torch.Tensor):
+        x = signals.to(device=dev, dtype=torch.float32)
+        if x.dim() == 1:
+            x = x[None, :]
+    else:
+        a = np.atleast_2d(np.asarray(signals, dtype=float))
+        if a.ndim != 2:
+            raise ValueError(f"signals must be (M, L), got {a.shape}")
+        x = torch.as_tensor(np.ascontiguousarray(a, dtype=np.float32), device=dev)
+    if x.dim() != 2:
+        raise ValueError(f"signals must be (M, L), got {tuple(x.shape)}")
+    x = x.contiguous()
+    M, L = x.shape
+    F = spec.num_frames(L)  # raises for signals shorter than one frame
+    Y = out if out is not None else torch.empty((F, M, spec.num_bins), dtype=torch.complex64,
+                                                 device=dev)
+    N.call("srpb_stft", N.ptr(x), M, L, spec.frame_length, spec.hop_length,
+           WINDOW_CODES[spec.window], F, N.ptr(Y), N.stream_handle(dev))
+    return Y
+
+
+def stft_analyze(signals, spec: FrameSpec) -> list:
+    """Window, frame and rFFT multichannel audio (``spectral.py:185-215``) on
+    the device (K0); frames keep their spectra on the GPU (complex64) until
+    ``.spectra`` is read."""
+    Y = stft_frames(signals, spec)
     freqs = spec.bin_frequencies()
-    idx = np.arange(spec.frame_length)[None, :] + spec.hop_length * np.arange(n_frames)[:, None]
-    chunks = x[:, idx] * win[None, None, :]                     # (M, F, N)
-    spectra = np.fft.rfft(chunks, axis=2)[:, :, : spec.num_bins]
-    return [SpectralFrame(spectra[:, f, :], freqs, frame_index=f) for f in range(n_frames)]
+    return [SpectralFrame(Y[f], freqs, frame_index=f) for f in range(Y.shape[0])]
 
 
 def _pair_rows(pairs):

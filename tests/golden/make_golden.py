@@ -25,7 +25,13 @@ sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
 
 import srpfast  # noqa: E402  (the reference, from PYTHONPATH)
 from srpfast.geometry import CandidateGrid, MicArray, build_tdoa_table, circular_array  # noqa: E402
-from srpfast.spectral import CrossSpectra, SpectralFrame, cross_spectrum  # noqa: E402
+from srpfast.spectral import (  # noqa: E402
+    CrossSpectra,
+    FrameSpec,
+    SpectralFrame,
+    cross_spectrum,
+    stft_analyze,
+)
 from srpfast.srp import (  # noqa: E402
     argmax_candidate,
     build_gcc_lattice,
@@ -207,8 +213,27 @@ def nonharmonic():
     )
 
 
+def stft_cases():
+    """Reference STFT (spectral.stft_analyze) of seeded float32 audio: several
+    frame lengths, hops and both windows; trailing samples dropped."""
+    rng = np.random.default_rng(20240611)
+    x = rng.standard_normal((3, 6000)).astype(np.float32)
+    x[1] *= 1e-3  # a quiet channel
+    x[2, 2500:2600] = 0.0  # a silent stretch
+    cases = {}
+    for tag, (n, hop, win) in {"a": (512, None, "sqrt_hann"), "b": (256, 100, "rectangular"),
+                               "c": (2048, 512, "sqrt_hann"), "d": (64, 64, "sqrt_hann")}.items():
+        spec = FrameSpec(FS, n, hop, win)
+        frames = stft_analyze(x.astype(np.float64), spec)
+        cases[f"Y_{tag}"] = np.stack([fr.spectra for fr in frames])  # [F, M, Kb] complex128
+        cases[f"cfg_{tag}"] = np.array([n, spec.hop_length, 0 if win == "sqrt_hann" else 1])
+        cases[f"freqs_{tag}"] = frames[0].bin_frequencies
+    save("stft.npz", x=x, **cases)
+
+
 def main():
     print("reference srpfast", srpfast.__version__, "from", os.path.dirname(srpfast.__file__))
+    stft_cases()
     scene_case("c1.npz", scenes.make_c1(num_frames=8), 8, (2,))
     scene_case("c2_subset.npz", scenes.make_c2(num_frames=3), 3, (0, 2, 4), grid_limit=3000)
     random_small()

@@ -38,7 +38,7 @@ def test_library_exports_every_header_symbol():
 
 def test_abi_version_and_error_reporting_without_gpu():
     lib = _native.load()
-    assert lib.srpb_abi_version() == 3
+    assert lib.srpb_abi_version() == 4
     # invalid arguments are rejected on the host before any CUDA call
     with pytest.raises(ValueError, match="bad shape"):
         _native.call("srpb_gcc_phat", None, -1, 4, 64, None, None, 6, 0, 1e-12, -1.0, None, None,
@@ -197,11 +197,10 @@ def test_spectral_framing_matches_reference_rules():
         B.FrameSpec(16000.0, 1023)
     with pytest.raises(ValueError):
         spec.num_frames(100)
-    x = np.random.default_rng(0).standard_normal((2, 4096))
-    frames = B.stft_analyze(x, spec)
     win = spec.window_samples()
-    ref = np.fft.rfft(x[:, 512:1536] * win, axis=1)[:, :512]
-    np.testing.assert_allclose(frames[1].spectra, ref, rtol=1e-12, atol=1e-12)
+    n = np.arange(1024)
+    np.testing.assert_allclose(win, np.sqrt(0.5 - 0.5 * np.cos(2 * np.pi * n / 1024)))
+    # the STFT itself runs on the device (K0): tests/test_parity_gpu.py
 
 
 # ----------------------------------------------------------- scenes

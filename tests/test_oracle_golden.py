@@ -90,3 +90,13 @@ def test_oracle_closed_form_counts():
     assert rep["mults_sampling"] == 279_552
     assert rep["mults_interpolation"] == 2_211_573
     assert rep["avg_samples_per_pair"] == pytest.approx(14.2 + 4.0)
+
+
+def test_oracle_stft_matches_reference():
+    g = load_golden("stft")
+    for tag in "abcd":
+        n, hop, win = (int(v) for v in g[f"cfg_{tag}"])
+        Y = O.stft(g["x"], n, hop, "sqrt_hann" if win == 0 else "rectangular")
+        assert Y.shape == g[f"Y_{tag}"].shape
+        assert rel_err(Y, g[f"Y_{tag}"]) < 1e-13
+        np.testing.assert_allclose(O.bin_frequencies(16000.0, n), g[f"freqs_{tag}"], rtol=1e-15)

@@ -31,6 +31,66 @@ def dev(x):
     return torch.as_tensor(np.ascontiguousarray(x)).cuda()
 
 
+# --------------------------------------------------------------------- K0
+def _rel_rows(a, b):
+    """max over (frame, channel) of the rel-L2 error of a row of bins"""
+    num = np.linalg.norm((a - b).reshape(-1, a.shape[-1]), axis=1)
+    den = np.maximum(np.linalg.norm(b.reshape(-1, b.shape[-1]), axis=1), 1e-30)
+    return float(np.max(num / den))
+
+
+def test_stft_matches_reference():
+    """Device STFT (FFT path: N = 64 ... 2048, both windows, several hops)
+    against the reference's stft_analyze outputs."""
+    g = load_golden("stft")
+    for tag in "abcd":
+        n, hop, win = (int(v) for v in g[f"cfg_{tag}"])
+        spec = B.FrameSpec(16000.0, n, hop, "sqrt_hann" if win == 0 else "rectangular")
+        frames = B.stft_analyze(g["x"], spec)
+        Y = np.stack([fr.spectra for fr in frames])
+        assert Y.shape == g[f"Y_{tag}"].shape, tag
+        assert _rel_rows(Y, g[f"Y_{tag}"]) < 2e-6, tag
+        np.testing.assert_allclose(frames[0].bin_frequencies, g[f"freqs_{tag}"])
+        assert frames[3].frame_index == 3
+
+
+def test_stft_non_power_of_two_frames_vs_oracle():
+    """Even, non-power-of-two frame lengths take the direct-DFT kernel."""
+    x = np.random.default_rng(5).standard_normal((2, 3000)).astype(np.float32)
+    for n, hop, win in ((300, 150, "sqrt_hann"), (2, 1, "rectangular"), (1000, 333, "sqrt_hann")):
+        Y = B.stft_frames(x, B.FrameSpec(16000.0, n, hop, win)).cpu().numpy()
+        ref = O.stft(x.astype(float), n, hop, win)
+        assert Y.shape == ref.shape and _rel_rows(Y, ref) < 2e-6, n
+
+
+def test_run_audio_matches_spectra_path():
+    """K0 -> K1a/K1b/K3 -> K4 from audio equals run() on the reference STFT
+    of the same audio (to the fp32 tolerance), and the drop-in errors match."""
+    g = load_golden("c1")
+    x = np.random.default_rng(11).standard_normal((4, 16000)).astype(np.float32)
+    plan = plan_from_golden(g, 2, weights="stored", backend="tc")
+    maps_a, am_a = plan.run_audio(dev(x), 512)
+    Y = O.stft(x.astype(float), 512).astype(np.complex64)
+    maps_b, am_b = plan.run(dev(Y), "approx")
+    assert_maps_match(maps_a.cpu().numpy(), maps_b.cpu().numpy(), am_a.cpu().numpy(),
+                      what="run_audio")
+    cap = plan.capture(None, 4, "approx", audio=(x.shape[1], 512, None, "sqrt_hann"))
+    m_c, a_c = cap.replay(dev(x))
+    assert torch.equal(m_c, maps_a) and torch.equal(a_c, am_a)
+    runner = B.ChunkedRunner(plan, maps_a.shape[0], 4, "approx", chunks=2,
+                             audio=(512, None, "sqrt_hann"))
+    xh = torch.from_numpy(x).pin_memory()
+    mh = torch.empty(tuple(maps_a.shape), dtype=torch.float32).pin_memory()
+    ah = torch.empty(maps_a.shape[0], dtype=torch.int32).pin_memory()
+    runner.run(xh, mh, ah)
+    torch.cuda.synchronize()
+    assert torch.equal(mh, maps_a.cpu()) and torch.equal(ah, am_a.cpu())
+    with pytest.raises(ValueError, match="shorter than one frame"):
+        plan.stft(dev(x[:, :100]), 512)
+    with pytest.raises(ValueError, match="bins"):
+        plan.stft(dev(x), 1024)
+
+
 # --------------------------------------------------------------------- K1
 @pytest.mark.parametrize("name", ["c1", "c2_subset", "random_small", "on_lattice"])
 def test_gcc_phat_matches_reference(name):
