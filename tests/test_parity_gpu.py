@@ -56,8 +56,9 @@ def test_stft_matches_reference():
 
 def test_stft_non_power_of_two_frames_vs_oracle():
     """Even, non-power-of-two frame lengths take the direct-DFT kernel."""
-    x = np.random.default_rng(5).standard_normal((2, 3000)).astype(np.float32)
-    for n, hop, win in ((300, 150, "sqrt_hann"), (2, 1, "rectangular"), (1000, 333, "sqrt_hann")):
+    x = np.random.default_rng(5).standard_normal((2, 9000)).astype(np.float32)
+    for n, hop, win in ((300, 150, "sqrt_hann"), (2, 1, "rectangular"), (1000, 333, "sqrt_hann"),
+                        (256, 77, "sqrt_hann"), (4096, 1001, "rectangular")):  # FFT, odd hops
         Y = B.stft_frames(x, B.FrameSpec(16000.0, n, hop, win)).cpu().numpy()
         ref = O.stft(x.astype(float), n, hop, win)
         assert Y.shape == ref.shape and _rel_rows(Y, ref) < 2e-6, n
