@@ -43,6 +43,24 @@ int srpb_abi_version(void);
 const char* srpb_last_error(void);
 
 /*
+ * Plan build on the device: candidate TDOAs (geometry.build_tdoa_table,
+ * geometry.py:365-398; near field |q - p_m| - |q - p_m'| over c, far field
+ * (p_m - p_m') . r / c) and their splits, fp64 in the reference's operation
+ * order: conventional x = (omega1 tau) period / 2pi -> conv_ti = rint(x) mod
+ * period, conv_tf = x - rint(x); sinc x = tau / sample_period -> sx_i, sx_f
+ * (srp.py:310).  Layout [P, J] (candidates fastest); tau [J, P] optional.
+ *   mic_pos [M, 3], points [J, 3] float64 (unit directions for far field)
+ *   bounds [P] float64 (pair distance / c); *violation set to 1 when some
+ *   |tau| > bound + slack (the reference raises AssertionError)
+ * Any of the (conv_ti, conv_tf), (sx_i, sx_f), tau outputs may be NULL.
+ */
+int srpb_tdoa_split(const double* mic_pos, int M, const double* points, int J,
+                    const int32_t* pair_m, const int32_t* pair_mp, int P, int far_field,
+                    double speed_of_sound, double omega1, int period, double sample_period,
+                    const double* bounds, double slack, int32_t* conv_ti, float* conv_tf,
+                    int32_t* sx_i, float* sx_f, double* tau, int* violation, void* stream);
+
+/*
  * K0 STFT on the device.  Replaces spectral.stft_analyze (spectral.py:185-215)
  * with FrameSpec's framing and window (:35-99): frame f covers samples
  * [f hop, f hop + N), periodic sqrt-Hann (window 0) or rectangular (1),

@@ -21,6 +21,9 @@ c_int, c_double, c_void_p = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
 _SIGNATURES = {
     "srpb_abi_version": [],
     "srpb_last_error": [],
+    "srpb_tdoa_split": [c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
+                        c_double, c_double, c_int, c_double, c_void_p, c_double, c_void_p,
+                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     "srpb_stft": [c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p],
     "srpb_gcc_phat": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
                       c_double, c_double, c_void_p, c_void_p, c_void_p],

@@ -11,6 +11,9 @@ namespace srpb {
 cudaError_t launch_gcc_phat(const float*, int, int, int, const int32_t*, const int32_t*, int, int,
                             double, double, float*, double*, cudaStream_t);
 cudaError_t launch_stft(const float*, int, int, int, int, int, int, float*, cudaStream_t);
+cudaError_t launch_tdoa_split(const double*, const double*, int, const int32_t*, const int32_t*,
+                              int, int, double, double, int, double, const double*, double,
+                              int32_t*, float*, int32_t*, float*, double*, int*, cudaStream_t);
 cudaError_t launch_gcc_floor(const float*, int, int, int, const int32_t*, const int32_t*, int,
                              double, double*, int32_t*, cudaStream_t);
 cudaError_t launch_lattice_from_spectra(const float*, int, int, int, const int32_t*,
@@ -86,7 +89,7 @@ static bool pow2_scale(float s) {
   return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
 }
 
-int srpb_abi_version(void) { return 4; }
+int srpb_abi_version(void) { return 5; }
 
 const char* srpb_last_error(void) { return g_err; }
 
@@ -107,6 +110,26 @@ int srpb_stft(const float* x, int M, int L, int frame_length, int hop, int windo
   REQUIRE(x && Y, "srpb_stft: null pointer");
   return status(srpb::launch_stft(x, M, L, frame_length, hop, window, F, Y, S(stream)),
                 "srpb_stft");
+}
+
+int srpb_tdoa_split(const double* mic_pos, int M, const double* points, int J,
+                    const int32_t* pair_m, const int32_t* pair_mp, int P, int far_field,
+                    double speed_of_sound, double omega1, int period, double sample_period,
+                    const double* bounds, double slack, int32_t* conv_ti, float* conv_tf,
+                    int32_t* sx_i, float* sx_f, double* tau, int* violation, void* stream) {
+  REQUIRE(M >= 2 && J >= 0 && P >= 1, "srpb_tdoa_split: bad shape M=%d J=%d P=%d", M, J, P);
+  REQUIRE(speed_of_sound > 0.0, "srpb_tdoa_split: speed_of_sound must be positive");
+  REQUIRE(!conv_ti == !conv_tf && !sx_i == !sx_f, "srpb_tdoa_split: split outputs go in pairs");
+  REQUIRE(!conv_ti || (period >= 1 && period <= 46340 && omega1 > 0.0),
+          "srpb_tdoa_split: conventional split needs period in [1, 46340] and omega1 > 0");
+  REQUIRE(!sx_i || sample_period > 0.0, "srpb_tdoa_split: sinc split needs sample_period > 0");
+  REQUIRE(J == 0 || (mic_pos && points && pair_m && pair_mp && bounds && violation),
+          "srpb_tdoa_split: null pointer");
+  return status(srpb::launch_tdoa_split(mic_pos, points, J, pair_m, pair_mp, P, far_field,
+                                        speed_of_sound, omega1, period, sample_period, bounds,
+                                        slack, conv_ti, conv_tf, sx_i, sx_f, tau, violation,
+                                        S(stream)),
+                "srpb_tdoa_split");
 }
 
 int srpb_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pair_m,

@@ -26,6 +26,7 @@ import numpy as np
 import torch
 
 from . import _native as N
+from .geometry import TDOA_BOUND_SLACK
 
 DEFAULT_PHAT_FLOOR_REL = 1e-12  # spectral.py:31-32
 #: store W when it needs at most this many bytes (else generate on the fly)
@@ -85,7 +86,7 @@ class SrpPlan:
     def __init__(self, tdoa_table, pair_m, pair_mp, tdoa_bounds, bin_frequencies,
                  sample_period=None, n_aux=None, weights="auto", device=None,
                  max_weight_bytes=DEFAULT_MAX_WEIGHT_BYTES, conventional=True, backend="auto",
-                 kb_per_group=4, interp_kb_per_group=10, precision="auto"):
+                 kb_per_group=4, interp_kb_per_group=10, precision="auto", _geometry=None):
         self.device = N.require_cuda(device)
         if precision not in ("auto", "tf32"):
             raise ValueError(f"precision must be auto|tf32, got {precision!r}")
@@ -105,11 +106,18 @@ class SrpPlan:
         self.interp_kb_per_group16 = self.interp_kb_per_group
         self.W_hi = self.W_lo = None
         self.W16 = None
-        table = np.asarray(tdoa_table, dtype=np.float64)
         omega = np.asarray(bin_frequencies, dtype=np.float64)
-        if table.ndim != 2 or table.shape[0] == 0:
-            raise ValueError(f"tdoa_table must have shape (J, P), got {table.shape}")
-        self.J, self.P = table.shape
+        self._geom = _geometry
+        if _geometry is not None:  # TDOAs and splits computed on the device
+            table = None
+            self.J, self.P = int(_geometry["points"].shape[0]), len(pair_m)
+            if self.J == 0:
+                raise ValueError("the candidate grid is empty")
+        else:
+            table = np.asarray(tdoa_table, dtype=np.float64)
+            if table.ndim != 2 or table.shape[0] == 0:
+                raise ValueError(f"tdoa_table must have shape (J, P), got {table.shape}")
+            self.J, self.P = table.shape
         self.Kb = omega.size
         if len(pair_m) != self.P or len(pair_mp) != self.P or len(tdoa_bounds) != self.P:
             raise ValueError(f"grid table has {self.P} pair columns, expected {len(pair_m)}")
@@ -134,8 +142,44 @@ class SrpPlan:
                                 weights, max_weight_bytes)
 
     # ------------------------------------------------------------------ build
+    def _device_split(self, conv=False, sinc=False, tau=False):
+        """srpb_tdoa_split from the plan's device geometry: returns the
+        requested (conv_ti, conv_tf), (sx_i, sx_f), tau tensors."""
+        g, dev = self._geom, self.device
+        J, P = self.J, self.P
+        out = {}
+        if conv:
+            out["conv"] = (torch.empty((P, J), dtype=torch.int32, device=dev),
+                           torch.empty((P, J), dtype=torch.float32, device=dev))
+        if sinc:
+            out["sinc"] = (torch.empty((P, J), dtype=torch.int32, device=dev),
+                           torch.empty((P, J), dtype=torch.float32, device=dev))
+        if tau:
+            out["tau"] = torch.empty((J, P), dtype=torch.float64, device=dev)
+        viol = torch.zeros(1, dtype=torch.int32, device=dev)
+        ci, cf = out.get("conv", (None, None))
+        si, sf = out.get("sinc", (None, None))
+        N.call("srpb_tdoa_split", N.ptr(g["pos"]), g["pos"].shape[0], N.ptr(g["points"]), J,
+               N.ptr(self.pair_m), N.ptr(self.pair_mp), P, 1 if g["far_field"] else 0,
+               float(g["c"]), float(self.omega[1]) if self.Kb > 1 else 0.0, self.period,
+               float(getattr(self, "sample_period", None) or 0.0), N.ptr(g["bounds"]),
+               TDOA_BOUND_SLACK,
+               N.ptr(ci), N.ptr(cf), N.ptr(si), N.ptr(sf), N.ptr(out.get("tau")), N.ptr(viol),
+               N.stream_handle(dev))
+        if int(viol.item()) != 0:
+            raise AssertionError("TDOA magnitude exceeded its physical bound")
+        return out
+
     def _build_conventional(self, table):
         dev = self.device
+        if self._geom is not None:
+            if self.harmonic:
+                self.conv_ti, self.conv_tf = self._device_split(conv=True)["conv"]
+            else:
+                self.omega_dev = torch.as_tensor(self.omega, device=dev)
+                self.tau_dev = self._device_split(tau=True)["tau"]
+            self._conv_ready = True
+            return
         if self.harmonic:
             # x = w_1 tau N / 2pi: theta_k / 2pi = k x / N (srp.py:370-372)
             x = np.ascontiguousarray((self.omega[1] * table.T) * self.period / (2.0 * math.pi))
@@ -164,12 +208,15 @@ class SrpPlan:
         N.call("srpb_lattice_twiddles", N.ptr(self.omega_dev), self.Kb, T, self.L,
                N.ptr(self.twiddles), s)
         # sinc split x = tau / T (srp.py:310)
-        xs = np.ascontiguousarray(table.T) / T
-        i, f = split_rint(xs)
-        if np.any(np.abs(i) > 2**30):
-            raise ValueError("tdoa / sample_period out of int32 range")
-        self.sx_i = torch.as_tensor(np.ascontiguousarray(i, dtype=np.int32), device=dev)
-        self.sx_f = torch.as_tensor(np.ascontiguousarray(f), device=dev)
+        if self._geom is not None:
+            self.sx_i, self.sx_f = self._device_split(sinc=True)["sinc"]
+        else:
+            xs = np.ascontiguousarray(table.T) / T
+            i, f = split_rint(xs)
+            if np.any(np.abs(i) > 2**30):
+                raise ValueError("tdoa / sample_period out of int32 range")
+            self.sx_i = torch.as_tensor(np.ascontiguousarray(i, dtype=np.int32), device=dev)
+            self.sx_f = torch.as_tensor(np.ascontiguousarray(f), device=dev)
         need = self.J * t_pad * 4
         if weights not in ("auto", "stored", "onthefly"):
             raise ValueError(f"weights must be auto|stored|onthefly, got {weights!r}")
@@ -441,6 +488,35 @@ class SrpPlan:
                 return self._approx_tc(xh, xl, out, self._keys(F))
             return self.approx(self.lattice_from_spectra(Y, weighting, phat_floor), maps)
         raise ValueError(f"unknown path {path!r}")
+
+    @classmethod
+    def from_geometry(cls, mic_positions, points, bin_frequencies, speed_of_sound=340.0,
+                      far_field=False, pair_m=None, pair_mp=None, **kw):
+        """Build a plan without a host TDOA table: the candidate TDOAs and
+        their phase / sinc splits are computed on the device
+        (``srpb_tdoa_split``; geometry.build_tdoa_table ``geometry.py:365-398``).
+        Pairs default to the canonical order (``geometry.py:141-176``);
+        bounds are pair distance / c.  ``points`` are candidate positions
+        (near field) or unit directions (far field).  Other keywords as in
+        ``SrpPlan``."""
+        pos = np.ascontiguousarray(mic_positions, dtype=np.float64)
+        pts = np.ascontiguousarray(points, dtype=np.float64)
+        if pos.ndim != 2 or pos.shape[1] != 3 or pts.ndim != 2 or pts.shape[1] != 3:
+            raise ValueError("mic_positions and points must be (M, 3) and (J, 3)")
+        if pair_m is None:
+            pairs = [(m, mp) for mp in range(pos.shape[0]) for m in range(mp + 1, pos.shape[0])]
+            pair_m = np.array([m for m, _ in pairs], dtype=np.int32)
+            pair_mp = np.array([mp for _, mp in pairs], dtype=np.int32)
+        pm, pmp = np.asarray(pair_m), np.asarray(pair_mp)
+        dist = np.linalg.norm(pos[pm] - pos[pmp], axis=1)
+        if np.any(dist == 0.0):
+            raise ValueError("coincident microphones in a pair")
+        bounds = dist / speed_of_sound
+        dev = N.require_cuda(kw.get("device"))
+        geom = {"pos": torch.as_tensor(pos, device=dev), "points": torch.as_tensor(pts, device=dev),
+                "far_field": bool(far_field), "c": float(speed_of_sound),
+                "bounds": torch.as_tensor(bounds, device=dev)}
+        return cls(None, pm, pmp, bounds, bin_frequencies, _geometry=geom, **kw)
 
     def stft(self, x, frame_length, hop_length=None, window="sqrt_hann", out=None):
         """K0: audio ``x`` [M, L] float32 (CUDA) -> Y [F, M, frame_length/2]

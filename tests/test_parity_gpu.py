@@ -366,6 +366,45 @@ def test_config_shapes_vs_oracle(cfg, backend):
     assert_maps_match(maps.cpu().numpy(), approx_ref, am.cpu().numpy(), what=f"{cfg} run")
 
 
+# --------------------------------------------- device geometry (plan build)
+def test_plan_from_geometry_matches_host_table():
+    """TDOAs + phase/sinc splits computed on the device equal the host path
+    (reference operation order, fp64): identical splits, identical maps."""
+    scene = scenes.make_c2(num_frames=4)
+    pts = scene.grid[::7]
+    arr = B.MicArray(scene.mic_pos, speed_of_sound=343.0)
+    grid = B.build_tdoa_table(arr, B.CandidateGrid("near_field", pts))
+    pm = np.array([p.index_m for p in arr.pairs], np.int32)
+    pmp = np.array([p.index_m_prime for p in arr.pairs], np.int32)
+    bounds = np.array([p.tdoa_bound for p in arr.pairs])
+    omega = O.bin_frequencies(16000.0, 1024)
+    host = SrpPlan(grid.tdoa_table, pm, pmp, bounds, omega, sample_period=T, n_aux=4,
+                   weights="stored")
+    devp = SrpPlan.from_geometry(scene.mic_pos, pts, omega, speed_of_sound=343.0,
+                                 sample_period=T, n_aux=4, weights="stored")
+    for name in ("conv_ti", "conv_tf", "sx_i", "sx_f"):
+        a, b = getattr(host, name), getattr(devp, name)
+        mism = int((a != b).sum().item())
+        assert mism <= a.numel() // 100000, (name, mism)  # exact up to rare rounding ties
+    Y = dev(scene.Y)
+    for path in ("approx", "conventional"):
+        m1, a1 = host.run(Y, path)
+        m2, a2 = devp.run(Y, path)
+        assert_maps_match(m2.cpu().numpy(), m1.cpu().numpy(), a2.cpu().numpy(), what=path)
+    # far field (unit directions) against the host table
+    dirs = np.random.default_rng(2).standard_normal((500, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    gf = B.build_tdoa_table(arr, B.CandidateGrid("far_field", dirs))
+    pf = SrpPlan.from_geometry(scene.mic_pos, dirs, omega, speed_of_sound=343.0, far_field=True)
+    hf = SrpPlan(gf.tdoa_table, pm, pmp, bounds, omega)
+    assert int((pf.conv_ti != hf.conv_ti).sum().item()) <= 2
+    assert float((pf.conv_tf - hf.conv_tf).abs().max().item()) < 1e-6
+    # a point outside the physical bound raises like the reference
+    with pytest.raises(AssertionError, match="exceeded"):
+        SrpPlan.from_geometry(scene.mic_pos, dirs * 2.0, omega, speed_of_sound=343.0,
+                              far_field=True)
+
+
 # ------------------------------------ size-independent properties at full C2
 def test_full_c2_frame_sharding_and_determinism():
     """BASELINE config C2 at full size (J=50k, F=311): maps are independent
