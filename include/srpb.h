@@ -164,9 +164,16 @@ int srpb_lattice(const float* Psi, int F, int P, int Kb, const float* tw, int L,
  * cross-spectra are formed in the lattice kernel's staging pass and never
  * stored (spectral.cross_spectrum spectral.py:218-285 feeding
  * srp.build_gcc_lattice srp.py:201-247).
- *   floors [F] float64 (srpb_gcc_floor) for PHAT with the relative floor, or
- *   NULL with abs_floor > 0 (explicit floor); ignored for identity weighting.
+ *   PHAT floor: floors [F] float64 (srpb_gcc_floor), or NULL with
+ *   abs_floor > 0 (explicit floor), or NULL with abs_floor <= 0: the
+ *   relative floor floor_rel * sqrt(mean |raw|^2) is applied speculatively --
+ *   the lattice runs unfloored while accumulating per-(frame, pair) |raw|^2
+ *   statistics, and a fix-up pass recomputes exactly every frame in which a
+ *   bin could fall below the floor or a power leaves the fast path's range
+ *   (identical results, no floor pass).  Ignored for identity weighting.
  *   clean [F] int32 (srpb_gcc_floor) or NULL (every bin range-tested).
+ *   spec_scratch: 12 F P bytes for the speculative floor's statistics, or
+ *   NULL (then allocated stream-ordered per call).
  *   tw 16-byte aligned.
  *   Xi [F, T_pad] float32 out and/or Xi_hi, Xi_lo [F, T_pad]: its operand
  *   split for the tensor-core K4 -- split_scale == 0: tf32 floats
@@ -177,7 +184,8 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
                               const int32_t* pair_mp, int P, int weighting, const double* floors,
                               double abs_floor, const int32_t* clean, const float* tw, int L,
                               const int32_t* off, const int32_t* reach, int T_pad, float* Xi,
-                              void* Xi_hi, void* Xi_lo, float split_scale, void* stream);
+                              void* Xi_hi, void* Xi_lo, float split_scale, double floor_rel,
+                              void* spec_scratch, void* stream);
 
 /*
  * Sinc interpolation table W[j, off[p] + n + reach[p]] = sinc(x[j,p] - n),

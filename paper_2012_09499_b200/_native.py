@@ -39,7 +39,7 @@ _SIGNATURES = {
     "srpb_lattice_from_spectra": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
                                   c_void_p, c_double, c_void_p, c_void_p, c_int, c_void_p,
                                   c_void_p, c_int, c_void_p, c_void_p, c_void_p, ctypes.c_float,
-                                  c_void_p],
+                                  c_double, c_void_p, c_void_p],
     "srpb_sinc_table": [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p,
                         c_void_p],
     "srpb_interp": [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],
@@ -111,8 +111,9 @@ def stream_handle(device=None):
 
 
 _LAUNCHING = {n for n in _SIGNATURES if n not in ("srpb_abi_version", "srpb_last_error")}
-# entry points that launch more than one kernel (floor/fill pass + psi pass)
-_KERNELS_PER_CALL = {"srpb_gcc_phat": 2}
+# entry points that launch more than one kernel (floor/fill pass + psi pass;
+# speculative-floor lattice + its fix-up pass)
+_KERNELS_PER_CALL = {"srpb_gcc_phat": 2, "srpb_lattice_from_spectra": 2}
 _launches = 0
 
 

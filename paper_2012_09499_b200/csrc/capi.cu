@@ -20,7 +20,7 @@ cudaError_t launch_lattice_from_spectra(const float*, int, int, int, const int32
                                         const int32_t*, int, int, const double*, double,
                                         const int32_t*, const float*, int, const int32_t*,
                                         const int32_t*, int, int, float*, void*, void*, float,
-                                        cudaStream_t);
+                                        double, void*, cudaStream_t);
 cudaError_t launch_conventional(const float*, int, int, int, int, const int32_t*, const float*,
                                 int, float*, unsigned long long*, cudaStream_t);
 cudaError_t launch_conventional_general(const float*, int, int, int, const double*,
@@ -89,7 +89,7 @@ static bool pow2_scale(float s) {
   return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
 }
 
-int srpb_abi_version(void) { return 5; }
+int srpb_abi_version(void) { return 7; }
 
 const char* srpb_last_error(void) { return g_err; }
 
@@ -208,13 +208,14 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
                               double abs_floor, const int32_t* clean, const float* tw, int L,
                               const int32_t* off,
                               const int32_t* reach, int T_pad, float* Xi, void* Xi_hi,
-                              void* Xi_lo, float split_scale, void* stream) {
+                              void* Xi_lo, float split_scale, double floor_rel,
+                              void* spec_scratch, void* stream) {
   REQUIRE(F >= 0 && M >= 1 && P >= 1 && Kb >= 1 && L >= 0 && T_pad >= 1,
           "srpb_lattice_from_spectra: bad shape");
   REQUIRE(weighting == SRPB_WEIGHT_PHAT || weighting == SRPB_WEIGHT_IDENTITY,
           "srpb_lattice_from_spectra: unknown weighting %d", weighting);
-  REQUIRE(weighting != SRPB_WEIGHT_PHAT || floors || abs_floor > 0.0,
-          "srpb_lattice_from_spectra: PHAT needs per-frame floors or abs_floor > 0");
+  REQUIRE(weighting != SRPB_WEIGHT_PHAT || floors || abs_floor > 0.0 || floor_rel > 0.0,
+          "srpb_lattice_from_spectra: PHAT needs floors, abs_floor > 0 or floor_rel > 0");
   REQUIRE((Xi_hi == nullptr) == (Xi_lo == nullptr),
           "srpb_lattice_from_spectra: Xi_hi and Xi_lo go together");
   REQUIRE(Xi || Xi_hi, "srpb_lattice_from_spectra: need Xi and/or Xi_hi/Xi_lo output");
@@ -227,7 +228,8 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
   return status(srpb::launch_lattice_from_spectra(Y, F, M, Kb, pair_m, pair_mp, P, weighting,
                                                   floors, abs_floor, clean, tw, L, off, reach,
                                                   2 * L + 1,
-                                                  T_pad, Xi, Xi_hi, Xi_lo, split_scale, S(stream)),
+                                                  T_pad, Xi, Xi_hi, Xi_lo, split_scale, floor_rel,
+                                                  spec_scratch, S(stream)),
                 "srpb_lattice_from_spectra");
 }
 

@@ -128,7 +128,32 @@ __device__ __forceinline__ float2 phat_one(float2 a, float2 b, int weighting, Ph
 }
 
 // Cross-spectrum modes of the fused lattice (CTA-uniform, compile-time):
-enum PsiMode { kPsiStaged = 0, kPsiIdentity = 1, kPsiPhatClean = 2, kPsiPhatChecked = 3 };
+enum PsiMode {
+  kPsiStaged = 0,
+  kPsiIdentity = 1,
+  kPsiPhatClean = 2,
+  kPsiPhatChecked = 3,
+  kPsiPhatSpec = 4  // relative floor deferred: raw/|raw|, stats for the fix-up pass
+};
+
+// Speculative PHAT (kPsiPhatSpec): per-lane statistics over the bins it
+// forms -- sum and min of |raw|^2 over nonzero bins, and whether any power
+// left the range (1e-15, 1e15) where the fast path and |raw|^2 in fp32 are
+// exact.  A frame whose min |raw|^2 could fall below floor^2 = rel^2
+// mean |raw|^2, or with an out-of-range power, is recomputed exactly.
+struct PhatSpecStats {
+  float sum = 0.0f;
+  float min = 3.0e38f;
+  int bad = 0;
+  __device__ __forceinline__ void add(float pa, float pb) {
+    if (pa != 0.0f && pb != 0.0f) {
+      const float q = pa * pb;
+      sum += q;
+      min = fminf(min, q);
+      bad |= !(pa > 1e-15f && pa < 1e15f && pb > 1e-15f && pb < 1e15f);
+    }
+  }
+};
 
 // warp form (all 32 lanes active), same values as phat_one: kPsiPhatClean
 // (every lane's frame flagged clean by K1a) skips the range test;

@@ -107,6 +107,11 @@ struct LatticeArgs {
   void* Xi_lo;   //   split_scale == 0: tf32 hi/lo floats; else fp16 hi/lo of split_scale * Xi
   float split_scale;
   int vec16;     // 16-byte copies (Kb even, 16-byte aligned source)
+  // speculative relative floor (kPsiPhatSpec): per (frame, pair) stats
+  float* spec_sum;  // [F, P] or NULL
+  float* spec_min;
+  int* spec_bad;
+  double floor_rel;
 };
 
 __device__ __forceinline__ void lattice_store(const LatticeArgs& a, size_t idx, float v) {
@@ -236,7 +241,8 @@ __device__ __forceinline__ int psi_slot(int f) {  // float2 offset of frame f in
 // psi of this lane's frame for the warp's 4 bins of chunk c -> psi_w row set
 template <int kMode, int kNch, bool kTma>
 __device__ __forceinline__ void lattice_psi(const LatticeArgs& a, const LatticeWarp& w, int c,
-                                            float2* psi_dst, int my_slot, PhatFloor fl) {
+                                            float2* psi_dst, int my_slot, PhatFloor fl,
+                                            PhatSpecStats& st) {
   const int lane = threadIdx.x & 31;
   const float4* stage = w.ring + (c % kLatStages) * LatGeom<kTma>::kStageW;
   const int kvalid = a.Kb - (c * kLatChunk + w.kbase);  // bins of the slice inside Kb
@@ -244,8 +250,18 @@ __device__ __forceinline__ void lattice_psi(const LatticeArgs& a, const LatticeW
   for (int pr = 0; pr < kLatBinsW / 2; ++pr) {
     const float4 ra = lattice_raw<kTma>(stage, 0, pr, lane);
     const float4 rb = kNch == 2 ? lattice_raw<kTma>(stage, 1, pr, lane) : ra;
-    float2 v0 = psi_warp<kMode>(make_float2(ra.x, ra.y), make_float2(rb.x, rb.y), fl);
-    float2 v1 = psi_warp<kMode>(make_float2(ra.z, ra.w), make_float2(rb.z, rb.w), fl);
+    float2 v0, v1;
+    if constexpr (kMode == kPsiPhatSpec) {
+      const PhatFloor nofloor{0.0, __int_as_float(0x7f800000)};
+      float pa, pb;
+      v0 = phat_fast(make_float2(ra.x, ra.y), make_float2(rb.x, rb.y), nofloor, pa, pb);
+      if (kTma || 2 * pr < kvalid) st.add(pa, pb);
+      v1 = phat_fast(make_float2(ra.z, ra.w), make_float2(rb.z, rb.w), nofloor, pa, pb);
+      if (kTma || 2 * pr + 1 < kvalid) st.add(pa, pb);
+    } else {
+      v0 = psi_warp<kMode>(make_float2(ra.x, ra.y), make_float2(rb.x, rb.y), fl);
+      v1 = psi_warp<kMode>(make_float2(ra.z, ra.w), make_float2(rb.z, rb.w), fl);
+    }
     if (!kTma) {  // clamped copies past Kb (TMA zero-fills them, twiddles included)
       if (2 * pr >= kvalid) v0 = make_float2(0.0f, 0.0f);
       if (2 * pr + 1 >= kvalid) v1 = make_float2(0.0f, 0.0f);
@@ -299,7 +315,8 @@ __device__ __forceinline__ void lattice_fma(const LatticeWarp& w, int c, const f
 template <int kMode, int FG, int HG, bool kTma>
 __device__ __forceinline__ void lattice_body(const LatticeArgs& a, const LatticeWarp& w,
                                              float2* psi_w, PhatFloor fl,
-                                             float (&A)[FG * HG], float (&B)[FG * HG]) {
+                                             float (&A)[FG * HG], float (&B)[FG * HG],
+                                             PhatSpecStats& st) {
   constexpr int kNch = kMode == kPsiStaged ? 1 : 2;
   constexpr int NHG = FG;  // half-lag groups
   constexpr int S = kLatStages;
@@ -330,7 +347,7 @@ __device__ __forceinline__ void lattice_body(const LatticeArgs& a, const Lattice
   else
     cp_async_wait<S - 2>();  // chunk 0
   __syncwarp();
-  lattice_psi<kMode, kNch, kTma>(a, w, 0, psi_w, my_slot, fl);
+  lattice_psi<kMode, kNch, kTma>(a, w, 0, psi_w, my_slot, fl, st);
   for (int c = 0; c < n; ++c) {
     // chunk c+1 landed, psi_w[c&1] written, stage (c-1)%S fully consumed
     if (c + 1 < n || !kTma) wait_chunk(c + 1);
@@ -338,7 +355,8 @@ __device__ __forceinline__ void lattice_body(const LatticeArgs& a, const Lattice
     if (c + S - 1 < n) issue(c + S - 1);
     if (!kTma) cp_async_commit();
     if (c + 1 < n)
-      lattice_psi<kMode, kNch, kTma>(a, w, c + 1, psi_w + ((c + 1) & 1) * kLatPsiW, my_slot, fl);
+      lattice_psi<kMode, kNch, kTma>(a, w, c + 1, psi_w + ((c + 1) & 1) * kLatPsiW, my_slot, fl,
+                                     st);
     lattice_fma<FG, HG, kTma>(w, c, psi_w + (c & 1) * kLatPsiW, fgi, hgi, A, B);
   }
   if (!kTma) cp_async_wait<0>();
@@ -385,7 +403,35 @@ __device__ __forceinline__ void lattice_run(const LatticeArgs& a, const LatticeW
   float A[FG * HG], B[FG * HG];
 #pragma unroll
   for (int e = 0; e < FG * HG; ++e) A[e] = B[e] = 0.0f;
-  lattice_body<kMode, FG, HG, kTma>(a, w, psi_w, fl, A, B);
+  PhatSpecStats st;
+  lattice_body<kMode, FG, HG, kTma>(a, w, psi_w, fl, A, B, st);
+  if constexpr (kMode == kPsiPhatSpec) {
+    // per-frame stats over the CTA's 8 K-slices, fixed order -> [F, P]
+    // (staged in the ring, which the reduction below reuses afterwards)
+    float* s_sum = red;
+    float* s_min = red + kLatWarps * 32;
+    int* s_bad = reinterpret_cast<int*>(red + 2 * kLatWarps * 32);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();  // every warp is done with its ring
+    s_sum[warp * 32 + lane] = st.sum;
+    s_min[warp * 32 + lane] = st.min;
+    s_bad[warp * 32 + lane] = st.bad;
+    __syncthreads();
+    if (blockIdx.z == 0 && threadIdx.x < 32 && threadIdx.x < fv) {
+      float sum = 0.0f, mn = 3.0e38f;
+      int bad = 0;
+#pragma unroll
+      for (int q = 0; q < kLatWarps; ++q) {
+        sum += s_sum[q * 32 + threadIdx.x];
+        mn = fminf(mn, s_min[q * 32 + threadIdx.x]);
+        bad |= s_bad[q * 32 + threadIdx.x];
+      }
+      const size_t o = static_cast<size_t>(f0 + threadIdx.x) * a.P + p;
+      a.spec_sum[o] = sum;
+      a.spec_min[o] = mn;
+      a.spec_bad[o] = bad;
+    }
+  }
   lattice_reduce_store<FG, HG>(a, red, p, f0, fv, hl0, R, A, B);
 }
 
@@ -471,6 +517,8 @@ lattice_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant
     const bool clean = __all_sync(0xffffffffu, a.clean != nullptr && __ldg(a.clean + f) != 0);
     if (a.weighting != 0)
       lattice_dispatch_hl<kPsiIdentity, kTma>(hlc, a, w, psi_w, fl, red, p, f0, fv, hl0, R);
+    else if (a.spec_sum != nullptr)
+      lattice_dispatch_hl<kPsiPhatSpec, kTma>(hlc, a, w, psi_w, fl, red, p, f0, fv, hl0, R);
     else if (clean)
       lattice_dispatch_hl<kPsiPhatClean, kTma>(hlc, a, w, psi_w, fl, red, p, f0, fv, hl0, R);
     else
@@ -478,6 +526,93 @@ lattice_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant
   } else {
     lattice_dispatch_hl<kPsiStaged, kTma>(hlc, a, w, psi_w, PhatFloor{0.0, 0.0f}, red, p, f0, fv,
                                           hl0, R);
+  }
+}
+
+// Fix-up of the speculative relative floor (kPsiPhatSpec): one CTA per frame
+// combines the per-pair stats; a frame is redone exactly when some nonzero
+// |raw|^2 could be below floor^2 = rel^2 mean |raw|^2 (with a margin covering
+// the fp32 sums) or some power left the fast path's range.  The redo forms
+// the fp64 floor like gcc_floor_kernel and recomputes every lattice sample of
+// the frame directly, Xi[n] = 2 Re sum_k psi_k e^{j w_k n T} with the
+// checked PHAT.  Unflagged frames (all of them on real data) exit at once:
+// for them min(1/|raw|, 1/floor) = 1/|raw| and the speculative samples are
+// exactly the floored ones.
+constexpr int kFixThreads = 256;
+
+__global__ void __launch_bounds__(kFixThreads)
+lattice_fixup_kernel(const LatticeArgs a) {
+  const int f = blockIdx.x;
+  __shared__ double s_red[kFixThreads / 32];
+  __shared__ float s_mn[kFixThreads / 32];
+  __shared__ int s_flag;
+  double sum = 0.0;
+  float mn = 3.0e38f;
+  int bad = 0;
+  for (int p = threadIdx.x; p < a.P; p += kFixThreads) {
+    const size_t o = static_cast<size_t>(f) * a.P + p;
+    sum += static_cast<double>(a.spec_sum[o]);
+    mn = fminf(mn, a.spec_min[o]);
+    bad |= a.spec_bad[o];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  }
+  bad = __syncthreads_or(bad);
+  if ((threadIdx.x & 31) == 0) {
+    s_red[threadIdx.x >> 5] = sum;
+    s_mn[threadIdx.x >> 5] = mn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    float m = 3.0e38f;
+    for (int w = 0; w < kFixThreads / 32; ++w) {
+      t += s_red[w];
+      m = fminf(m, s_mn[w]);
+    }
+    const double floor2 = a.floor_rel * a.floor_rel * t / (static_cast<double>(a.P) * a.Kb);
+    s_flag = bad || static_cast<double>(m) < 1.01 * floor2;
+  }
+  __syncthreads();
+  if (!s_flag) return;
+
+  // exact redo of frame f: fp64 floor over all pairs and bins
+  const float2* y = a.src + static_cast<size_t>(f) * a.M * a.Kb;
+  double acc = 0.0;
+  for (int k = threadIdx.x; k < a.Kb; k += kFixThreads)
+    for (int p = 0; p < a.P; ++p) {
+      const float2 u = y[static_cast<size_t>(__ldg(a.pm + p)) * a.Kb + k];
+      const float2 v = y[static_cast<size_t>(__ldg(a.pmp + p)) * a.Kb + k];
+      acc += (static_cast<double>(u.x) * u.x + static_cast<double>(u.y) * u.y) *
+             (static_cast<double>(v.x) * v.x + static_cast<double>(v.y) * v.y);
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < kFixThreads / 32; ++w) t += s_red[w];
+  const PhatFloor fl = make_phat_floor(a.floor_rel * sqrt(t / (static_cast<double>(a.P) * a.Kb)));
+  const int total = __ldg(a.off + a.P);
+  for (int col = threadIdx.x; col < total; col += kFixThreads) {
+    int p = 0;
+    while (__ldg(a.off + p + 1) <= col) ++p;
+    const int R = __ldg(a.reach + p);
+    const int n = col - __ldg(a.off + p) - R;  // lag
+    const int na = n < 0 ? -n : n;
+    const float sgn = n < 0 ? -1.0f : 1.0f;     // lag -n: conjugate twiddle
+    const float2* ya = y + static_cast<size_t>(__ldg(a.pm + p)) * a.Kb;
+    const float2* yb = y + static_cast<size_t>(__ldg(a.pmp + p)) * a.Kb;
+    float re = 0.0f;
+    for (int k = 0; k < a.Kb; ++k) {
+      const float2 ps = phat_one(ya[k], yb[k], 0, fl);
+      const float2 tw = a.tw[static_cast<size_t>(k) * a.Hs + na];
+      re = fmaf(ps.x, tw.x, fmaf(-ps.y, sgn * tw.y, re));
+    }
+    lattice_store(a, static_cast<size_t>(f) * a.T_pad + col, 2.0f * re);
   }
 }
 
@@ -539,7 +674,8 @@ cudaError_t launch_lattice(const float* Psi, int F, int P, int Kb, const float* 
   if (F == 0) return cudaSuccess;
   LatticeArgs a{reinterpret_cast<const float2*>(Psi), F, P, Kb, 0, nullptr, nullptr, 1,
                 nullptr, 0.0, nullptr, reinterpret_cast<const float2*>(tw), twiddle_stride(L),
-                off, reach, T_pad, Xi, nullptr, nullptr, 0.0f, Kb % 2 == 0 && aligned16(Psi)};
+                off, reach, T_pad, Xi, nullptr, nullptr, 0.0f, Kb % 2 == 0 && aligned16(Psi),
+                nullptr, nullptr, nullptr, 0.0};
   return launch_lattice_args(a, false, max_Tp, stream);
 }
 
@@ -549,14 +685,35 @@ cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, co
                                         const int32_t* clean, const float* tw,
                                         int L, const int32_t* off, const int32_t* reach,
                                         int max_Tp, int T_pad, float* Xi, void* Xi_hi,
-                                        void* Xi_lo, float split_scale, cudaStream_t stream) {
+                                        void* Xi_lo, float split_scale, double floor_rel,
+                                        void* spec_scratch, cudaStream_t stream) {
   if (F == 0) return cudaSuccess;
+  // PHAT with the relative floor and no precomputed floors: speculative
+  // lattice + per-frame fix-up (scratch: 12 bytes per frame and pair)
+  const bool spec = weighting == 0 && floors == nullptr && !(abs_floor > 0.0);
   LatticeArgs a{reinterpret_cast<const float2*>(Y), F, P, Kb, M, pm, pmp, weighting,
                 weighting == 0 ? floors : nullptr, weighting == 0 ? abs_floor : 0.0,
                 weighting == 0 ? clean : nullptr, reinterpret_cast<const float2*>(tw),
                 twiddle_stride(L), off, reach, T_pad, Xi, Xi_hi, Xi_lo, split_scale,
-                Kb % 2 == 0 && aligned16(Y)};
-  return launch_lattice_args(a, true, max_Tp, stream);
+                Kb % 2 == 0 && aligned16(Y), nullptr, nullptr, nullptr, floor_rel};
+  if (!spec) return launch_lattice_args(a, true, max_Tp, stream);
+  void* scratch = spec_scratch;
+  const size_t n = static_cast<size_t>(F) * P;
+  cudaError_t e = cudaSuccess;
+  if (scratch == nullptr) {  // no caller scratch: stream-ordered allocation
+    e = cudaMallocAsync(&scratch, n * 12, stream);
+    if (e != cudaSuccess) return e;
+  }
+  a.spec_sum = static_cast<float*>(scratch);
+  a.spec_min = a.spec_sum + n;
+  a.spec_bad = reinterpret_cast<int*>(a.spec_min + n);
+  e = launch_lattice_args(a, true, max_Tp, stream);
+  if (e == cudaSuccess) {
+    lattice_fixup_kernel<<<F, kFixThreads, 0, stream>>>(a);
+    e = cudaGetLastError();
+  }
+  const cudaError_t e2 = spec_scratch == nullptr ? cudaFreeAsync(scratch, stream) : cudaSuccess;
+  return e != cudaSuccess ? e : e2;
 }
 
 }  // namespace srpb

@@ -290,14 +290,9 @@ class SrpPlan:
         if split == "f16" and wcode != 0:
             raise ValueError("the fp16 split needs PHAT-bounded lattice samples")
         s = N.stream_handle(self.device)
+        # PHAT with the relative floor: applied speculatively inside the
+        # lattice call (no floor pass); an explicit floor needs no pass either
         floors = clean = None
-        if wcode == 0:  # K1a: relative floors and per-frame range flags
-            clean = torch.empty(F, dtype=torch.int32, device=self.device)
-            if abs_floor <= 0:
-                floors = torch.empty(F, dtype=torch.float64, device=self.device)
-            self._main("srpb_gcc_floor", N.ptr(Y), F, Y.shape[1], self.Kb, N.ptr(self.pair_m),
-                       N.ptr(self.pair_mp), self.P, DEFAULT_PHAT_FLOOR_REL, N.ptr(floors),
-                       N.ptr(clean), s)
         shape = (F, self.T_pad)
         scale = 0.0
         if split:
@@ -307,10 +302,14 @@ class SrpPlan:
             scale = self.xi_scale16 if split == "f16" else 0.0
         else:
             outs = (torch.empty(shape, dtype=torch.float32, device=self.device), None, None)
+        spec = None
+        if wcode == 0 and abs_floor <= 0:  # speculative floor statistics
+            spec = torch.empty(3 * F * self.P, dtype=torch.float32, device=self.device)
         self._main("srpb_lattice_from_spectra", N.ptr(Y), F, Y.shape[1], self.Kb,
                    N.ptr(self.pair_m), N.ptr(self.pair_mp), self.P, wcode, N.ptr(floors),
                    abs_floor, N.ptr(clean), N.ptr(self.twiddles), self.L, N.ptr(self.off),
-                   N.ptr(self.reach), self.T_pad, *(N.ptr(o) for o in outs), float(scale), s)
+                   N.ptr(self.reach), self.T_pad, *(N.ptr(o) for o in outs), float(scale),
+                   DEFAULT_PHAT_FLOOR_REL, N.ptr(spec), s)
         return outs[1:] if split else outs[0]
 
     def _use_tc(self, F, kind):

@@ -184,6 +184,36 @@ def test_lattice_from_spectra_fused(name):
             assert rel_l2(xi[f, :total], g[f"lattice_{n_aux}"][f]) <= REL_L2_TOL
 
 
+def test_speculative_floor_fixup_frames():
+    """The relative PHAT floor is applied speculatively inside the fused
+    lattice; frames where a bin falls below the floor (powers in range),
+    where powers leave the fast range, or that are all zero must still match
+    the exact two-step path (fp64 floor in K1) and the oracle."""
+    g = load_golden("random_small")
+    Y = g["Y"].astype(np.complex64).copy()          # [3, 5, 64]
+    Y = np.concatenate([Y, Y[:1], Y[:1]])            # 5 frames
+    Y[0, 1, 7] = 1e-13 + 0j                          # |raw| tiny but powers in range
+    Y[0, 2, 7] = 1e-12 + 0j
+    Y[1, 0, 3] = 1e-20 + 1e-20j                      # power out of the fast range
+    Y[3] = 0                                         # all-zero frame
+    Y[4, :, 5] = 0                                   # exact-zero bin
+    plan = plan_from_golden(g, 3)
+    Yd = dev(Y)
+    fused = plan.lattice_from_spectra(Yd).cpu().numpy()
+    exact = plan.lattice(plan.cross_spectra(Yd)[0]).cpu().numpy()
+    total = plan.total_samples
+    for f in range(Y.shape[0]):
+        ref = np.concatenate(O.gcc_lattice(O.cross_spectrum(Y[f].astype(complex), g["pair_m"],
+                                                            g["pair_mp"])[0],
+                                           g["omega"], g["bounds"], T, 3)[1])
+        if f == 3:
+            assert np.all(fused[f] == 0.0) and np.all(ref == 0.0)
+            continue
+        assert rel_l2(fused[f, :total], ref) <= REL_L2_TOL, f
+        assert rel_l2(fused[f, :total], exact[f, :total]) <= REL_L2_TOL, f
+    assert np.array_equal(fused[2], exact[2])  # an untouched frame: bitwise the exact path
+
+
 def test_lattice_from_spectra_odd_bins_and_ragged_tiles():
     """Odd Kb (partial bin chunk), F not a multiple of the 64-frame tile,
     reach > 32 lags (several lag tiles) vs the oracle."""
