@@ -278,6 +278,20 @@ int srpb_interp_tc16(const void* w_hi, const void* w_lo, float w_scale, const vo
                      unsigned long long* keys, int kb_per_group, void* stream);
 
 /*
+ * K4 on the tensor cores in 3xFP16 without a stored W: the sinc weights are
+ * generated in tensor memory by the epilogue warps from the sinc split (the
+ * same arithmetic as srpb_sinc_table + srpb_f16_split with w_scale 2^14, so
+ * the maps equal srpb_interp_tc16's bit for bit), removing W's HBM footprint
+ * (J * T_pad * 8 bytes) and traffic.
+ *   sx_i, sx_f [P, J], off [P+1], reach [P] as for srpb_sinc_table;
+ *   xi_hi/xi_lo [F, T_pad] fp16 split of xi_scale * Xi; T_pad % 8 == 0.
+ */
+int srpb_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, int P, const int32_t* off,
+                              const int32_t* reach, const void* xi_hi, const void* xi_lo,
+                              float xi_scale, int F, int J, int T_pad, float* maps,
+                              unsigned long long* keys, int kb_per_group, void* stream);
+
+/*
  * K5 per-frame argmax, lowest index on ties (srp.argmax_candidate,
  * srp.py:107-109) over stored maps [F, J]: folds into keys [F].
  */

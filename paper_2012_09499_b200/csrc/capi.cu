@@ -49,6 +49,9 @@ cudaError_t launch_conventional_tc16(const void*, const void*, float, int, int, 
                                      unsigned long long*, int, cudaStream_t);
 cudaError_t launch_interp_tc16(const void*, const void*, float, const void*, const void*, float,
                                int, int, int, float*, unsigned long long*, int, cudaStream_t);
+cudaError_t launch_interp_tc16_onthefly(const int32_t*, const float*, int, const int32_t*,
+                                        const int32_t*, const void*, const void*, float, int, int,
+                                        int, float*, unsigned long long*, int, cudaStream_t);
 cudaError_t launch_argmax_f64(const double*, int, int, int32_t*, cudaStream_t);
 cudaError_t launch_keys_reset(unsigned long long*, int, cudaStream_t);
 cudaError_t launch_keys_to_index(const unsigned long long*, int, int32_t*, cudaStream_t);
@@ -89,7 +92,7 @@ static bool pow2_scale(float s) {
   return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
 }
 
-int srpb_abi_version(void) { return 7; }
+int srpb_abi_version(void) { return 8; }
 
 const char* srpb_last_error(void) { return g_err; }
 
@@ -308,6 +311,23 @@ int srpb_conventional_tc16(const void* psi_hi, const void* psi_lo, float psi_sca
   return status(srpb::launch_conventional_tc16(psi_hi, psi_lo, psi_scale, F, P, Kb, period, tau_i,
                                                tau_f, J, maps, keys, kb_per_group, S(stream)),
                 "srpb_conventional_tc16");
+}
+
+int srpb_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, int P, const int32_t* off,
+                              const int32_t* reach, const void* xi_hi, const void* xi_lo,
+                              float xi_scale, int F, int J, int T_pad, float* maps,
+                              unsigned long long* keys, int kb_per_group, void* stream) {
+  REQUIRE(F >= 0 && J >= 0 && P >= 1 && T_pad >= 1, "srpb_interp_tc16_onthefly: bad shape");
+  REQUIRE(T_pad % 8 == 0, "srpb_interp_tc16_onthefly: T_pad must be a multiple of 8, got %d",
+          T_pad);
+  REQUIRE(pow2_scale(xi_scale), "srpb_interp_tc16_onthefly: xi_scale must be a power of two");
+  REQUIRE(F == 0 || J == 0 || (sx_i && sx_f && off && reach && xi_hi && xi_lo),
+          "srpb_interp_tc16_onthefly: null pointer");
+  REQUIRE(maps || keys, "srpb_interp_tc16_onthefly: need maps and/or keys output");
+  return status(srpb::launch_interp_tc16_onthefly(sx_i, sx_f, P, off, reach, xi_hi, xi_lo,
+                                                  xi_scale, F, J, T_pad, maps, keys, kb_per_group,
+                                                  S(stream)),
+                "srpb_interp_tc16_onthefly");
 }
 
 int srpb_interp_tc16(const void* w_hi, const void* w_lo, float w_scale, const void* xi_hi,

@@ -177,4 +177,26 @@ __device__ __forceinline__ float2 psi_warp(float2 a, float2 b, PhatFloor fl) {
   }
 }
 
+// Sinc weight sinc(x - n) from the split x = i + f (|f| <= 1/2), the
+// reference's normalised sinc snapped to exactly 1 / 0 at integer arguments
+// (srp._sinc_kernel srp.py:250-261): with d = i - n,
+//   sinc(d + f) = (-1)^d (sin(pi f) / pi) / (d + f),   exactly [d == 0] if f == 0.
+// spi = sin(pi f) / pi per (candidate, pair); the reciprocal is the
+// single-instruction approximation (<= 1 ulp), and the same function feeds
+// both the stored table and the in-TMEM generator, so they agree bitwise.
+__device__ __forceinline__ float rcp_approx_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sinc_spi(float f) {
+  return sinpif(f) * 0.318309886183790671538f;  // sin(pi f) / pi
+}
+__device__ __forceinline__ float sinc_weight_fast(int i, float f, float spi, int n) {
+  const int d = i - n;
+  const float w = __uint_as_float(__float_as_uint(spi * rcp_approx_ftz(static_cast<float>(d) + f)) ^
+                                  (static_cast<uint32_t>(d & 1) << 31));
+  return f == 0.0f ? (d == 0 ? 1.0f : 0.0f) : w;
+}
+
 }  // namespace srpb

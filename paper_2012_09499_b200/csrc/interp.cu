@@ -40,9 +40,9 @@ __global__ void sinc_table_kernel(const int32_t* __restrict__ sx_i, const float*
     const int R = reach[p], base = off[p];
     const int i = sx_i[static_cast<size_t>(p) * J + j];
     const float fr = sx_f[static_cast<size_t>(p) * J + j];
-    const float sp = sinpif(fr);
+    const float spi = sinc_spi(fr);
     for (int ni = threadIdx.x; ni < 2 * R + 1; ni += blockDim.x)
-      row[base + ni] = sinc_split(i, fr, sp, ni - R);
+      row[base + ni] = sinc_weight_fast(i, fr, spi, ni - R);
   }
   for (int t = off[P] + threadIdx.x; t < T_pad; t += blockDim.x) row[t] = 0.0f;
 }

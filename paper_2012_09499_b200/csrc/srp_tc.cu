@@ -50,6 +50,7 @@
 #include <cuda_fp16.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "tmap.cuh"
@@ -70,7 +71,7 @@ constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 8;
 constexpr int kABytes = kTcM * 128;  // one of A_hi / A_lo per stage
 
-enum : int { kAFromTma = 0, kAPhase = 1 };
+enum : int { kAFromTma = 0, kAPhase = 1, kASinc = 2 };
 
 template <int kAMode, bool kPair, bool kF16>
 struct TcCfg {
@@ -115,6 +116,12 @@ struct TcParams {
   int kb_per_pair;    // Kb / 16
   int period, mask;
   float inv_period;
+  // K4 with sinc weights generated on the fly (kASinc)
+  const int32_t* sx_i;   // [P, J]
+  const float* sx_f;     // [P, J]
+  const int32_t* off;    // [P + 1] lattice column offsets
+  const int32_t* reach;  // [P]
+  int P;
 };
 
 struct TcSmem {
@@ -381,6 +388,76 @@ struct PhaseGen {
   }
 };
 
+// Sinc-weight generator of one A row (candidate j) for K4 without a stored
+// W: columns t = 64 kb + 32 half + c (c < 32) of the lattice layout,
+// W[j, t] = sinc(x_jp - n) for the pair p owning t and its lag n, computed
+// with the stored table's function (sinc_weight_fast) and split like
+// srpb_f16_split (v = 2^14 w, hi = half(v), lo = half(v - hi)), so the A
+// operand -- and the maps -- equal the stored-W kernel's bit for bit.  The
+// pair is tracked incrementally (columns only increase within an item; all
+// rows of a warp share the column sequence, so pair changes are
+// warp-uniform); the next pair's split is prefetched into registers one
+// pair ahead, hiding its global-load latency.
+struct SincGen {
+  int p, next, base, total, P;  // current pair, its end column, column of lag 0
+  int si, nsi;                  // current / prefetched split
+  float sf, spi, nsf;
+  const int2* cols;             // shared: per pair (end column, column of lag 0)
+
+  __device__ __forceinline__ void fetch(const TcParams& prm, int j, int q) {
+    nsi = 0;
+    nsf = 0.0f;
+    if (q < P && j < prm.J) {
+      nsi = __ldg(prm.sx_i + static_cast<size_t>(q) * prm.J + j);
+      nsf = __ldg(prm.sx_f + static_cast<size_t>(q) * prm.J + j);
+    }
+  }
+
+  __device__ __forceinline__ void start_tile(const TcParams& prm, int j, const int2* pair_cols) {
+    P = prm.P;
+    p = -1;
+    next = 0;
+    cols = pair_cols;
+    total = pair_cols[P - 1].x;
+    fetch(prm, j, 0);
+  }
+
+  __device__ __forceinline__ void advance(const TcParams& prm, int j) {
+    ++p;
+    si = nsi;
+    sf = nsf;
+    spi = sinc_spi(sf);
+    const int2 c = cols[p];
+    next = c.x;
+    base = c.y;
+    fetch(prm, j, p + 1);
+  }
+
+  __device__ __forceinline__ void block(const TcParams& prm, int j, int half, int kb,
+                                        uint32_t a_hi_tmem, uint32_t a_lo_tmem) {
+    uint32_t hi[16], lo[16];
+    const int t0 = 64 * kb + 32 * half;
+#pragma unroll
+    for (int c = 0; c < 32; c += 2) {
+      float w[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int t = t0 + c + u;
+        // a thread sees 32 of every 64 columns: pairs may end in the skipped half
+        while (t >= next && t < total) advance(prm, j);
+        w[u] = t < total ? sinc_weight_fast(si, sf, spi, t - base) * kF16PhaseScale : 0.0f;
+      }
+      const __half2 h = __floats2half2_rn(w[0], w[1]);
+      const float2 hf = __half22float2(h);
+      const __half2 l = __floats2half2_rn(w[0] - hf.x, w[1] - hf.y);
+      hi[c >> 1] = *reinterpret_cast<const uint32_t*>(&h);
+      lo[c >> 1] = *reinterpret_cast<const uint32_t*>(&l);
+    }
+    tmem_st16(a_hi_tmem + 16 * half, hi);
+    tmem_st16(a_lo_tmem + 16 * half, lo);
+  }
+};
+
 template <int kAMode, bool kPair, bool kF16>
 __global__ void __launch_bounds__(kTcThreads, 1)
 srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
@@ -402,6 +479,11 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const size_t stage_bytes = tc_stage_bytes(p.N, kASmem, kPair);
   TcSmem* bar = reinterpret_cast<TcSmem*>(smem + S * stage_bytes);
+  // kASinc: per pair (end column, column of lag 0), after the barriers
+  int2* pair_cols = reinterpret_cast<int2*>(bar + 1);
+  if (kAMode == kASinc)
+    for (int q = threadIdx.x; q < p.P; q += blockDim.x)
+      pair_cols[q] = make_int2(__ldg(p.off + q + 1), __ldg(p.off + q) + __ldg(p.reach + q));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b_rows = kPair ? p.N / 2 : p.N;  // B rows held by this CTA
   const uint32_t b_bytes = static_cast<uint32_t>(b_rows) * 128;
@@ -464,7 +546,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // full: producers (x kCta) + K2 A-generator warps (x kCta) arrive on the
     // leader's barrier; empty / acc_full: one commit from the leader's MMA;
     // acc_empty: the epilogue warps of both CTAs arrive on the leader's.
-    const int full_count = kCta * (1 + (kAMode == kAPhase ? kEpiWarps : 0));
+    const int full_count = kCta * (1 + (kAMode != kAFromTma ? kEpiWarps : 0));
     for (int s = 0; s < S; ++s) {
       mbar_init(&bar->full[s], full_count);
       mbar_init(&bar->empty[s], 1);
@@ -694,16 +776,20 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       ++drained;
     };
     { TCP_T0();
-    if (kAMode == kAPhase) {
+    if constexpr (kAMode != kAFromTma) {
       // generator thread: TMEM lane (row) 32*quarter + lane, K columns
       // [16*half, +16) of each 32-column A block
       const int r = 32 * quarter + lane;
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
-      PhaseGen<kF16> gen;
+      using Gen = typename std::conditional<kAMode == kASinc, SincGen, PhaseGen<kF16>>::type;
+      Gen gen;
       int kg = 0, s = 0, ph = 0;  // stage ring position
       for (int it = 0; it < my_tiles; ++it) {
         const int j = item(it).m0 + r;
-        gen.start_tile(p);
+        if constexpr (kAMode == kASinc)
+          gen.start_tile(p, j, pair_cols);
+        else
+          gen.start_tile(p);
         for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
           { TCP_T0();
           mbar_wait(&bar->empty[s], ph ^ 1);
@@ -711,7 +797,10 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
           { TCP_T0();
           tc_fence_after();  // MMAs that read this stage have completed
           const uint32_t a_col = lane_base + static_cast<uint32_t>(tc_a_tmem_col(p.N, s));
-          gen.block(p, j, half, a_col, a_col + 32);
+          if constexpr (kAMode == kASinc)
+            gen.block(p, j, half, kb, a_col, a_col + 32);
+          else
+            gen.block(p, j, half, a_col, a_col + 32);
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
@@ -842,7 +931,8 @@ template <int kAMode, bool kPair, bool kF16>
 cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
                       const CUtensorMap& bl, const TcParams& p, cudaStream_t stream) {
   using Cfg = TcCfg<kAMode, kPair, kF16>;
-  const size_t smem = tc_smem_bytes(p.N, Cfg::kASmem, kPair, Cfg::kStages);
+  const size_t smem = tc_smem_bytes(p.N, Cfg::kASmem, kPair, Cfg::kStages) +
+                      (kAMode == kASinc ? sizeof(int2) * static_cast<size_t>(p.P) : 0);
   auto kern = srp_tc_kernel<kAMode, kPair, kF16>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -933,6 +1023,34 @@ static cudaError_t interp_tc(const void* w_hi, const void* w_lo, const void* xi_
                 : launch_tc<kAFromTma, false, true>(ah, al, bh, bl, p, stream);
   return pair ? launch_tc<kAFromTma, true, false>(ah, al, bh, bl, p, stream)
               : launch_tc<kAFromTma, false, false>(ah, al, bh, bl, p, stream);
+}
+
+// K4 with the sinc weights generated in TMEM (no stored W): B = Xi fp16 split
+cudaError_t launch_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, int P,
+                                        const int32_t* off, const int32_t* reach,
+                                        const void* xi_hi, const void* xi_lo, float xi_scale,
+                                        int F, int J, int T_pad, float* maps,
+                                        unsigned long long* keys, int kb_per_group,
+                                        cudaStream_t stream) {
+  if (F == 0 || J == 0) return cudaSuccess;
+  TcParams p{};
+  p.F = F;
+  p.J = J;
+  p.num_kb = (T_pad + kTcKBlock16 - 1) / kTcKBlock16;
+  finish_params(p, kb_per_group, false, true);
+  p.scale = 1.0f / (kF16PhaseScale * xi_scale);
+  p.maps = maps;
+  p.keys = keys;
+  p.sx_i = sx_i;
+  p.sx_f = sx_f;
+  p.off = off;
+  p.reach = reach;
+  p.P = P;
+  CUtensorMap bh, bl;
+  cudaError_t e = make_map(&bh, xi_hi, F, T_pad, 16, true);
+  if (e == cudaSuccess) e = make_map(&bl, xi_lo, F, T_pad, 16, true);
+  if (e != cudaSuccess) return e;
+  return launch_tc<kASinc, false, true>(bh, bl, bh, bl, p, stream);
 }
 
 cudaError_t launch_conventional_tc(const float* psi_hi, const float* psi_lo, int F, int P, int Kb,

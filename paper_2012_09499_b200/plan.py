@@ -319,7 +319,12 @@ class SrpPlan:
         less work."""
         if self.backend == "simt":
             return False
-        ok = (self.harmonic and self.Kb % 16 == 0) if kind == "conv" else (self.W is not None)
+        if kind == "conv":
+            ok = self.harmonic and self.Kb % 16 == 0
+        elif kind == "interp16":  # 3xFP16 K4: stored W or weights generated in TMEM
+            ok = True
+        else:                     # 3xTF32 K4 needs the stored W
+            ok = self.W is not None
         if self.backend == "tc":
             if not ok:
                 raise ValueError(f"tensor-core {kind} path unavailable for this plan")
@@ -370,7 +375,7 @@ class SrpPlan:
             return False
         if kind == "conv":
             return self.harmonic and self.Kb % 32 == 0
-        return self.W is not None
+        return True  # stored W, or weights generated in TMEM
 
     def conventional(self, psi, maps=True, maps_out=None, _bounded=False):
         """K2 (+ fused K5): Psi [F, P, Kb] -> (maps [F, J] fp32 | None,
@@ -440,7 +445,15 @@ class SrpPlan:
         return out, self.keys_to_index(keys)
 
     def _approx_tc16(self, xh, xl, out, keys):
-        """K4 in 3xFP16 from the fp16 split of xi_scale16 * Xi."""
+        """K4 in 3xFP16 from the fp16 split of xi_scale16 * Xi (weights from
+        the stored W split, or generated in tensor memory when W is not
+        stored)."""
+        if self.W is None:
+            self._main("srpb_interp_tc16_onthefly", N.ptr(self.sx_i), N.ptr(self.sx_f), self.P,
+                       N.ptr(self.off), N.ptr(self.reach), N.ptr(xh), N.ptr(xl),
+                       self.xi_scale16, xh.shape[0], self.J, self.T_pad, N.ptr(out), N.ptr(keys),
+                       self.interp_kb_per_group16, N.stream_handle(self.device))
+            return out, self.keys_to_index(keys)
         if self.W16 is None:
             self.W16 = self.split_f16(self.W, self.F16_UNIT_SCALE)
         xs = self.xi_scale16
@@ -477,10 +490,11 @@ class SrpPlan:
             return self.conventional(psi, maps, _bounded=bounded)
         if path == "approx":
             F = Y.shape[0]
-            if self.sample_period is not None and self._use_tc(F, "interp"):
+            f16 = self._f16_ok("interp", bounded)
+            if self.sample_period is not None and self._use_tc(F, "interp16" if f16 else "interp"):
                 out = torch.empty((F, self.J), dtype=torch.float32,
                                   device=self.device) if maps else None
-                if self._f16_ok("interp", bounded):
+                if f16:
                     xh, xl = self.lattice_from_spectra(Y, weighting, phat_floor, split="f16")
                     return self._approx_tc16(xh, xl, out, self._keys(F))
                 xh, xl = self.lattice_from_spectra(Y, weighting, phat_floor, split=True)

@@ -317,6 +317,24 @@ def test_run_tensor_core_precisions(name, precision):
         assert list(am.cpu().numpy()) == list(g["argmax_conv"])
 
 
+@pytest.mark.parametrize("name", ["c1", "c2_subset", "random_small", "on_lattice"])
+def test_tc16_onthefly_weights_bitwise_equal_stored(name):
+    """K4 with the sinc weights generated in tensor memory equals the
+    stored-W 3xFP16 kernel bit for bit (same weight arithmetic and split),
+    and both match the reference."""
+    g = load_golden(name)
+    Y = dev(g["Y"])
+    for n_aux in g["n_aux"]:
+        st = plan_from_golden(g, int(n_aux), weights="stored", backend="tc")
+        ot = plan_from_golden(g, int(n_aux), weights="onthefly", backend="tc")
+        assert ot.W is None
+        m1, a1 = st.run(Y, "approx")
+        m2, a2 = ot.run(Y, "approx")
+        assert torch.equal(m1, m2) and torch.equal(a1, a2), (name, n_aux)
+        assert_maps_match(m2.cpu().numpy(), g[f"approx_{n_aux}"], a2.cpu().numpy(),
+                          what=f"{name} onthefly-tc16")
+
+
 def test_captured_step_and_chunked_runner_match_eager():
     """CUDA-graph replay (CapturedStep) and the 3-stream chunked host
     pipeline give bitwise the same maps/argmax as the eager plan.run."""

@@ -31,7 +31,7 @@ class T:
 def main():
     scene, pm, pmp, bounds, tdoa, omega = bench.workload(0)
     plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=bench.T, n_aux=bench.N_AUX,
-                   weights="stored")
+                   weights=os.environ.get("SRPB_WEIGHTS", "stored"))
     Y = torch.from_numpy(scene.Y).cuda()
     for path in sys.argv[1:] or ["approx"]:
         for maps in (True, False):

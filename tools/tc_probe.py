@@ -58,7 +58,7 @@ def main():
     scene, pm, pmp, bounds, tdoa, omega = bench.workload(0)
     kbg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
     plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=bench.T, n_aux=bench.N_AUX,
-                   weights="stored", kb_per_group=kbg)
+                   weights=os.environ.get("SRPB_WEIGHTS", "stored"), kb_per_group=kbg)
     Y = torch.from_numpy(scene.Y).cuda()
     paths = sys.argv[2].split(",") if len(sys.argv) > 2 else ["approx", "conventional"]
     for path in paths:
