@@ -248,6 +248,16 @@ int srpb_interp_tc(const float* w_hi, const float* w_lo, const float* xi_hi, con
                    int kb_per_group, void* stream);
 
 /*
+ * In-kernel argmax finish (srpb_conventional_tc16, srpb_interp_tc16,
+ * srpb_interp_tc16_onthefly): with argmax_out [F] int32 and done_counter (one
+ * unsigned int) non-NULL, the kernel's last CTA decodes keys into argmax_out
+ * (as srpb_keys_to_index) and resets keys to 0 and *done_counter to 0, so a
+ * caller that keeps keys and the counter zero-initialised between calls needs
+ * neither srpb_argmax_keys_reset nor srpb_keys_to_index.  Calls sharing keys /
+ * counter buffers must be stream-ordered.
+ */
+
+/*
  * 3xFP16 operand split: hi = fp16(scale x), lo = fp16(scale x - hi), scale a
  * power of two keeping |scale x| < 65504 (fp16 has tf32's 11-bit
  * significand: the split is as exact as the tf32 one).
@@ -265,7 +275,7 @@ int srpb_f16_split(const float* x, size_t n, float scale, void* hi, void* lo, vo
 int srpb_conventional_tc16(const void* psi_hi, const void* psi_lo, float psi_scale, int F, int P,
                            int Kb, int period, const int32_t* tau_i, const float* tau_f, int J,
                            float* maps, unsigned long long* keys, int kb_per_group,
-                           void* stream);
+                           int32_t* argmax_out, unsigned int* done_counter, void* stream);
 
 /*
  * K4 on the tensor cores in 3xFP16; same maps as srpb_interp_tc.
@@ -275,7 +285,8 @@ int srpb_conventional_tc16(const void* psi_hi, const void* psi_lo, float psi_sca
  */
 int srpb_interp_tc16(const void* w_hi, const void* w_lo, float w_scale, const void* xi_hi,
                      const void* xi_lo, float xi_scale, int F, int J, int T_pad, float* maps,
-                     unsigned long long* keys, int kb_per_group, void* stream);
+                     unsigned long long* keys, int kb_per_group, int32_t* argmax_out,
+                     unsigned int* done_counter, void* stream);
 
 /*
  * K4 on the tensor cores in 3xFP16 without a stored W: the sinc weights are
@@ -289,7 +300,8 @@ int srpb_interp_tc16(const void* w_hi, const void* w_lo, float w_scale, const vo
 int srpb_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, int P, const int32_t* off,
                               const int32_t* reach, const void* xi_hi, const void* xi_lo,
                               float xi_scale, int F, int J, int T_pad, float* maps,
-                              unsigned long long* keys, int kb_per_group, void* stream);
+                              unsigned long long* keys, int kb_per_group, int32_t* argmax_out,
+                              unsigned int* done_counter, void* stream);
 
 /*
  * K5 per-frame argmax, lowest index on ties (srp.argmax_candidate,

@@ -52,12 +52,14 @@ _SIGNATURES = {
                        c_void_p, c_int, c_void_p],
     "srpb_f16_split": [c_void_p, ctypes.c_size_t, ctypes.c_float, c_void_p, c_void_p, c_void_p],
     "srpb_conventional_tc16": [c_void_p, c_void_p, ctypes.c_float, c_int, c_int, c_int, c_int,
-                               c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_int, c_void_p],
+                               c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_int, c_void_p,
+                               c_void_p, c_void_p],
     "srpb_interp_tc16": [c_void_p, c_void_p, ctypes.c_float, c_void_p, c_void_p, ctypes.c_float,
-                         c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p],
+                         c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
+                         c_void_p],
     "srpb_interp_tc16_onthefly": [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
                                   c_void_p, ctypes.c_float, c_int, c_int, c_int, c_void_p,
-                                  c_void_p, c_int, c_void_p],
+                                  c_void_p, c_int, c_void_p, c_void_p, c_void_p],
     "srpb_argmax": [c_void_p, c_int, c_int, c_void_p, c_void_p],
     "srpb_argmax_f64": [c_void_p, c_int, c_int, c_void_p, c_void_p],
     "srpb_argmax_keys_reset": [c_void_p, c_int, c_void_p],

@@ -46,12 +46,15 @@ cudaError_t launch_tf32_split(const float*, size_t, float*, float*, cudaStream_t
 cudaError_t launch_f16_split(const float*, size_t, float, void*, void*, cudaStream_t);
 cudaError_t launch_conventional_tc16(const void*, const void*, float, int, int, int, int,
                                      const int32_t*, const float*, int, float*,
-                                     unsigned long long*, int, cudaStream_t);
+                                     unsigned long long*, int, int32_t*, unsigned int*,
+                                     cudaStream_t);
 cudaError_t launch_interp_tc16(const void*, const void*, float, const void*, const void*, float,
-                               int, int, int, float*, unsigned long long*, int, cudaStream_t);
+                               int, int, int, float*, unsigned long long*, int, int32_t*,
+                               unsigned int*, cudaStream_t);
 cudaError_t launch_interp_tc16_onthefly(const int32_t*, const float*, int, const int32_t*,
                                         const int32_t*, const void*, const void*, float, int, int,
-                                        int, float*, unsigned long long*, int, cudaStream_t);
+                                        int, float*, unsigned long long*, int, int32_t*,
+                                        unsigned int*, cudaStream_t);
 cudaError_t launch_argmax_f64(const double*, int, int, int32_t*, cudaStream_t);
 cudaError_t launch_keys_reset(unsigned long long*, int, cudaStream_t);
 cudaError_t launch_keys_to_index(const unsigned long long*, int, int32_t*, cudaStream_t);
@@ -92,7 +95,7 @@ static bool pow2_scale(float s) {
   return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
 }
 
-int srpb_abi_version(void) { return 8; }
+int srpb_abi_version(void) { return 9; }
 
 const char* srpb_last_error(void) { return g_err; }
 
@@ -299,8 +302,10 @@ int srpb_f16_split(const float* x, size_t n, float scale, void* hi, void* lo, vo
 int srpb_conventional_tc16(const void* psi_hi, const void* psi_lo, float psi_scale, int F, int P,
                            int Kb, int period, const int32_t* tau_i, const float* tau_f, int J,
                            float* maps, unsigned long long* keys, int kb_per_group,
-                           void* stream) {
+                           int32_t* argmax_out, unsigned int* done_counter, void* stream) {
   REQUIRE(F >= 0 && P >= 1 && Kb >= 1 && J >= 0, "srpb_conventional_tc16: bad shape");
+  REQUIRE(!argmax_out || (keys && done_counter),
+          "srpb_conventional_tc16: argmax_out needs keys and done_counter");
   REQUIRE(Kb % 32 == 0, "srpb_conventional_tc16: Kb must be a multiple of 32, got %d", Kb);
   REQUIRE(period >= 1 && period <= 46340, "srpb_conventional_tc16: period %d out of range",
           period);
@@ -309,15 +314,19 @@ int srpb_conventional_tc16(const void* psi_hi, const void* psi_lo, float psi_sca
           "srpb_conventional_tc16: null pointer");
   REQUIRE(maps || keys, "srpb_conventional_tc16: need maps and/or keys output");
   return status(srpb::launch_conventional_tc16(psi_hi, psi_lo, psi_scale, F, P, Kb, period, tau_i,
-                                               tau_f, J, maps, keys, kb_per_group, S(stream)),
+                                               tau_f, J, maps, keys, kb_per_group, argmax_out,
+                                               done_counter, S(stream)),
                 "srpb_conventional_tc16");
 }
 
 int srpb_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, int P, const int32_t* off,
                               const int32_t* reach, const void* xi_hi, const void* xi_lo,
                               float xi_scale, int F, int J, int T_pad, float* maps,
-                              unsigned long long* keys, int kb_per_group, void* stream) {
+                              unsigned long long* keys, int kb_per_group, int32_t* argmax_out,
+                              unsigned int* done_counter, void* stream) {
   REQUIRE(F >= 0 && J >= 0 && P >= 1 && T_pad >= 1, "srpb_interp_tc16_onthefly: bad shape");
+  REQUIRE(!argmax_out || (keys && done_counter),
+          "srpb_interp_tc16_onthefly: argmax_out needs keys and done_counter");
   REQUIRE(T_pad % 8 == 0, "srpb_interp_tc16_onthefly: T_pad must be a multiple of 8, got %d",
           T_pad);
   REQUIRE(pow2_scale(xi_scale), "srpb_interp_tc16_onthefly: xi_scale must be a power of two");
@@ -326,21 +335,25 @@ int srpb_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, int P, con
   REQUIRE(maps || keys, "srpb_interp_tc16_onthefly: need maps and/or keys output");
   return status(srpb::launch_interp_tc16_onthefly(sx_i, sx_f, P, off, reach, xi_hi, xi_lo,
                                                   xi_scale, F, J, T_pad, maps, keys, kb_per_group,
-                                                  S(stream)),
+                                                  argmax_out, done_counter, S(stream)),
                 "srpb_interp_tc16_onthefly");
 }
 
 int srpb_interp_tc16(const void* w_hi, const void* w_lo, float w_scale, const void* xi_hi,
                      const void* xi_lo, float xi_scale, int F, int J, int T_pad, float* maps,
-                     unsigned long long* keys, int kb_per_group, void* stream) {
+                     unsigned long long* keys, int kb_per_group, int32_t* argmax_out,
+                     unsigned int* done_counter, void* stream) {
   REQUIRE(F >= 0 && J >= 0 && T_pad >= 1, "srpb_interp_tc16: bad shape");
+  REQUIRE(!argmax_out || (keys && done_counter),
+          "srpb_interp_tc16: argmax_out needs keys and done_counter");
   REQUIRE(T_pad % 8 == 0, "srpb_interp_tc16: T_pad must be a multiple of 8, got %d", T_pad);
   REQUIRE(pow2_scale(w_scale) && pow2_scale(xi_scale),
           "srpb_interp_tc16: scales must be powers of two");
   REQUIRE(F == 0 || J == 0 || (w_hi && w_lo && xi_hi && xi_lo), "srpb_interp_tc16: null pointer");
   REQUIRE(maps || keys, "srpb_interp_tc16: need maps and/or keys output");
   return status(srpb::launch_interp_tc16(w_hi, w_lo, w_scale, xi_hi, xi_lo, xi_scale, F, J, T_pad,
-                                         maps, keys, kb_per_group, S(stream)),
+                                         maps, keys, kb_per_group, argmax_out, done_counter,
+                                         S(stream)),
                 "srpb_interp_tc16");
 }
 

@@ -110,6 +110,10 @@ struct TcParams {
   float scale;
   float* maps;
   unsigned long long* keys;
+  // optional in-kernel argmax finish: the last CTA decodes keys -> argmax_out
+  // and resets keys and the counter for the next call
+  int32_t* argmax_out;
+  unsigned int* done;
   // K2 phase generation
   const int32_t* tau_i;
   const float* tau_f;
@@ -833,9 +837,31 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
 #ifdef SRPB_TC_PROFILE
   const long long t_work = clock64();
 #endif
+  // in-kernel argmax finish: every thread's key atomics are visible device-wide
+  // before its CTA counts itself done (one fence per thread, at exit)
+  if (p.argmax_out) __threadfence();
   tc_fence_before();
   __syncthreads();
   if (kPair) cluster_sync();  // the pair leaves together (remote arrivals landed)
+  if (p.argmax_out) {
+    // last CTA: keys -> argmax (srpb_keys_to_index), keys and counter reset
+    // (srpb_argmax_keys_reset) for the next call -- two launches saved
+    __shared__ unsigned int s_last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(p.done, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (int f = threadIdx.x; f < p.F; f += blockDim.x) {
+        const unsigned long long k = __ldcg(p.keys + f);
+        p.argmax_out[f] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(k));
+        p.keys[f] = 0ull;
+      }
+      if (threadIdx.x == 0) *p.done = 0u;
+    }
+  }
 #ifdef SRPB_TC_PROFILE
   if (threadIdx.x == 0) {
     atomicAdd(&g_tc_prof[16], static_cast<unsigned long long>(clock64() - t_entry));
@@ -963,7 +989,8 @@ static cudaError_t conventional_tc(const void* psi_hi, const void* psi_lo, bool 
                                    int F, int P, int Kb, int period, const int32_t* tau_i,
                                    const float* tau_f, int J, float* maps,
                                    unsigned long long* keys, int kb_per_group,
-                                   cudaStream_t stream) {
+                                   cudaStream_t stream, int32_t* argmax_out = nullptr,
+                                   unsigned int* done = nullptr) {
   if (F == 0 || J == 0) return cudaSuccess;
   TcParams p{};
   p.F = F;
@@ -975,6 +1002,8 @@ static cudaError_t conventional_tc(const void* psi_hi, const void* psi_lo, bool 
   p.scale = f16 ? 2.0f / (kF16PhaseScale * psi_scale) : 2.0f;
   p.maps = maps;
   p.keys = keys;
+  p.argmax_out = argmax_out;
+  p.done = done;
   p.tau_i = tau_i;
   p.tau_f = tau_f;
   p.period = period;
@@ -999,7 +1028,8 @@ static cudaError_t conventional_tc(const void* psi_hi, const void* psi_lo, bool 
 static cudaError_t interp_tc(const void* w_hi, const void* w_lo, const void* xi_hi,
                              const void* xi_lo, bool f16, float scale, int F, int J, int T_pad,
                              float* maps, unsigned long long* keys, int kb_per_group,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, int32_t* argmax_out = nullptr,
+                             unsigned int* done = nullptr) {
   if (F == 0 || J == 0) return cudaSuccess;
   TcParams p{};
   p.F = F;
@@ -1011,6 +1041,8 @@ static cudaError_t interp_tc(const void* w_hi, const void* w_lo, const void* xi_
   p.scale = scale;
   p.maps = maps;
   p.keys = keys;
+  p.argmax_out = argmax_out;
+  p.done = done;
   CUtensorMap ah, al, bh, bl;
   const int brows = 16;  // B boxes of 16 rows (any item width)
   cudaError_t e = make_map(&ah, w_hi, J, T_pad, kTcM, f16);
@@ -1031,9 +1063,12 @@ cudaError_t launch_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, 
                                         const void* xi_hi, const void* xi_lo, float xi_scale,
                                         int F, int J, int T_pad, float* maps,
                                         unsigned long long* keys, int kb_per_group,
+                                        int32_t* argmax_out, unsigned int* done,
                                         cudaStream_t stream) {
   if (F == 0 || J == 0) return cudaSuccess;
   TcParams p{};
+  p.argmax_out = argmax_out;
+  p.done = done;
   p.F = F;
   p.J = J;
   p.num_kb = (T_pad + kTcKBlock16 - 1) / kTcKBlock16;
@@ -1065,9 +1100,10 @@ cudaError_t launch_conventional_tc16(const void* psi_hi, const void* psi_lo, flo
                                      int P, int Kb, int period, const int32_t* tau_i,
                                      const float* tau_f, int J, float* maps,
                                      unsigned long long* keys, int kb_per_group,
+                                     int32_t* argmax_out, unsigned int* done,
                                      cudaStream_t stream) {
   return conventional_tc(psi_hi, psi_lo, true, psi_scale, F, P, Kb, period, tau_i, tau_f, J, maps,
-                         keys, kb_per_group, stream);
+                         keys, kb_per_group, stream, argmax_out, done);
 }
 
 cudaError_t launch_interp_tc(const float* w_hi, const float* w_lo, const float* xi_hi,
@@ -1080,9 +1116,9 @@ cudaError_t launch_interp_tc(const float* w_hi, const float* w_lo, const float* 
 cudaError_t launch_interp_tc16(const void* w_hi, const void* w_lo, float w_scale,
                                const void* xi_hi, const void* xi_lo, float xi_scale, int F, int J,
                                int T_pad, float* maps, unsigned long long* keys, int kb_per_group,
-                               cudaStream_t stream) {
+                               int32_t* argmax_out, unsigned int* done, cudaStream_t stream) {
   return interp_tc(w_hi, w_lo, xi_hi, xi_lo, true, 1.0f / (w_scale * xi_scale), F, J, T_pad, maps,
-                   keys, kb_per_group, stream);
+                   keys, kb_per_group, stream, argmax_out, done);
 }
 
 // hi = tf32(x), lo = tf32(x - hi): operand split for 3xTF32

@@ -231,6 +231,18 @@ class SrpPlan:
         self.weight_mode = "stored" if store else "onthefly"
 
     # ---------------------------------------------------------------- helpers
+    def _argmax_state(self, F):
+        """Persistent zeroed (keys [F], done counter) for the tensor-core
+        kernels' in-kernel argmax finish: the last CTA decodes the keys and
+        resets both, so no reset / decode launches are needed per call."""
+        st = getattr(self, "_am_state", None)
+        if st is None:
+            st = self._am_state = {}
+        if F not in st:
+            st[F] = (torch.zeros(F, dtype=torch.int64, device=self.device),
+                     torch.zeros(1, dtype=torch.int32, device=self.device))
+        return st[F]
+
     def _keys(self, F):
         keys = torch.empty(F, dtype=torch.int64, device=self.device)
         N.call("srpb_argmax_keys_reset", N.ptr(keys), F, N.stream_handle(self.device))
@@ -391,14 +403,18 @@ class SrpPlan:
         if maps:
             out = maps_out if maps_out is not None else torch.empty(
                 (F, self.J), dtype=torch.float32, device=self.device)
-        keys = self._keys(F)
         s = N.stream_handle(self.device)
         if self._use_tc(F, "conv") and self._f16_ok("conv", _bounded):
             hi, lo = self.split_f16(psi, self.F16_UNIT_SCALE)
+            keys, done = self._argmax_state(F)
+            idx = torch.empty(F, dtype=torch.int32, device=self.device)
             self._main("srpb_conventional_tc16", N.ptr(hi), N.ptr(lo), self.F16_UNIT_SCALE, F,
                        self.P, self.Kb, self.period, N.ptr(self.conv_ti), N.ptr(self.conv_tf),
-                       self.J, N.ptr(out), N.ptr(keys), self.kb_per_group16, s)
-        elif self._use_tc(F, "conv"):
+                       self.J, N.ptr(out), N.ptr(keys), self.kb_per_group16, N.ptr(idx),
+                       N.ptr(done), s)
+            return out, idx
+        keys = self._keys(F)
+        if self._use_tc(F, "conv"):
             hi, lo = self.split_tf32(psi)
             self._main("srpb_conventional_tc", N.ptr(hi), N.ptr(lo), F, self.P, self.Kb, self.period,
                    N.ptr(self.conv_ti), N.ptr(self.conv_tf), self.J, N.ptr(out), N.ptr(keys),
@@ -447,24 +463,28 @@ class SrpPlan:
                    N.ptr(out), N.ptr(keys), s)
         return out, self.keys_to_index(keys)
 
-    def _approx_tc16(self, xh, xl, out, keys):
+    def _approx_tc16(self, xh, xl, out):
         """K4 in 3xFP16 from the fp16 split of xi_scale16 * Xi (weights from
         the stored W split, or generated in tensor memory when W is not
-        stored)."""
+        stored); argmax finished in-kernel."""
+        F = xh.shape[0]
+        keys, done = self._argmax_state(F)
+        idx = torch.empty(F, dtype=torch.int32, device=self.device)
         if self.W is None:
             self._main("srpb_interp_tc16_onthefly", N.ptr(self.sx_i), N.ptr(self.sx_f), self.P,
                        N.ptr(self.off), N.ptr(self.reach), N.ptr(xh), N.ptr(xl),
-                       self.xi_scale16, xh.shape[0], self.J, self.T_pad, N.ptr(out), N.ptr(keys),
-                       self.interp_kb_per_group16, N.stream_handle(self.device))
-            return out, self.keys_to_index(keys)
+                       self.xi_scale16, F, self.J, self.T_pad, N.ptr(out), N.ptr(keys),
+                       self.interp_kb_per_group16, N.ptr(idx), N.ptr(done),
+                       N.stream_handle(self.device))
+            return out, idx
         if self.W16 is None:
             self.W16 = self.split_f16(self.W, self.F16_UNIT_SCALE)
         xs = self.xi_scale16
         self._main("srpb_interp_tc16", N.ptr(self.W16[0]), N.ptr(self.W16[1]),
-                   self.F16_UNIT_SCALE, N.ptr(xh), N.ptr(xl), xs, xh.shape[0], self.J, self.T_pad,
-                   N.ptr(out), N.ptr(keys), self.interp_kb_per_group16,
+                   self.F16_UNIT_SCALE, N.ptr(xh), N.ptr(xl), xs, F, self.J, self.T_pad,
+                   N.ptr(out), N.ptr(keys), self.interp_kb_per_group16, N.ptr(idx), N.ptr(done),
                    N.stream_handle(self.device))
-        return out, self.keys_to_index(keys)
+        return out, idx
 
     def _approx_tc(self, xh, xl, out, keys):
         if self.W_hi is None:
@@ -499,7 +519,7 @@ class SrpPlan:
                                   device=self.device) if maps else None
                 if f16:
                     xh, xl = self.lattice_from_spectra(Y, weighting, phat_floor, split="f16")
-                    return self._approx_tc16(xh, xl, out, self._keys(F))
+                    return self._approx_tc16(xh, xl, out)
                 xh, xl = self.lattice_from_spectra(Y, weighting, phat_floor, split=True)
                 return self._approx_tc(xh, xl, out, self._keys(F))
             return self.approx(self.lattice_from_spectra(Y, weighting, phat_floor), maps)
