@@ -328,10 +328,12 @@ class SrpPlan:
         return outs[1:] if split else outs[0]
 
     def _use_tc(self, F, kind):
-        """Size heuristic for the tensor-core kernels (not a backend switch:
-        both are this library's sm_100a kernels).  A tcgen05 tile is 128
-        candidates x >= 32 frames; below 32 frames the SIMT kernel wastes
-        less work."""
+        """Tensor-core kernels whenever the plan allows them (not a backend
+        switch: both families are this library's sm_100a kernels).  Measured
+        at C5 (J = 200k): even at F = 1 the tcgen05 kernels win (the steering
+        phases / weights dominate and are shared by the frames of a tile), so
+        the SIMT kernels serve only shapes the tensor-core path cannot take
+        (Kb % 16 != 0, non-harmonic bins, tf32 without a stored W)."""
         if self.backend == "simt":
             return False
         if kind == "conv":
@@ -340,11 +342,9 @@ class SrpPlan:
             ok = True
         else:                     # 3xTF32 K4 needs the stored W
             ok = self.W is not None
-        if self.backend == "tc":
-            if not ok:
-                raise ValueError(f"tensor-core {kind} path unavailable for this plan")
-            return True
-        return ok and F >= 32
+        if self.backend == "tc" and not ok:
+            raise ValueError(f"tensor-core {kind} path unavailable for this plan")
+        return ok
 
     #: optional profiler hook: an object with before(name) / after(name)
     #: called around each main kernel launch (bench.py records CUDA events)
