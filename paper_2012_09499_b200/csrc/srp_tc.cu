@@ -186,6 +186,19 @@ __device__ __forceinline__ void tc_drain(const TcParams& p, TcSmem* bar, bool re
   }
 }
 
+// One 16-column chunk C of a TMEM accumulator half folded into the totals
+// (compile-time C keeps `tot` in registers).
+template <int C>
+__device__ __forceinline__ void tc_drain_chunk16(uint32_t base, float (&tot)[kTcMaxN / 2]) {
+  if constexpr (16 * C < kTcMaxN / 2) {
+    uint32_t r[16];
+    tmem_ld16(base + 16 * C, r);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) tot[16 * C + i] += __uint_as_float(r[i]);
+  }
+}
+
 // Final output of one tile: scale, store maps, fused per-frame argmax
 // (lowest j on ties), then reset the totals for the next tile.  The four
 // lane-quarter warps of a column half combine their warp maxima in shared
@@ -761,6 +774,60 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     TCP_DECL(c_drain);
     TCP_DECL(c_write);
     TCP_DECL(c_all);
+    // incremental fold (generator modes): one 16-column chunk per generated K
+    // block, so a drain never stalls the A generation for long; the buffer
+    // is released when the group is complete (the ping-pong leaves the MMA
+    // kb_per_group blocks of slack)
+    int d_chunk = -1;  // chunk of group `drained` next to fold (-1: not started)
+    uint32_t d_base = 0;
+    auto finish_group = [&](const Item& t) {
+      if (d_gl == p.groups_per_tile - 1) {
+        TCP_T0();
+        tc_write_tile(p, bar, t.m0, t.n0, t.nc, quarter, half, lane, tot);
+        TCP_ACC(c_write);
+        ++d_it;
+        d_gl = 0;
+        d_last_kg = d_it * p.num_kb + min(p.kb_per_group, p.num_kb) - 1;
+      } else {
+        ++d_gl;
+        d_last_kg = d_it * p.num_kb + min((d_gl + 1) * p.kb_per_group, p.num_kb) - 1;
+      }
+      ++drained;
+    };
+    auto fold_step = [&]() {
+      const Item t = item(d_it);
+      TCP_T0();
+      const int b = drained & 1;
+      if (d_chunk < 0) {
+        mbar_wait(&bar->acc_full[b], (drained >> 1) & 1);
+        tc_fence_after();
+        d_base = tmem + (static_cast<uint32_t>(32 * quarter) << 16) +
+                 static_cast<uint32_t>(b * p.N + half * (t.nc / 2));
+        d_chunk = 0;
+      }
+      switch (d_chunk) {
+        case 0: tc_drain_chunk16<0>(d_base, tot); break;
+        case 1: tc_drain_chunk16<1>(d_base, tot); break;
+        case 2: tc_drain_chunk16<2>(d_base, tot); break;
+        case 3: tc_drain_chunk16<3>(d_base, tot); break;
+        default: tc_drain_chunk16<4>(d_base, tot); break;
+      }
+      if (++d_chunk == t.nc / 32) {  // group folded: release the buffer
+        tc_fence_before();
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+          if (!leader)
+            mbar_arrive_cluster(acc_empty_addr0 + 8u * b);
+          else
+            mbar_arrive(&bar->acc_empty[b]);
+        }
+        d_chunk = -1;
+        TCP_ACC(c_drain);
+        finish_group(t);
+      } else {
+        TCP_ACC(c_drain);
+      }
+    };
     auto fold_next = [&]() {
       const Item t = item(d_it);
       { TCP_T0();
@@ -819,10 +886,12 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
             s = 0;
             ph ^= 1;
           }
-          // fold groups whose last K block is at least S behind
-          while (drained < total_groups && d_last_kg <= kg - S) fold_next();
+          // fold one chunk of the oldest group whose last K block is at
+          // least S behind
+          if (d_chunk >= 0 || (drained < total_groups && d_last_kg <= kg - S)) fold_step();
         }
       }
+      while (drained < total_groups) fold_step();
     }
     while (drained < total_groups) fold_next();
     TCP_ACC(c_all); }
