@@ -322,6 +322,35 @@ int srpb_argmax_keys_reset(unsigned long long* keys, int F, void* stream);
 /* idx[f] = candidate index held by keys[f] (int32). */
 int srpb_keys_to_index(const unsigned long long* keys, int F, int32_t* idx, void* stream);
 
+/* ---- device-side cross-checks ---------------------- */
+
+/*
+ * Quadratic-form SRP map in fp64 -- replaces srp.srp_oracle
+ * (pkg/src/srpfast/srp.py:468-515) for pair cross-spectra:
+ *   maps[f, j] = sum_k sum_p 2 Re(Psi[f,p,k] conj(h_m) h_m'),
+ *   h_m = exp(-i omega[k] tau_rel[j, m]),  (m, m') = (pair_m[p], pair_mp[p])
+ * which equals sum_k [h^H Psi h - tr Psi] for the cross matrix assembled from
+ * the pairs (srp.py:432-442).  Every exponential is an fp64 sincos (no
+ * recurrence, no tensor cores): an independent check of K2.
+ *   Psi [F, P, Kb] complex64; omega [Kb] fp64; tau_rel [J, M] fp64 delays
+ *   relative to mic 0 (column 0 = 0, columns 1.. = the first M-1 canonical
+ *   TDOA columns, srp.py:495-498); maps [F, J] fp64 out.
+ */
+int srpb_srp_quadform(const float* Psi, int F, int P, int Kb, const double* omega,
+                      const double* tau_rel, int J, int M, const int32_t* pair_m,
+                      const int32_t* pair_mp, double* maps, void* stream);
+
+/*
+ * Per-frame map error energy for metrics.approximation_error_db
+ * (pkg/src/srpfast/metrics.py:22-41): num[f] = sum_j (ref - app)^2,
+ * den[f] = sum_j ref^2, fp64 accumulation in a fixed order.
+ *   ref, app [F, J], fp32 or fp64 each (ref_f64 / app_f64 = 1 for fp64);
+ *   scratch: SRPB_MAP_ERROR_SCRATCH * F doubles; num, den [F] fp64 out.
+ */
+#define SRPB_MAP_ERROR_SCRATCH 128
+int srpb_map_error(const void* ref, int ref_f64, const void* app, int app_f64, int F, int J,
+                   double* scratch, double* num, double* den, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,7 @@ from .geometry import (
     tdoa_farfield,
     tdoa_nearfield,
 )
+from .metrics import APPROX_ERROR_FLOOR_DB, approximation_error_db, map_error_energy
 from .pipeline import ChunkedRunner, chunk_bounds
 from .plan import CapturedStep, SrpPlan, lattice_layout, standalone_argmax
 from .spectral import (
@@ -50,6 +51,8 @@ from .srp import (
     srp_approx_frames,
     srp_conventional,
     srp_conventional_frames,
+    srp_oracle,
+    srp_oracle_frames,
 )
 
 __version__ = "0.1.0"
@@ -66,6 +69,7 @@ __all__ = [
     "ComplexityReport", "GccLattice", "MultCounter", "SincTable", "SrpMap",
     "argmax_candidate", "build_gcc_lattice", "build_gcc_lattice_frames", "complexity_report",
     "gcc_at_lag", "lattice_half_counts", "precompute_sinc_table", "srp_approx",
-    "srp_approx_frames", "srp_conventional", "srp_conventional_frames",
+    "srp_approx_frames", "srp_conventional", "srp_conventional_frames", "srp_oracle",
+    "srp_oracle_frames", "APPROX_ERROR_FLOOR_DB", "approximation_error_db", "map_error_energy",
     "__version__",
 ]

@@ -64,6 +64,10 @@ _SIGNATURES = {
     "srpb_argmax_f64": [c_void_p, c_int, c_int, c_void_p, c_void_p],
     "srpb_argmax_keys_reset": [c_void_p, c_int, c_void_p],
     "srpb_keys_to_index": [c_void_p, c_int, c_void_p, c_void_p],
+    "srpb_srp_quadform": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
+                          c_void_p, c_void_p, c_void_p, c_void_p],
+    "srpb_map_error": [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p,
+                       c_void_p, c_void_p],
 }
 _RESTYPES = {"srpb_last_error": ctypes.c_char_p}
 
@@ -118,7 +122,7 @@ def stream_handle(device=None):
 _LAUNCHING = {n for n in _SIGNATURES if n not in ("srpb_abi_version", "srpb_last_error")}
 # entry points that launch more than one kernel (floor/fill pass + psi pass;
 # speculative-floor lattice + its fix-up pass)
-_KERNELS_PER_CALL = {"srpb_gcc_phat": 2, "srpb_lattice_from_spectra": 2}
+_KERNELS_PER_CALL = {"srpb_gcc_phat": 2, "srpb_lattice_from_spectra": 2, "srpb_map_error": 2}
 _launches = 0
 
 

@@ -58,6 +58,10 @@ cudaError_t launch_interp_tc16_onthefly(const int32_t*, const float*, int, const
 cudaError_t launch_argmax_f64(const double*, int, int, int32_t*, cudaStream_t);
 cudaError_t launch_keys_reset(unsigned long long*, int, cudaStream_t);
 cudaError_t launch_keys_to_index(const unsigned long long*, int, int32_t*, cudaStream_t);
+cudaError_t launch_quadform(const float*, int, int, int, const double*, const double*, int, int,
+                            const int32_t*, const int32_t*, double*, cudaStream_t);
+cudaError_t launch_map_error(const void*, int, const void*, int, int, int, double*, double*,
+                             double*, cudaStream_t);
 }  // namespace srpb
 
 namespace {
@@ -95,7 +99,7 @@ static bool pow2_scale(float s) {
   return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
 }
 
-int srpb_abi_version(void) { return 9; }
+int srpb_abi_version(void) { return 10; }
 
 const char* srpb_last_error(void) { return g_err; }
 
@@ -390,6 +394,29 @@ int srpb_argmax_keys_reset(unsigned long long* keys, int F, void* stream) {
 int srpb_keys_to_index(const unsigned long long* keys, int F, int32_t* idx, void* stream) {
   REQUIRE(F >= 0 && (F == 0 || (keys && idx)), "srpb_keys_to_index: bad argument");
   return status(srpb::launch_keys_to_index(keys, F, idx, S(stream)), "srpb_keys_to_index");
+}
+
+int srpb_srp_quadform(const float* Psi, int F, int P, int Kb, const double* omega,
+                      const double* tau_rel, int J, int M, const int32_t* pair_m,
+                      const int32_t* pair_mp, double* maps, void* stream) {
+  REQUIRE(F >= 0 && P >= 1 && Kb >= 1 && J >= 0 && M >= 2,
+          "srpb_srp_quadform: bad shape F=%d P=%d Kb=%d J=%d M=%d", F, P, Kb, J, M);
+  REQUIRE(M <= 64, "srpb_srp_quadform: at most 64 channels supported, got %d", M);
+  REQUIRE(P <= 2016, "srpb_srp_quadform: at most 2016 pairs supported, got %d", P);
+  REQUIRE(F == 0 || J == 0 || (Psi && omega && tau_rel && pair_m && pair_mp && maps),
+          "srpb_srp_quadform: null pointer");
+  return status(srpb::launch_quadform(Psi, F, P, Kb, omega, tau_rel, J, M, pair_m, pair_mp, maps,
+                                      S(stream)),
+                "srpb_srp_quadform");
+}
+
+int srpb_map_error(const void* ref, int ref_f64, const void* app, int app_f64, int F, int J,
+                   double* scratch, double* num, double* den, void* stream) {
+  REQUIRE(F >= 0 && J >= 1, "srpb_map_error: bad shape F=%d J=%d", F, J);
+  REQUIRE(F == 0 || (ref && app && scratch && num && den), "srpb_map_error: null pointer");
+  return status(srpb::launch_map_error(ref, ref_f64, app, app_f64, F, J, scratch, num, den,
+                                       S(stream)),
+                "srpb_map_error");
 }
 
 }  // extern "C"

@@ -91,6 +91,52 @@ def keys_index(keys_u: torch.Tensor) -> torch.Tensor:
     return (0xFFFFFFFF - (keys_u & 0xFFFFFFFF)).to(torch.int64)
 
 
+def keys_from_maps(maps: torch.Tensor, argmax: torch.Tensor, j_offset: int = 0) -> torch.Tensor:
+    """Packed keys (``common.cuh`` make_key) of each frame's maximum, from
+    fp32 maps [F, J_r] and their argmax [F] over a candidate slice starting
+    at global index ``j_offset`` (uint64 bits in an int64 tensor)."""
+    v = maps.gather(1, argmax.to(torch.int64)[:, None])[:, 0].float() + 0.0  # -0 -> +0
+    b = v.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    neg = (b & 0x80000000) != 0
+    ordered = torch.where(neg, (~b) & 0xFFFFFFFF, b | 0x80000000)
+    j = argmax.to(torch.int64) + int(j_offset)
+    return (ordered << 32) | (0xFFFFFFFF - j)
+
+
+def gather_candidates(local: torch.Tensor, num_candidates: int, align: int = 128,
+                      group=None) -> torch.Tensor:
+    """All-gather per-rank candidate blocks ``[F, J_r]`` into ``[F, J]``
+    (ranges from :func:`candidate_ranges`; uneven blocks padded, trimmed)."""
+    world = dist.get_world_size(group)
+    ranges = candidate_ranges(num_candidates, world, align)
+    width = max(max(hi - lo for lo, hi in ranges), 1)
+    F = local.shape[0]
+    pad = torch.zeros((width, F), dtype=local.dtype, device=local.device)
+    pad[: local.shape[1]] = local.t()
+    out = torch.empty((world * width, F), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    parts = [out[r * width: r * width + (hi - lo)] for r, (lo, hi) in enumerate(ranges)]
+    return torch.cat(parts, dim=0).t().contiguous()
+
+
+def run_candidate_sharded(plan_local, Y, j_offset, num_candidates, path="approx", maps=True,
+                          align=128, group=None):
+    """Batch-1 / small-batch sharding: ``plan_local`` covers
+    this rank's candidate range ``[j_offset, j_offset + plan_local.J)`` of
+    :func:`candidate_ranges`; every rank runs all frames of ``Y``.  The
+    global argmax is one all-reduce MAX of the packed keys (largest value,
+    then lowest global index -- deterministic); maps are all-gathered only
+    when requested.  Returns (maps [F, J] or None, argmax [F] int32)."""
+    m, am = plan_local.run(Y, path, maps=True)
+    keys = keys_from_maps(m, am, j_offset)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        keys = allreduce_argmax(keys, group)
+        m = gather_candidates(m, num_candidates, align, group) if maps else None
+    elif not maps:
+        m = None
+    return m, keys_index(keys).to(torch.int32)
+
+
 def run_frame_sharded(plan, Y_all, path="approx", maps=True, gather=True, group=None):
     """Run ``plan`` on this rank's frame range of ``Y_all`` [F, M, Kb] and
     optionally gather maps/argmax from all ranks (NCCL all-gather)."""

@@ -6,9 +6,10 @@ and sinc table is computed by ``libsrpb.so`` kernels through
 :class:`~.plan.SrpPlan`.  Results stay on the device until a caller reads
 ``.values`` / ``.samples`` / ``.weights`` (materialised once per batch).
 
-Not mirrored: ``srp_oracle`` (``srp.py:468-515``), the quadratic-form
-reference the reference itself uses only to verify the other paths; it stays
-a CPU cross-check (``oracle/``) and is out of scope for the device path.
+``srp_oracle`` (``srp.py:468-515``), the quadratic-form map the reference
+uses to verify its fast paths, runs on the device too, in fp64 with direct
+exponentials (``srpb_srp_quadform``): an independent full-scale check of the
+conventional path, not a CPU fallback.
 """
 
 from __future__ import annotations
@@ -40,6 +41,8 @@ __all__ = [
     "srp_conventional_frames",
     "srp_approx",
     "srp_approx_frames",
+    "srp_oracle",
+    "srp_oracle_frames",
     "argmax_candidate",
     "complexity_report",
 ]
@@ -112,10 +115,13 @@ def argmax_candidate(srp_map) -> int:
     if am is not None:
         return int(am)
     dev_row = srp_map.device_values() if hasattr(srp_map, "device_values") else None
-    if dev_row is not None:
+    if dev_row is not None and dev_row.dtype == torch.float32:
         return int(standalone_argmax(dev_row.contiguous())[0].item())
     dev = N.require_cuda()
-    v = torch.as_tensor(np.ascontiguousarray(srp_map.values, dtype=np.float64), device=dev)
+    if dev_row is not None:  # fp64 device maps (srp_oracle)
+        v = dev_row.contiguous()
+    else:
+        v = torch.as_tensor(np.ascontiguousarray(srp_map.values, dtype=np.float64), device=dev)
     idx = torch.empty(1, dtype=torch.int32, device=dev)
     N.call("srpb_argmax_f64", N.ptr(v), 1, v.numel(), N.ptr(idx), N.stream_handle(dev))
     return int(idx.item())
@@ -453,6 +459,81 @@ def srp_conventional_frames(frames, grid, counter=None, maps=True) -> list:
 def srp_conventional(cross, grid, counter=None) -> SrpMap:
     """Exact SRP map of one frame (``srp.py:376-388``)."""
     return srp_conventional_frames([cross], grid, counter=counter)[0]
+
+
+class _IndexPair:
+    """Pair indices only: what the cross matrix of ``srp_oracle`` needs."""
+
+    __slots__ = ("index_m", "index_m_prime")
+
+    def __init__(self, m, mp):
+        self.index_m, self.index_m_prime = m, mp
+
+
+def _full_pair_count(n_pairs):
+    m = int(round((1.0 + math.sqrt(1.0 + 8.0 * n_pairs)) / 2.0))
+    if m * (m - 1) // 2 != n_pairs:
+        raise ValueError(f"{n_pairs} pair rows do not form a full pair set")
+    return m
+
+
+def srp_oracle_frames(frames, grid, weighting="phat", phat_floor=None) -> list:
+    """Batched :func:`srp_oracle`: one ``srpb_srp_quadform`` launch (fp64)."""
+    frames = list(frames)
+    if not frames:
+        return []
+    table = grid.require_table()
+    dev = N.require_cuda()
+    if all(hasattr(fr, "pairs") for fr in frames):  # CrossSpectra (srp.py:484-487)
+        crosses = frames
+        m = _full_pair_count(len(crosses[0].pairs))
+    else:  # spectral frames: the pair rows of the weighted cross matrix (:488-491)
+        from .spectral import cross_spectrum_frames
+        m = int(getattr(frames[0], "num_channels", 0) or np.shape(frames[0].spectra)[0])
+        pairs = [_IndexPair(b, a) for a in range(m) for b in range(a + 1, m)]
+        crosses = cross_spectrum_frames(frames, pairs, weighting, phat_floor, device=dev)
+    if table.shape[1] != m * (m - 1) // 2:
+        raise ValueError(
+            f"grid table has {table.shape[1]} pair columns, expected "
+            f"{m * (m - 1) // 2} for {m} channels"
+        )
+    omega = np.asarray(crosses[0].bin_frequencies, dtype=np.float64)
+    for cr in crosses:
+        if len(cr.pairs) != len(crosses[0].pairs) or np.any(
+                np.asarray(cr.bin_frequencies, dtype=np.float64) != omega):
+            raise ValueError("all frames must share the same pairs and bin frequencies")
+    pm = torch.as_tensor([p.index_m for p in crosses[0].pairs], dtype=torch.int32, device=dev)
+    pmp = torch.as_tensor([p.index_m_prime for p in crosses[0].pairs], dtype=torch.int32,
+                          device=dev)
+    # delays of each mic relative to mic 0: canonical columns 0 .. M-2 (:495-498)
+    tau_rel = np.concatenate([np.zeros((table.shape[0], 1)), table[:, : m - 1]], axis=1)
+    maps = quadform_maps(_device_psi(crosses, dev), omega, torch.as_tensor(
+        np.ascontiguousarray(tau_rel), device=dev), pm, pmp)
+    rows = _DeviceRows(maps, np.float64)
+    return [SrpMap(None, "oracle", frame_index=getattr(fr, "frame_index", 0), _rows=rows, _row=i)
+            for i, fr in enumerate(frames)]
+
+
+def srp_oracle(data, grid, weighting="phat", phat_floor=None, candidate_chunk=256) -> SrpMap:
+    """Quadratic-form SRP map, trace removed (``srp.py:468-515``), in fp64 on
+    the device.  Accepts a spectral frame or pair cross-spectra, like the
+    reference; ``candidate_chunk`` is accepted for signature parity (the
+    kernel tiles candidates itself)."""
+    return srp_oracle_frames([data], grid, weighting, phat_floor)[0]
+
+
+def quadform_maps(psi, omega, tau_rel, pair_m, pair_mp) -> torch.Tensor:
+    """``srpb_srp_quadform``: psi [F, P, Kb] complex64, tau_rel [J, M] fp64
+    (device) -> maps [F, J] fp64."""
+    dev = psi.device
+    psi, tau_rel = psi.contiguous(), tau_rel.contiguous()
+    F, P, Kb = psi.shape
+    J, M = tau_rel.shape
+    om = torch.as_tensor(np.ascontiguousarray(omega, dtype=np.float64), device=dev)
+    maps = torch.empty((F, J), dtype=torch.float64, device=dev)
+    N.call("srpb_srp_quadform", N.ptr(psi), F, P, Kb, N.ptr(om), N.ptr(tau_rel), J, M, N.ptr(pair_m), N.ptr(pair_mp), N.ptr(maps),
+           N.stream_handle(dev))
+    return maps
 
 
 @dataclass(frozen=True)

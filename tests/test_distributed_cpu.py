@@ -57,7 +57,16 @@ def _worker(rank, world, port, F, J, maps_all, ret):
         red = D.allreduce_argmax(kt)
         idx = D.keys_index(red)
         ok_cand = torch.equal(idx, torch.from_numpy(np.argmax(maps_all, axis=1)))
-        ret[rank] = (ok_frames, ok_am, ok_cand)
+        # the torch key builder used by run_candidate_sharded agrees
+        sl = torch.from_numpy(maps_all[:, jlo:jhi].copy())
+        am_l = torch.from_numpy(np.argmax(maps_all[:, jlo:jhi], axis=1))
+        k2 = D.keys_from_maps(sl, am_l, jlo)
+        ok_keys = torch.equal(k2, kt)
+        idx2 = D.keys_index(D.allreduce_argmax(k2))
+        ok_cand = ok_cand and torch.equal(idx2, idx)
+        # candidate-block gather reassembles the full maps
+        ok_gather = torch.equal(D.gather_candidates(sl, J, align=8), torch.from_numpy(maps_all))
+        ret[rank] = (ok_frames, ok_am, ok_cand and ok_keys and ok_gather)
     finally:
         dist.destroy_process_group()
 
@@ -69,6 +78,8 @@ def test_two_rank_gather_and_candidate_argmax(F):
     maps_all = rng.standard_normal((F, J)).astype(np.float32)
     maps_all[0, 5] = maps_all[0, 30] = 9.0   # exact tie across ranks: lowest j wins
     maps_all[1, :] = 0.0                       # all-equal frame -> index 0
+    maps_all[2, :] = -1.0                      # negative maximum, ties everywhere
+    maps_all[2, 20] = -0.5
     mgr = mp.Manager()
     ret = mgr.dict()
     port = _free_port()

@@ -38,7 +38,7 @@ def test_library_exports_every_header_symbol():
 
 def test_abi_version_and_error_reporting_without_gpu():
     lib = _native.load()
-    assert lib.srpb_abi_version() == 9
+    assert lib.srpb_abi_version() == 10
     # invalid arguments are rejected on the host before any CUDA call
     with pytest.raises(ValueError, match="bad shape"):
         _native.call("srpb_gcc_phat", None, -1, 4, 64, None, None, 6, 0, 1e-12, -1.0, None, None,
@@ -225,3 +225,32 @@ def test_chunk_bounds():
     assert chunk_bounds(100, 3) == [(0, 34), (34, 67), (67, 100)]
     b = chunk_bounds(1000, 7)
     assert b[0][0] == 0 and b[-1][1] == 1000 and all(x[1] == y[0] for x, y in zip(b, b[1:]))
+
+
+def test_harness_install_rebinds_and_restores():
+    """harness.installed swaps exactly the hot-path names a harness module
+    binds, and restores the originals."""
+    import types
+    import paper_2012_09499_b200 as B
+    from paper_2012_09499_b200 import harness as H
+
+    def stub(*a, **k):
+        raise NotImplementedError
+
+    ns = types.SimpleNamespace(cross_spectrum=stub, srp_approx=stub, argmax_candidate=stub,
+                               approximation_error_db=stub, unrelated=stub)
+    table = H.drop_ins()
+    assert set(table) == set(H.SWAPPED_NAMES)
+    assert table["srp_oracle"] is B.srp_oracle
+    assert table["approximation_error_db"] is B.approximation_error_db
+    with H.installed(ns):
+        assert ns.cross_spectrum is B.cross_spectrum
+        assert ns.srp_approx is B.srp_approx
+        assert ns.argmax_candidate is B.argmax_candidate
+        assert ns.unrelated is stub
+        assert not hasattr(ns, "srp_oracle")  # only names the module already binds
+    assert ns.cross_spectrum is stub and ns.srp_approx is stub
+    restore = H.install(ns)
+    assert ns.approximation_error_db is B.approximation_error_db
+    restore()
+    assert ns.approximation_error_db is stub

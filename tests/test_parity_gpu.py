@@ -486,3 +486,34 @@ def test_full_c2_frame_sharding_and_determinism():
     for i, f in enumerate(sel):
         assert rel_l2(conv[f].cpu().numpy(), conv_ref[i]) <= REL_L2_TOL
         assert int(np.argmax(conv_ref[i])) == int(torch.argmax(conv[f]).item())
+
+
+@pytest.mark.parametrize("path", ["approx", "conventional"])
+def test_candidate_sharding_batch1(path):
+    """C5-style batch 1: the candidate-range plans two ranks
+    would hold reproduce the full plan's maps bitwise, and their packed keys
+    reduce (MAX, as the all-reduce does) to the full plan's argmax."""
+    from paper_2012_09499_b200 import distributed as D
+    scene = scenes.make_c2(num_frames=3)
+    pairs = O.canonical_pairs(8)
+    pm = np.array([a for a, _ in pairs], np.int32)
+    pmp = np.array([b for _, b in pairs], np.int32)
+    bounds = np.array([np.linalg.norm(scene.mic_pos[a] - scene.mic_pos[b]) / 343.0
+                       for a, b in pairs])
+    tdoa = O.tdoa_table_nearfield(scene.mic_pos, scene.grid, pairs, 343.0)
+    omega = O.bin_frequencies(16000.0, 1024)
+    J = tdoa.shape[0]
+    full = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=4)
+    for F in (1, 3):
+        Y = dev(scene.Y[:F])
+        m_full, a_full = full.run(Y, path)
+        maps, keys = [], []
+        for lo, hi in D.candidate_ranges(J, 2):
+            p = SrpPlan(tdoa[lo:hi], pm, pmp, bounds, omega, sample_period=T, n_aux=4)
+            m, a = D.run_candidate_sharded(p, Y, lo, J, path)  # no process group: local
+            assert int(a.min()) >= lo and int(a.max()) < hi
+            maps.append(m)
+            keys.append(D.keys_to_signed(D.keys_from_maps(m, a.long() - lo, lo)))
+        assert torch.equal(torch.cat(maps, dim=1), m_full)
+        red = D.keys_from_signed(torch.maximum(keys[0], keys[1]))
+        assert torch.equal(D.keys_index(red).to(torch.int32), a_full)
