@@ -338,6 +338,9 @@ def run_ours(args):
     # per candidate tile, independent of the frames in it)
     runners = {"approx": ChunkedRunner(plan, F, Y.shape[1], "approx", chunks=args.e2e_chunks),
                "conventional": ChunkedRunner(plan, F, Y.shape[1], "conventional", chunks=2)}
+    # argmax-only serving (maps never leave the device; the drop-in's SrpMap
+    # fetches values lazily, so a caller reading only argmax_candidate pays this)
+    runner_am = ChunkedRunner(plan, F, Y.shape[1], "approx", chunks=3, maps=False)
 
     # audio-input end to end: pinned host audio of the
     # C2 shape (8 x 160,000 samples -> the same 311 frames), K0 STFT inside
@@ -363,6 +366,9 @@ def run_ours(args):
 
     def e2e_step(path):
         runners[path].run(Y_host, maps_host, am_host)
+
+    def e2e_argmax_step(path):
+        runner_am.run(Y_host, None, am_host)
 
     def timed(fn, path, profile=False):
         for _ in range(args.warmup):
@@ -408,6 +414,7 @@ def run_ours(args):
     e2e_a, _, _ = timed(e2e_step, "approx")
     e2e_c, _, _ = timed(e2e_step, "conventional")
     e2e_x, _, _ = timed(e2e_audio_step, "approx")
+    e2e_m, _, _ = timed(e2e_argmax_step, "approx")
     clk = clocks.stop()
 
     units = F * J * world
@@ -439,6 +446,11 @@ def run_ours(args):
                       "api": "ChunkedRunner(audio=...) on pinned host audio [8, %d] (seeded "
                              "white noise of the C2 shape): K0 STFT + approx path per chunk"
                              % L_audio},
+        "e2e_argmax_only": {"value": units / (e2e_m * 1e-3), "unit": UNIT,
+                            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": F * 4,
+                            "ms_per_step": e2e_m,
+                            "api": "ChunkedRunner(maps=False, 3 chunks): pinned host Y -> "
+                                   "pinned host argmax; maps not materialised"},
         "gpu_launches": launches_a,
         "roofline": roof_a,
         "conventional": {"value": units / (ms_c * 1e-3), "unit": UNIT, "ms_per_step": ms_c,

@@ -248,13 +248,17 @@ int srpb_interp_tc(const float* w_hi, const float* w_lo, const float* xi_hi, con
                    int kb_per_group, void* stream);
 
 /*
- * In-kernel argmax finish (srpb_conventional_tc16, srpb_interp_tc16,
- * srpb_interp_tc16_onthefly): with argmax_out [F] int32 and done_counter (one
- * unsigned int) non-NULL, the kernel's last CTA decodes keys into argmax_out
- * (as srpb_keys_to_index) and resets keys to 0 and *done_counter to 0, so a
- * caller that keeps keys and the counter zero-initialised between calls needs
- * neither srpb_argmax_keys_reset nor srpb_keys_to_index.  Calls sharing keys /
- * counter buffers must be stream-ordered.
+ * Dynamic scheduling and in-kernel argmax finish (srpb_conventional_tc16,
+ * srpb_interp_tc16, srpb_interp_tc16_onthefly): done_counter points to two
+ * zero-initialised unsigned ints -- [0] CTAs finished, [1] the work-item
+ * cursor from which CTAs (pairs) take their next tile once their first is
+ * done.  The kernel's last CTA resets both to 0; with argmax_out [F] int32
+ * also non-NULL it first decodes keys into argmax_out (as
+ * srpb_keys_to_index) and resets keys to 0, so a caller that keeps keys and
+ * the counters zero-initialised between calls needs neither
+ * srpb_argmax_keys_reset nor srpb_keys_to_index.  done_counter NULL: static
+ * round-robin tiles.  Calls sharing keys / counter buffers must be
+ * stream-ordered.
  */
 
 /*

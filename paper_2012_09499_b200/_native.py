@@ -85,7 +85,8 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or _LIB_PATH
+    # SRPB_LIB: an alternative build of the same ABI (tuning experiments)
+    path = path or os.environ.get("SRPB_LIB") or _LIB_PATH
     if not os.path.exists(path):
         raise ImportError(
             f"libsrpb.so not found at {path}; build it with `make` or "

@@ -73,11 +73,19 @@ constexpr int kABytes = kTcM * 128;  // one of A_hi / A_lo per stage
 
 enum : int { kAFromTma = 0, kAPhase = 1, kASinc = 2 };
 
+#ifndef SRPB_K4_STAGES
+#define SRPB_K4_STAGES 4
+#endif
+
 template <int kAMode, bool kPair, bool kF16>
 struct TcCfg {
-  // smem stages: K4 pairs fit 4 x (32 KB A + N/2 rows of B hi/lo); K2 is
-  // bounded by its A stages in TMEM (2N + 64 S <= 512)
-  static constexpr int kStages = (kAMode == kAFromTma && kPair) ? 4 : 3;
+  // smem stages: K4 pairs take 4 x (32 KB A + N/2 rows of B hi/lo) plus the
+  // 16 KB epilogue staging (227 KB total); K2 is bounded by its A stages in
+  // TMEM (2N + 64 S <= 512)
+  static constexpr int kStages = (kAMode == kAFromTma && kPair) ? SRPB_K4_STAGES : 3;
+  // K4 pairs: maps leave through shared memory (TMA store) and the argmax
+  // reads the staged tile transposed
+  static constexpr bool kEpiStage = kAMode == kAFromTma && kPair;
   static constexpr bool kASmem = kAMode == kAFromTma;
   static constexpr int kKbElems = kF16 ? kTcKBlock16 : kTcKBlock;  // elements per K block
 };
@@ -105,6 +113,9 @@ struct TcParams {
   int n_piece0;       // frames of a split item's first piece (second: N - n_piece0)
   int total_items;    // full_items + 2 * (num_items - full_items)
   int num_kb;         // K blocks of 32 per tile
+  int maps_tma;       // staged epilogue: maps stored by TMA (J % 4 == 0), else st.global
+  int dbg;            // experiments only (SRPB_TC_DBG): 1 = A rows mod 2048
+  int b_box;          // rows per B TMA box: this CTA's full B buffer (N, or N/2 per pair)
   int kb_per_group;   // TMEM drain period (K blocks)
   int groups_per_tile;
   float scale;
@@ -113,6 +124,8 @@ struct TcParams {
   // optional in-kernel argmax finish: the last CTA decodes keys -> argmax_out
   // and resets keys and the counter for the next call
   int32_t* argmax_out;
+  // done[0]: CTAs finished; done[1]: dynamic item cursor (both reset to 0 by
+  // the last CTA).  NULL: static round-robin items, no finish.
   unsigned int* done;
   // K2 phase generation
   const int32_t* tau_i;
@@ -128,12 +141,16 @@ struct TcParams {
   int P;
 };
 
+constexpr int kItemRing = 8;  // work-item ids in flight between the roles
+
 struct TcSmem {
   uint64_t full[kTcMaxStages];
   uint64_t empty[kTcMaxStages];
   uint64_t acc_full[2];
   uint64_t acc_empty[2];
-  unsigned long long tile_keys[4 * kTcMaxN];  // per-quarter, per-frame tile argmax
+  uint64_t item_full[kItemRing];   // ring slot holds the next item id (each CTA)
+  uint64_t item_empty[kItemRing];  // every consumer is done with the slot (leader)
+  int item_ring[kItemRing];
   uint32_t tmem_base;
 };
 
@@ -141,8 +158,17 @@ struct TcSmem {
 __host__ __device__ inline size_t tc_stage_bytes(int N, bool a_in_smem, bool pair) {
   return (a_in_smem ? 2 * kABytes : 0) + 2 * size_t(pair ? N / 2 : N) * 128;
 }
-__host__ __device__ inline size_t tc_smem_bytes(int N, bool a_in_smem, bool pair, int stages) {
-  return 1024 /*align slack*/ + stages * tc_stage_bytes(N, a_in_smem, pair) + sizeof(TcSmem);
+// staged epilogue (K4 pairs): per epilogue warp two 2 KB buffers of 16
+// frames x 32 candidates (fp32, TMA 128-byte swizzle)
+constexpr int kEpiChunk = 8;  // frames per staged chunk (one 1 KB swizzle atom)
+constexpr int kEpiStageBytes = kEpiChunk * 128;
+constexpr int kEpiStageTotal = kEpiWarps * 2 * kEpiStageBytes;
+// other kernels: per-quarter, per-frame tile argmax keys [4][kTcMaxN]
+constexpr int kTileKeysBytes = 4 * kTcMaxN * 8;
+__host__ __device__ inline size_t tc_smem_bytes(int N, bool a_in_smem, bool pair, int stages,
+                                                bool epi_stage = false) {
+  return 1024 /*align slack*/ + stages * tc_stage_bytes(N, a_in_smem, pair) +
+         (epi_stage ? kEpiStageTotal : kTileKeysBytes) + sizeof(TcSmem);
 }
 // TMEM columns: accumulators [0, 2N); K2's A stages (hi 32 + lo 32 columns
 // each) from column 2N: 2N + 64 * 3 <= 512 for N <= 160.
@@ -276,7 +302,8 @@ __device__ __forceinline__ void tc_write_cols(const TcParams& p, unsigned long l
   }
 }
 
-__device__ __forceinline__ void tc_write_tile(const TcParams& p, TcSmem* bar, int m0, int n0,
+__device__ __forceinline__ void tc_write_tile(const TcParams& p, unsigned long long* tile_keys,
+                                              int m0, int n0,
                                               int nc, int quarter, int half, int lane,
                                               float (&tot)[kTcMaxN / 2]) {
   const int J = p.J;
@@ -287,7 +314,7 @@ __device__ __forceinline__ void tc_write_tile(const TcParams& p, TcSmem* bar, in
   const int nv = max(0, min(ncols, p.F - (n0 + cbase)));  // columns with f < F
   const int lim = j < J ? nv : 0;
   float* ptr = p.maps ? p.maps + (static_cast<size_t>(n0 + cbase) * J + j) : nullptr;
-  unsigned long long* tk = bar->tile_keys;  // [4 quarters][kTcMaxN columns]
+  unsigned long long* tk = tile_keys;  // [4 quarters][kTcMaxN columns]
   TCP_DECL(w_loop);
   TCP_DECL(w_flush);
   { TCP_T0();
@@ -318,6 +345,140 @@ __device__ __forceinline__ void tc_write_tile(const TcParams& p, TcSmem* bar, in
   if (threadIdx.x == kEpiWarp0 * 32) {
     TCP_FLUSH(12, w_loop);
     TCP_FLUSH(13, w_flush);
+  }
+}
+
+// Staged epilogue (K4 pairs).  Per 8-frame chunk the warp writes its 32 rows
+// x 8 frames into a 1 KB shared buffer in the TMA 128-byte-swizzled layout
+// (frame-major: one 128-byte line per frame = the warp's 32 candidates) and
+// one lane stores it with a TMA bulk tensor store (no per-column st.global
+// from the LSU).  The same buffer serves the argmax transposed: lane L reads
+// frame L % 8's candidates [8 (L / 8), +8) with two conflict-free 16-byte
+// loads, keeps the best (value, lowest j) key, merges across the four lanes
+// of its frame (two shuffles) and pushes it with one global atomicMax.  Two
+// buffers per warp alternate; a buffer is rewritten only after the store
+// issued from it two chunks earlier has finished reading it.
+__device__ __forceinline__ void tc_write_tile_staged(const TcParams& p, const CUtensorMap* tm_maps,
+                                                     uint32_t sbase, int& chunk_seq, int m0, int n0,
+                                                     int nc, int quarter, int half, int lane,
+                                                     float (&tot)[kTcMaxN / 2]) {
+  const int J = p.J;
+  const uint32_t jbase = static_cast<uint32_t>(m0 + 32 * quarter);
+  const int cbase = half * (nc / 2);
+  const int ncols = nc / 2;
+  const int f_base = n0 + cbase;
+  const int j = static_cast<int>(jbase) + lane;
+  const int nv = max(0, min(ncols, p.F - f_base));  // columns with f < F
+  TCP_DECL(w_loop);
+  TCP_DECL(w_wait);
+  TCP_DECL(w_sts);
+  TCP_DECL(w_am);
+  { TCP_T0();
+  if (p.maps && !p.maps_tma) {  // J % 4 != 0: no TMA map for the maps; direct stores
+    float* ptr = p.maps + (static_cast<size_t>(f_base) * J + j);
+    const int lim = j < J ? nv : 0;
+#pragma unroll
+    for (int i = 0; i < kTcMaxN / 2; ++i) {
+      st_cs_pred(ptr, tot[i] * p.scale, i < lim);
+      ptr += J;
+    }
+  }
+  // swizzled slot of (frame row r, this lane's candidate) in an 8 x 128 B atom;
+  // rows past J are staged as -inf (the TMA store clips them; the argmax
+  // never picks them)
+  const uint32_t lane_off = static_cast<uint32_t>(lane & 3) * 4u;
+  const int lane_chunk = lane >> 2;
+  uint32_t slot[kEpiChunk];
+#pragma unroll
+  for (int r = 0; r < kEpiChunk; ++r)
+    slot[r] = static_cast<uint32_t>(r) * 128u + (static_cast<uint32_t>(lane_chunk ^ r) << 4) +
+              lane_off;
+  const float scale = p.scale;
+  const bool row_ok = j < J;
+  // argmax over a 16-frame super-chunk (both buffers): lane -> frame
+  // u16 = lane % 16 (buffer u16 / 8, row u16 % 8), candidates [16 hh, +16)
+  const int u16 = lane & 15;
+  const int hh = lane >> 4;
+  const int ur = u16 & 7;
+  uint32_t rd[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    rd[k] = static_cast<uint32_t>(u16 >> 3) * kEpiStageBytes + static_cast<uint32_t>(ur) * 128u +
+            (static_cast<uint32_t>((4 * hh + k) ^ ur) << 4);
+#pragma unroll
+  for (int cc = 0; cc < (kTcMaxN / 2) / 16; ++cc) {
+    if (16 * cc < ncols) {  // uniform (ncols is a multiple of 16)
+      { TCP_T0();
+      if (chunk_seq > 0) {  // both buffers' previous stores have read them
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+      }
+      TCP_ACC(w_wait); }
+      chunk_seq = 1;
+      { TCP_T0();
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int r = 0; r < kEpiChunk; ++r) {
+          const float v = row_ok ? tot[16 * cc + 8 * b + r] * scale : -INFINITY;
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(sbase + b * kEpiStageBytes + slot[r]),
+                       "f"(v)
+                       : "memory");
+        }
+      if (p.maps && p.maps_tma) fence_proxy_async_smem();  // STS -> visible to the TMA engine
+      __syncwarp();
+      if (lane == 0 && p.maps && p.maps_tma) {
+        tma_store_2d(tm_maps, sbase, static_cast<int>(jbase), f_base + 16 * cc);
+        tma_store_2d(tm_maps, sbase + kEpiStageBytes, static_cast<int>(jbase),
+                     f_base + 16 * cc + 8);
+        bulk_commit();
+      }
+      TCP_ACC(w_sts); }
+      TCP_T0();
+      if (p.keys) {
+        const int f_col = 16 * cc + u16;
+        float vv[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(vv[4 * k]), "=f"(vv[4 * k + 1]), "=f"(vv[4 * k + 2]),
+                         "=f"(vv[4 * k + 3])
+                       : "r"(sbase + rd[k])
+                       : "memory");
+        // tree max with lowest-index ties: at each level keep the left
+        // (lower j) element unless the right one is strictly greater (NaN
+        // never selected; -inf marks rows past J)
+        int id[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) id[e] = e;
+#pragma unroll
+        for (int w = 1; w < 16; w <<= 1)
+#pragma unroll
+          for (int e = 0; e < 16; e += 2 * w)
+            if (vv[e + w] > vv[e]) {
+              vv[e] = vv[e + w];
+              id[e] = id[e + w];
+            }
+        unsigned long long best =
+            (f_col < nv && vv[0] > -INFINITY)
+                ? (static_cast<unsigned long long>(orderable_bits(vv[0])) << 32) |
+                      static_cast<unsigned long long>(0xFFFFFFFFu - (jbase + 16 * hh + id[0]))
+                : 0ull;
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, 16);
+        best = other > best ? other : best;
+        if (hh == 0 && best != 0ull) atomicMax(p.keys + f_base + f_col, best);
+      }
+      TCP_ACC(w_am);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kTcMaxN / 2; ++i) tot[i] = 0.0f;
+  TCP_ACC(w_loop); }
+  if (threadIdx.x == kEpiWarp0 * 32) {
+    TCP_FLUSH(12, w_loop);
+    TCP_FLUSH(14, w_wait);
+    TCP_FLUSH(13, w_sts);
+    TCP_FLUSH(8, w_am);
   }
 }
 
@@ -479,7 +640,7 @@ template <int kAMode, bool kPair, bool kF16>
 __global__ void __launch_bounds__(kTcThreads, 1)
 srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
               const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
-              const TcParams p) {
+              const __grid_constant__ CUtensorMap tmMaps, const TcParams p) {
   using Cfg = TcCfg<kAMode, kPair, kF16>;
   constexpr int S = Cfg::kStages;
   constexpr bool kASmem = Cfg::kASmem;
@@ -495,7 +656,11 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   // address space visible to the compiler: STS/LDS, not generic accesses)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const size_t stage_bytes = tc_stage_bytes(p.N, kASmem, kPair);
-  TcSmem* bar = reinterpret_cast<TcSmem*>(smem + S * stage_bytes);
+  // [stages][epilogue staging (K4 pairs) | tile argmax keys][barriers]
+  uint8_t* epi_stage = smem + S * stage_bytes;  // 1024-aligned
+  unsigned long long* tile_keys = reinterpret_cast<unsigned long long*>(epi_stage);
+  TcSmem* bar = reinterpret_cast<TcSmem*>(epi_stage +
+                                          (Cfg::kEpiStage ? kEpiStageTotal : kTileKeysBytes));
   // kASinc: per pair (end column, column of lag 0), after the barriers
   int2* pair_cols = reinterpret_cast<int2*>(bar + 1);
   if (kAMode == kASinc)
@@ -507,21 +672,25 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   const int rank = kPair ? static_cast<int>(cluster_ctarank()) : 0;
   const bool leader = rank == 0;
 
-  // Work items: (frame tile, candidate tile of 128 x kCta rows); CTA (pair) c
-  // takes items c, c + #CTAs(pairs), ...; in a pair, CTA `rank` owns rows
-  // [128 rank, 128 rank + 128) of the 256-row tile.
+  // Work items: (frame tile, candidate tile of 128 x kCta rows); in a pair,
+  // CTA `rank` owns rows [128 rank, 128 rank + 128) of the 256-row tile.
+  // Scheduling is dynamic: CTA (pair) c starts with item c, then takes the
+  // next id from a global cursor (done[1]) whenever its producer is ready, so
+  // faster SMs take more items and the exit spread shrinks to ~one item.  The
+  // leader's producer fetches ids into a shared ring (both CTAs of a pair);
+  // the MMA issuer and epilogue warps read the same sequence and release
+  // each slot when done with the item.  Items are computed identically
+  // wherever they run, so results do not depend on the schedule.
   // The last partial wave's items are split into two frame pieces (n_piece0
   // and N - n_piece0 frames) so the wave's work spreads over more CTAs; every
   // output element accumulates over K in the same order whatever its item's
   // width, so maps are bitwise independent of the split.
   const int cid = static_cast<int>(blockIdx.x) / kCta;
   const int ncl = static_cast<int>(gridDim.x) / kCta;
-  const int my_tiles = p.total_items > cid ? (p.total_items - 1 - cid) / ncl + 1 : 0;
   struct Item {
     int m0, n0, nc;  // candidate row base (this CTA), frame base, frames
   };
-  auto item = [&](int it) {
-    const int g = cid + it * ncl;
+  auto item_of = [&](int g) {
     int b = g, piece = -1;
     if (g >= p.full_items) {
       b = p.full_items + ((g - p.full_items) >> 1);
@@ -537,6 +706,45 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       r.nc = p.N - p.n_piece0;
     }
     return r;
+  };
+  unsigned int* const cursor = p.done ? p.done + 1 : nullptr;
+  // item id of the it-th item of this CTA (pair): waits for the ring slot
+  // (-1 = no more items)
+  auto item_id = [&](int it) -> int {
+    const int slot = it % kItemRing;
+    if (kPair && !leader)
+      mbar_wait_acq_cluster(&bar->item_full[slot], (it / kItemRing) & 1);
+    else
+      mbar_wait(&bar->item_full[slot], (it / kItemRing) & 1);
+    return *reinterpret_cast<volatile int*>(&bar->item_ring[slot]);
+  };
+  // a consumer warp is done with its it-th item (one arrive per warp)
+  auto item_release = [&](int it) {
+    if (lane == 0) {
+      const int slot = it % kItemRing;
+      if (kPair && !leader)
+        mbar_arrive_cluster_relaxed(mapa(&bar->item_empty[slot], 0));
+      else
+        mbar_arrive(&bar->item_empty[slot]);
+    }
+  };
+  // leader producer: publish the it-th item id to the ring of every CTA
+  auto item_fetch = [&](int it) -> int {
+    int g = 0;
+    if (lane == 0) {
+      const int slot = it % kItemRing;
+      if (it >= kItemRing) mbar_wait(&bar->item_empty[slot], ((it / kItemRing) - 1) & 1);
+      g = it == 0 ? cid
+                  : (cursor ? ncl + static_cast<int>(atomicAdd(cursor, 1u)) : cid + it * ncl);
+      if (g >= p.total_items) g = -1;
+      bar->item_ring[slot] = g;
+      if (kPair) {
+        st_shared_cluster_u32(mapa(&bar->item_ring[slot], 1), static_cast<uint32_t>(g));
+        mbar_arrive_cluster(mapa(&bar->item_full[slot], 1));
+      }
+      mbar_arrive(&bar->item_full[slot]);
+    }
+    return __shfl_sync(0xffffffffu, g, 0);
   };
 
   const size_t a_bytes = kASmem ? 2 * kABytes : 0;
@@ -572,7 +780,14 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       mbar_init(&bar->acc_full[b], 1);
       mbar_init(&bar->acc_empty[b], kCta * kEpiWarps);
     }
-    for (int c = 0; c < 4 * kTcMaxN; ++c) bar->tile_keys[c] = 0ull;
+    // item ring: the leader producer fills every CTA's slot; consumers are the
+    // MMA issuer, all epilogue warps and the peer's producer
+    for (int r = 0; r < kItemRing; ++r) {
+      mbar_init(&bar->item_full[r], 1);
+      mbar_init(&bar->item_empty[r], 1 + kCta * kEpiWarps + (kCta - 1));
+    }
+    if (!Cfg::kEpiStage)
+      for (int c = 0; c < 4 * kTcMaxN; ++c) tile_keys[c] = 0ull;
     fence_mbar_init();
   }
   tc_fence_before();
@@ -597,13 +812,20 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     TCP_DECL(w_empty);
     TCP_DECL(t_all);
     { TCP_T0();
-    for (int it = 0; it < my_tiles; ++it) {
-      const Item t = item(it);
-      const int m0 = t.m0;
+    for (int it = 0;; ++it) {
+      const int gid = leader ? item_fetch(it) : item_id(it);
+      if (gid < 0) break;
+      const Item t = item_of(gid);
+      if (!leader) item_release(it);
+      const int m0 = (p.dbg & 1) ? t.m0 % 2048 : t.m0;
       const int rows = kPair ? t.nc / 2 : t.nc;    // this CTA's B rows (multiple of 16)
       const int nb = t.n0 + rank * rows;
+      // one box per B buffer: b_box = the buffer's rows, so a narrower
+      // (split) item loads unused tail rows -- never past the buffer
+      const int nbox = (rows + p.b_box - 1) / p.b_box;
       const uint32_t tx = static_cast<uint32_t>(kCta) *
-                          (2 * static_cast<uint32_t>(rows) * 128 + (kASmem ? 2 * kABytes : 0));
+                          (((p.dbg & 4) ? 1 : 2) * static_cast<uint32_t>(nbox * p.b_box) * 128 +
+                           (kASmem ? ((p.dbg & 2) ? 1 : 2) * kABytes : 0));
       for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
         const int s = kg % S;
         { TCP_T0();
@@ -614,20 +836,20 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
           if (kPair) {
             // leader arms the pair's byte count, the peer arrives remotely
             if (leader)
-              mbar_expect_tx(&bar->full[s], tx);
+              mbar_expect_tx(&bar->full[s], (p.dbg & 256) ? 0u : tx);
             else
               mbar_arrive_cluster_relaxed(fb);
-            for (int r = 0; r < rows; r += 16) {  // 16-row boxes: any item width
+            for (int r = 0; r < rows && !(p.dbg & 256); r += p.b_box) {
               tma_load_2d_pair(b_hi(s) + r * 128, &tmB_hi, fb, kb * KBE, nb + r);
-              tma_load_2d_pair(b_lo(s) + r * 128, &tmB_lo, fb, kb * KBE, nb + r);
+              if (!(p.dbg & 4)) tma_load_2d_pair(b_lo(s) + r * 128, &tmB_lo, fb, kb * KBE, nb + r);
             }
-            if (kASmem) {
+            if (kASmem && !(p.dbg & 256)) {
               tma_load_2d_pair(a_hi(s), &tmA_hi, fb, kb * KBE, m0);
-              tma_load_2d_pair(a_lo(s), &tmA_lo, fb, kb * KBE, m0);
+              if (!(p.dbg & 2)) tma_load_2d_pair(a_lo(s), &tmA_lo, fb, kb * KBE, m0);
             }
           } else {
             mbar_expect_tx(&bar->full[s], tx);
-            for (int r = 0; r < rows; r += 16) {
+            for (int r = 0; r < rows; r += p.b_box) {
               tma_load_2d(b_hi(s) + r * 128, &tmB_hi, &bar->full[s], kb * KBE, nb + r);
               tma_load_2d(b_lo(s) + r * 128, &tmB_lo, &bar->full[s], kb * KBE, nb + r);
             }
@@ -662,8 +884,11 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       TCP_DECL(w_acc);
       TCP_DECL(t_all);
       { TCP_T0();
-      for (int it = 0; it < my_tiles; ++it) {
-        const int nc = item(it).nc;
+      for (int it = 0;; ++it) {
+        const int gid = item_id(it);
+        if (gid < 0) break;
+        const int nc = item_of(gid).nc;
+        item_release(it);
         const uint32_t idesc = kF16 ? idesc_f16(kTcM * kCta, nc) : idesc_tf32(kTcM * kCta, nc);
         for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
           const int s = kg % S;
@@ -692,9 +917,11 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
                 const uint32_t o = 2 * ks;      // in 16-byte units
                 const uint32_t acc0 = (in_group > 0 || ks > 0) ? 1u : 0u;
                 if constexpr (kPair && kF16) {
-                  mma_f16_pair(d, al + o, bh + o, idesc, acc0);
-                  mma_f16_pair(d, ah + o, bl + o, idesc, 1u);
-                  mma_f16_pair(d, ah + o, bh + o, idesc, 1u);
+                  if (!(p.dbg & 8)) {
+                    mma_f16_pair(d, al + o, bh + o, idesc, acc0);
+                    mma_f16_pair(d, ah + o, bl + o, idesc, 1u);
+                  }
+                  mma_f16_pair(d, ah + o, bh + o, idesc, (p.dbg & 8) ? acc0 : 1u);
                 } else if constexpr (kPair) {
                   mma_tf32_pair(d, al + o, bh + o, idesc, acc0);
                   mma_tf32_pair(d, ah + o, bl + o, idesc, 1u);
@@ -763,7 +990,6 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     float tot[kTcMaxN / 2];
 #pragma unroll
     for (int i = 0; i < kTcMaxN / 2; ++i) tot[i] = 0.0f;
-    const int total_groups = my_tiles * p.groups_per_tile;
     int drained = 0;  // next global group to fold
     // incremental position of group `drained`: its tile, index in the tile,
     // and the global K block index of its last block (no divisions)
@@ -783,8 +1009,9 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     auto finish_group = [&](const Item& t) {
       if (d_gl == p.groups_per_tile - 1) {
         TCP_T0();
-        tc_write_tile(p, bar, t.m0, t.n0, t.nc, quarter, half, lane, tot);
+        tc_write_tile(p, tile_keys, t.m0, t.n0, t.nc, quarter, half, lane, tot);
         TCP_ACC(c_write);
+        item_release(d_it);
         ++d_it;
         d_gl = 0;
         d_last_kg = d_it * p.num_kb + min(p.kb_per_group, p.num_kb) - 1;
@@ -795,7 +1022,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       ++drained;
     };
     auto fold_step = [&]() {
-      const Item t = item(d_it);
+      const Item t = item_of(item_id(d_it));
       TCP_T0();
       const int b = drained & 1;
       if (d_chunk < 0) {
@@ -828,15 +1055,22 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
         TCP_ACC(c_drain);
       }
     };
-    auto fold_next = [&]() {
-      const Item t = item(d_it);
+    const uint32_t epi_sbase =
+        smem_u32(epi_stage) + static_cast<uint32_t>(e) * 2u * kEpiStageBytes;
+    int chunk_seq = 0;  // staged chunks written by this warp (buffer parity)
+    auto fold_next = [&](const Item& t) {
       { TCP_T0();
       tc_drain(p, bar, !leader, acc_empty_addr0, tmem, drained, t.nc, quarter, half, tot);
       TCP_ACC(c_drain); }
       if (d_gl == p.groups_per_tile - 1) {
         TCP_T0();
-        tc_write_tile(p, bar, t.m0, t.n0, t.nc, quarter, half, lane, tot);
+        if constexpr (Cfg::kEpiStage)
+          tc_write_tile_staged(p, &tmMaps, epi_sbase, chunk_seq, t.m0, t.n0, t.nc, quarter,
+                               half, lane, tot);
+        else
+          tc_write_tile(p, tile_keys, t.m0, t.n0, t.nc, quarter, half, lane, tot);
         TCP_ACC(c_write);
+        item_release(d_it);
         ++d_it;
         d_gl = 0;
         d_last_kg = d_it * p.num_kb + min(p.kb_per_group, p.num_kb) - 1;
@@ -855,8 +1089,12 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       using Gen = typename std::conditional<kAMode == kASinc, SincGen, PhaseGen<kF16>>::type;
       Gen gen;
       int kg = 0, s = 0, ph = 0;  // stage ring position
-      for (int it = 0; it < my_tiles; ++it) {
-        const int j = item(it).m0 + r;
+      int n_items = 0;            // items seen so far (the fold trails them)
+      for (int it = 0;; ++it) {
+        const int gid = item_id(it);
+        if (gid < 0) break;
+        n_items = it + 1;
+        const int j = item_of(gid).m0 + r;
         if constexpr (kAMode == kASinc)
           gen.start_tile(p, j, pair_cols);
         else
@@ -888,12 +1126,18 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
           }
           // fold one chunk of the oldest group whose last K block is at
           // least S behind
-          if (d_chunk >= 0 || (drained < total_groups && d_last_kg <= kg - S)) fold_step();
+          if (d_chunk >= 0 || (d_it < n_items && d_last_kg <= kg - S)) fold_step();
         }
       }
-      while (drained < total_groups) fold_step();
+      while (d_it < n_items) fold_step();
+    } else {
+      for (;;) {
+        const int gid = item_id(d_it);
+        if (gid < 0) break;
+        fold_next(item_of(gid));
+      }
+      if (Cfg::kEpiStage && lane == 0) bulk_wait_all();  // maps written, staging free
     }
-    while (drained < total_groups) fold_next();
     TCP_ACC(c_all); }
     if (warp == kEpiWarp0 && lane == 0) {
       TCP_FLUSH(5, c_gen_wait);
@@ -912,9 +1156,10 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   tc_fence_before();
   __syncthreads();
   if (kPair) cluster_sync();  // the pair leaves together (remote arrivals landed)
-  if (p.argmax_out) {
-    // last CTA: keys -> argmax (srpb_keys_to_index), keys and counter reset
-    // (srpb_argmax_keys_reset) for the next call -- two launches saved
+  if (p.done) {
+    // last CTA: keys -> argmax (srpb_keys_to_index), keys, counter and item
+    // cursor reset (srpb_argmax_keys_reset) for the next call -- two launches
+    // saved
     __shared__ unsigned int s_last;
     if (threadIdx.x == 0) {
       __threadfence();
@@ -923,12 +1168,17 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     __syncthreads();
     if (s_last) {
       __threadfence();
-      for (int f = threadIdx.x; f < p.F; f += blockDim.x) {
-        const unsigned long long k = __ldcg(p.keys + f);
-        p.argmax_out[f] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(k));
-        p.keys[f] = 0ull;
+      if (p.argmax_out) {
+        for (int f = threadIdx.x; f < p.F; f += blockDim.x) {
+          const unsigned long long k = __ldcg(p.keys + f);
+          p.argmax_out[f] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(k));
+          p.keys[f] = 0ull;
+        }
       }
-      if (threadIdx.x == 0) *p.done = 0u;
+      if (threadIdx.x == 0) {
+        p.done[0] = 0u;  // every CTA has fetched its last (sentinel) item id
+        p.done[1] = 0u;
+      }
     }
   }
 #ifdef SRPB_TC_PROFILE
@@ -1019,14 +1269,17 @@ void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16) {
   p.full_items = split ? p.num_items / units * units : p.num_items;
   p.total_items = p.full_items + 2 * (p.num_items - p.full_items);
   p.kb_per_group = max(f16 ? 2 : 4, kb_per_group);
+  p.b_box = getenv("SRPB_TC_BOX16") ? 16 : (pair ? p.N / 2 : p.N);
+  p.dbg = getenv("SRPB_TC_DBG") ? atoi(getenv("SRPB_TC_DBG")) : 0;
   p.groups_per_tile = (p.num_kb + p.kb_per_group - 1) / p.kb_per_group;
 }
 
 template <int kAMode, bool kPair, bool kF16>
 cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh,
-                      const CUtensorMap& bl, const TcParams& p, cudaStream_t stream) {
+                      const CUtensorMap& bl, const TcParams& p, cudaStream_t stream,
+                      const CUtensorMap* maps_map = nullptr) {
   using Cfg = TcCfg<kAMode, kPair, kF16>;
-  const size_t smem = tc_smem_bytes(p.N, Cfg::kASmem, kPair, Cfg::kStages) +
+  const size_t smem = tc_smem_bytes(p.N, Cfg::kASmem, kPair, Cfg::kStages, Cfg::kEpiStage) +
                       (kAMode == kASinc ? sizeof(int2) * static_cast<size_t>(p.P) : 0);
   auto kern = srp_tc_kernel<kAMode, kPair, kF16>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1046,7 +1299,8 @@ cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtens
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, p);
+  // kernels without a staged epilogue never touch the maps map
+  e = cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, maps_map ? *maps_map : bh, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -1080,9 +1334,8 @@ static cudaError_t conventional_tc(const void* psi_hi, const void* psi_lo, bool 
   p.inv_period = 1.0f / static_cast<float>(period);
   CUtensorMap bh, bl;
   const int cols = 2 * P * Kb;
-  const int brows = 16;  // B boxes of 16 rows (any item width)
-  cudaError_t e = make_map(&bh, psi_hi, F, cols, brows, f16);
-  if (e == cudaSuccess) e = make_map(&bl, psi_lo, F, cols, brows, f16);
+  cudaError_t e = make_map(&bh, psi_hi, F, cols, p.b_box, f16);
+  if (e == cudaSuccess) e = make_map(&bl, psi_lo, F, cols, p.b_box, f16);
   if (e != cudaSuccess) return e;
   if (f16)
     return pair ? launch_tc<kAPhase, true, true>(bh, bl, bh, bl, p, stream)
@@ -1113,16 +1366,30 @@ static cudaError_t interp_tc(const void* w_hi, const void* w_lo, const void* xi_
   p.argmax_out = argmax_out;
   p.done = done;
   CUtensorMap ah, al, bh, bl;
-  const int brows = 16;  // B boxes of 16 rows (any item width)
   cudaError_t e = make_map(&ah, w_hi, J, T_pad, kTcM, f16);
   if (e == cudaSuccess) e = make_map(&al, w_lo, J, T_pad, kTcM, f16);
-  if (e == cudaSuccess) e = make_map(&bh, xi_hi, F, T_pad, brows, f16);
-  if (e == cudaSuccess) e = make_map(&bl, xi_lo, F, T_pad, brows, f16);
+  if (e == cudaSuccess) e = make_map(&bh, xi_hi, F, T_pad, p.b_box, f16);
+  if (e == cudaSuccess) e = make_map(&bl, xi_lo, F, T_pad, p.b_box, f16);
   if (e != cudaSuccess) return e;
+  // staged epilogue (pairs): maps [F, J] fp32 leave by TMA in 32 x 16 boxes
+  // (needs a 16-byte row pitch: J % 4 == 0; otherwise direct stores)
+  CUtensorMap mm;
+  p.maps_tma = 0;
+  if (pair && maps && J % 4 == 0 && (reinterpret_cast<uintptr_t>(maps) & 15) == 0 &&
+      !(p.dbg & 512)) {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(J), static_cast<cuuint64_t>(F)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(J) * 4};
+    cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kEpiChunk)};
+    e = encode_tensor_map(&mm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, maps, dims, strides, box,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+    if (e != cudaSuccess) return e;
+    p.maps_tma = 1;
+  }
+  const CUtensorMap* mmp = p.maps_tma ? &mm : nullptr;
   if (f16)
-    return pair ? launch_tc<kAFromTma, true, true>(ah, al, bh, bl, p, stream)
+    return pair ? launch_tc<kAFromTma, true, true>(ah, al, bh, bl, p, stream, mmp)
                 : launch_tc<kAFromTma, false, true>(ah, al, bh, bl, p, stream);
-  return pair ? launch_tc<kAFromTma, true, false>(ah, al, bh, bl, p, stream)
+  return pair ? launch_tc<kAFromTma, true, false>(ah, al, bh, bl, p, stream, mmp)
               : launch_tc<kAFromTma, false, false>(ah, al, bh, bl, p, stream);
 }
 
@@ -1151,8 +1418,8 @@ cudaError_t launch_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, 
   p.reach = reach;
   p.P = P;
   CUtensorMap bh, bl;
-  cudaError_t e = make_map(&bh, xi_hi, F, T_pad, 16, true);
-  if (e == cudaSuccess) e = make_map(&bl, xi_lo, F, T_pad, 16, true);
+  cudaError_t e = make_map(&bh, xi_hi, F, T_pad, p.b_box, true);
+  if (e == cudaSuccess) e = make_map(&bl, xi_lo, F, T_pad, p.b_box, true);
   if (e != cudaSuccess) return e;
   return launch_tc<kASinc, false, true>(bh, bl, bh, bl, p, stream);
 }

@@ -232,15 +232,17 @@ class SrpPlan:
 
     # ---------------------------------------------------------------- helpers
     def _argmax_state(self, F):
-        """Persistent zeroed (keys [F], done counter) for the tensor-core
-        kernels' in-kernel argmax finish: the last CTA decodes the keys and
-        resets both, so no reset / decode launches are needed per call."""
+        """Persistent zeroed (keys [F], done counter + item cursor) for the
+        tensor-core kernels' dynamic item scheduling and in-kernel argmax
+        finish: the last CTA decodes the keys and resets all three, so no
+        reset / decode launches are needed per call."""
         st = getattr(self, "_am_state", None)
         if st is None:
             st = self._am_state = {}
         if F not in st:
+            # done counter [0] and the dynamic item cursor [1]
             st[F] = (torch.zeros(F, dtype=torch.int64, device=self.device),
-                     torch.zeros(1, dtype=torch.int32, device=self.device))
+                     torch.zeros(2, dtype=torch.int32, device=self.device))
         return st[F]
 
     def _keys(self, F):

@@ -27,8 +27,8 @@ import bench  # noqa: E402
 from paper_2012_09499_b200.plan import SrpPlan  # noqa: E402
 
 NAMES = {0: "mma_total", 1: "mma_wait_full", 2: "mma_wait_acc_empty", 3: "tma_wait_empty",
-         4: "tma_total", 5: "epi_gen_wait_empty", 6: "epi_gen", 7: "epi_drain", 9: "epi_write",
-         10: "epi_total", 11: "ctas", 12: "write_loop", 13: "write_flush", 14: "write_stores",
+         4: "tma_total", 5: "epi_gen_wait_empty", 6: "epi_gen", 7: "epi_drain", 8: "staged_argmax", 9: "epi_write",
+         10: "epi_total", 11: "ctas", 12: "write_loop", 13: "write_flush|staged_sts", 14: "write_stores|staged_wait",
          15: "write_argmax", 16: "cta_lifetime(all CTAs)", 17: "setup(all CTAs)",
          18: "teardown_wait(all CTAs)", 19: "cta_count"}
 
