@@ -812,11 +812,16 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     TCP_DECL(w_empty);
     TCP_DECL(t_all);
     { TCP_T0();
+    // the leader fetches item ids one ahead: the cursor's atomic latency hides
+    // behind the current item (measured: an L2 prefetch of the next item's W
+    // rows from here made K4 slower, 60 -> 80 us)
+    int gid_next = leader ? item_fetch(0) : 0;
     for (int it = 0;; ++it) {
-      const int gid = leader ? item_fetch(it) : item_id(it);
+      const int gid = leader ? gid_next : item_id(it);
       if (gid < 0) break;
       const Item t = item_of(gid);
       if (!leader) item_release(it);
+      if (leader) gid_next = item_fetch(it + 1);
       const int m0 = (p.dbg & 1) ? t.m0 % 2048 : t.m0;
       const int rows = kPair ? t.nc / 2 : t.nc;    // this CTA's B rows (multiple of 16)
       const int nb = t.n0 + rank * rows;
