@@ -188,6 +188,38 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
                               void* spec_scratch, void* stream);
 
 /*
+ * Tensor-core form of the same step (replaces spectral.cross_spectrum ->
+ * srp.build_gcc_lattice, spectral.py:218-285 + srp.py:201-247, like the
+ * entry above): the lattice twiddles do not depend on the pair, so all
+ * (frame, pair) rows form one GEMM  C[f P + p, c] = sum_k Re(psi e^{j w_k n T})
+ * over lag slots c = n + L, psi generated by PHAT on the fly (3xFP16,
+ * tcgen05).  Used for PHAT with the relative floor (speculative + fix-up) and
+ * the fp16 split output when Kb % 32 == 0, Kb >= 64 and
+ * srpb_lattice_tc_cols(L) <= 64; any other call behaves exactly like
+ * srpb_lattice_from_spectra.  Arguments as there, plus
+ *   tc_b_hi, tc_b_lo  [srpb_lattice_tc_cols(L), 2 Kb] fp16 from
+ *                     srpb_lattice_tc_twiddles (both NULL: SIMT path).
+ */
+int srpb_lattice_from_spectra_tc(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                                 const int32_t* pair_mp, int P, int weighting,
+                                 const double* floors, double abs_floor, const int32_t* clean,
+                                 const float* tw, int L, const int32_t* off, const int32_t* reach,
+                                 int T_pad, float* Xi, void* Xi_hi, void* Xi_lo, float split_scale,
+                                 double floor_rel, void* spec_scratch, const void* tc_b_hi,
+                                 const void* tc_b_lo, void* stream);
+
+/* Lag slots of the tensor-core lattice: 2L + 1 rounded up to 16. */
+int srpb_lattice_tc_cols(int L);
+
+/*
+ * Its B operand: row c (lag n = c - L, zero rows past 2L), K = 2 Kb
+ * interleaved (cos, -sin)(omega[k] n T) x 2^14, fp16 hi/lo split (fp64
+ * phases as srpb_lattice_twiddles).  b_hi, b_lo [srpb_lattice_tc_cols(L), 2 Kb].
+ */
+int srpb_lattice_tc_twiddles(const double* omega, int Kb, double sample_period, int L, void* b_hi,
+                             void* b_lo, void* stream);
+
+/*
  * Sinc interpolation table W[j, off[p] + n + reach[p]] = sinc(x[j,p] - n),
  * exact 1/0 at integer arguments (srp._sinc_kernel srp.py:250-261,
  * srp.precompute_sinc_table srp.py:287-317), x = tau / T split on the host in

@@ -40,6 +40,13 @@ _SIGNATURES = {
                                   c_void_p, c_double, c_void_p, c_void_p, c_int, c_void_p,
                                   c_void_p, c_int, c_void_p, c_void_p, c_void_p, ctypes.c_float,
                                   c_double, c_void_p, c_void_p],
+    "srpb_lattice_tc_cols": [c_int],
+    "srpb_lattice_tc_twiddles": [c_void_p, c_int, c_double, c_int, c_void_p, c_void_p, c_void_p],
+    "srpb_lattice_from_spectra_tc": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
+                                     c_int, c_void_p, c_double, c_void_p, c_void_p, c_int,
+                                     c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                                     ctypes.c_float, c_double, c_void_p, c_void_p, c_void_p,
+                                     c_void_p],
     "srpb_sinc_table": [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p,
                         c_void_p],
     "srpb_interp": [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],
@@ -123,7 +130,8 @@ def stream_handle(device=None):
 _LAUNCHING = {n for n in _SIGNATURES if n not in ("srpb_abi_version", "srpb_last_error")}
 # entry points that launch more than one kernel (floor/fill pass + psi pass;
 # speculative-floor lattice + its fix-up pass)
-_KERNELS_PER_CALL = {"srpb_gcc_phat": 2, "srpb_lattice_from_spectra": 2, "srpb_map_error": 2}
+_KERNELS_PER_CALL = {"srpb_gcc_phat": 2, "srpb_lattice_from_spectra": 2,
+                     "srpb_lattice_from_spectra_tc": 2, "srpb_map_error": 2}
 _launches = 0
 
 

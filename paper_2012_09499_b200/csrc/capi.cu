@@ -20,7 +20,10 @@ cudaError_t launch_lattice_from_spectra(const float*, int, int, int, const int32
                                         const int32_t*, int, int, const double*, double,
                                         const int32_t*, const float*, int, const int32_t*,
                                         const int32_t*, int, int, float*, void*, void*, float,
-                                        double, void*, cudaStream_t);
+                                        double, void*, cudaStream_t, const void*, const void*);
+int lattice_tc_n(int L);
+cudaError_t launch_lattice_tc_twiddles(const double*, int, double, int, void*, void*,
+                                       cudaStream_t);
 cudaError_t launch_conventional(const float*, int, int, int, int, const int32_t*, const float*,
                                 int, float*, unsigned long long*, cudaStream_t);
 cudaError_t launch_conventional_general(const float*, int, int, int, const double*,
@@ -99,7 +102,7 @@ static bool pow2_scale(float s) {
   return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
 }
 
-int srpb_abi_version(void) { return 10; }
+int srpb_abi_version(void) { return 11; }
 
 const char* srpb_last_error(void) { return g_err; }
 
@@ -213,13 +216,13 @@ int srpb_lattice(const float* Psi, int F, int P, int Kb, const float* tw, int L,
                 "srpb_lattice");
 }
 
-int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
-                              const int32_t* pair_mp, int P, int weighting, const double* floors,
-                              double abs_floor, const int32_t* clean, const float* tw, int L,
-                              const int32_t* off,
-                              const int32_t* reach, int T_pad, float* Xi, void* Xi_hi,
-                              void* Xi_lo, float split_scale, double floor_rel,
-                              void* spec_scratch, void* stream) {
+static int lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                                const int32_t* pair_mp, int P, int weighting,
+                                const double* floors, double abs_floor, const int32_t* clean,
+                                const float* tw, int L, const int32_t* off, const int32_t* reach,
+                                int T_pad, float* Xi, void* Xi_hi, void* Xi_lo, float split_scale,
+                                double floor_rel, void* spec_scratch, const void* tc_b_hi,
+                                const void* tc_b_lo, void* stream) {
   REQUIRE(F >= 0 && M >= 1 && P >= 1 && Kb >= 1 && L >= 0 && T_pad >= 1,
           "srpb_lattice_from_spectra: bad shape");
   REQUIRE(weighting == SRPB_WEIGHT_PHAT || weighting == SRPB_WEIGHT_IDENTITY,
@@ -239,8 +242,47 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
                                                   floors, abs_floor, clean, tw, L, off, reach,
                                                   2 * L + 1,
                                                   T_pad, Xi, Xi_hi, Xi_lo, split_scale, floor_rel,
-                                                  spec_scratch, S(stream)),
+                                                  spec_scratch, S(stream), tc_b_hi, tc_b_lo),
                 "srpb_lattice_from_spectra");
+}
+
+int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                              const int32_t* pair_mp, int P, int weighting, const double* floors,
+                              double abs_floor, const int32_t* clean, const float* tw, int L,
+                              const int32_t* off, const int32_t* reach, int T_pad, float* Xi,
+                              void* Xi_hi, void* Xi_lo, float split_scale, double floor_rel,
+                              void* spec_scratch, void* stream) {
+  return lattice_from_spectra(Y, F, M, Kb, pair_m, pair_mp, P, weighting, floors, abs_floor,
+                              clean, tw, L, off, reach, T_pad, Xi, Xi_hi, Xi_lo, split_scale,
+                              floor_rel, spec_scratch, nullptr, nullptr, stream);
+}
+
+int srpb_lattice_tc_cols(int L) { return L >= 0 ? srpb::lattice_tc_n(L) : -1; }
+
+int srpb_lattice_tc_twiddles(const double* omega, int Kb, double sample_period, int L, void* b_hi,
+                             void* b_lo, void* stream) {
+  REQUIRE(Kb >= 1 && L >= 0 && omega && b_hi && b_lo, "srpb_lattice_tc_twiddles: bad argument");
+  REQUIRE(sample_period > 0.0, "srpb_lattice_tc_twiddles: sample_period must be positive");
+  REQUIRE(((reinterpret_cast<uintptr_t>(b_hi) | reinterpret_cast<uintptr_t>(b_lo)) & 15) == 0,
+          "srpb_lattice_tc_twiddles: operands must be 16-byte aligned");
+  return status(srpb::launch_lattice_tc_twiddles(omega, Kb, sample_period, L, b_hi, b_lo,
+                                                 S(stream)),
+                "srpb_lattice_tc_twiddles");
+}
+
+int srpb_lattice_from_spectra_tc(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                                 const int32_t* pair_mp, int P, int weighting,
+                                 const double* floors, double abs_floor, const int32_t* clean,
+                                 const float* tw, int L, const int32_t* off, const int32_t* reach,
+                                 int T_pad, float* Xi, void* Xi_hi, void* Xi_lo, float split_scale,
+                                 double floor_rel, void* spec_scratch, const void* tc_b_hi,
+                                 const void* tc_b_lo, void* stream) {
+  REQUIRE(!tc_b_hi == !tc_b_lo, "srpb_lattice_from_spectra_tc: tc_b_hi and tc_b_lo go together");
+  REQUIRE(((reinterpret_cast<uintptr_t>(tc_b_hi) | reinterpret_cast<uintptr_t>(tc_b_lo)) & 15) == 0,
+          "srpb_lattice_from_spectra_tc: tensor-core twiddles must be 16-byte aligned");
+  return lattice_from_spectra(Y, F, M, Kb, pair_m, pair_mp, P, weighting, floors, abs_floor,
+                              clean, tw, L, off, reach, T_pad, Xi, Xi_hi, Xi_lo, split_scale,
+                              floor_rel, spec_scratch, tc_b_hi, tc_b_lo, stream);
 }
 
 int srpb_sinc_table(const int32_t* sx_i, const float* sx_f, int J, int P, const int32_t* off,

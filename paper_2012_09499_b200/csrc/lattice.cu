@@ -679,6 +679,538 @@ cudaError_t launch_lattice(const float* Psi, int F, int P, int Kb, const float* 
   return launch_lattice_args(a, false, max_Tp, stream);
 }
 
+// ---------------------------------------------------------------------------
+// K1b+K3 on the tensor cores (PHAT, speculative floor): one GEMM over all
+// (frame, pair) rows.  The lattice twiddles e^{j w_k n T} do not depend on
+// the pair, so with rows r = f P + p (the pair's PHAT cross-spectrum psi_r
+// generated on the fly) and lag slots c = n + L (n in [-L, L], L = max reach):
+//   C[r, c] = sum_k Re(psi_r[k]) cos(w_k n T) - Im(psi_r[k]) sin(w_k n T)
+//   Xi[f, off_p + reach_p + n] = 2 C[r, n + L],   |n| <= reach_p
+// A = psi rows (K = 2 Kb: Re, Im interleaved), B = [cos; -sin] rows per lag
+// slot (built once per plan), both 3xFP16 split (x 2^14, |psi| <= 1 and
+// |twiddle| <= 1), fp32 accumulation in TMEM.  Pairs with reach < L waste
+// the unused lag slots -- free on the tensor core.
+//
+// CTA = 128 rows; a cluster of two CTAs splits the bins (K) and CTA 1 folds
+// its partial accumulator and PHAT statistics into CTA 0 through distributed
+// shared memory (fixed order: deterministic).  Warps: 0 TMA producer (B),
+// 1 TMEM allocator + MMA issuer, 2..9 psi generators (16 rows each: lane =
+// bin, coalesced Y loads, fast PHAT = psi_warp<kPsiPhatSpec> arithmetic,
+// per-row stats for the fix-up pass); warps 4..7 (lane quarters 0..3) are the
+// epilogue.  Bounded by the PHAT generation (2 MUFU + ~20 ALU per psi), not
+// by the MMA (3 x 4 MMAs of 128 x N x 16 per 32-bin block).
+#ifdef SRPB_TC_PROFILE
+__device__ unsigned long long g_lt_prof[16];
+#define LTP_T(v) const long long v = clock64()
+#define LTP_ADD(i, v) atomicAdd(&g_lt_prof[i], static_cast<unsigned long long>(v))
+#else
+#define LTP_T(v)
+#define LTP_ADD(i, v)
+#endif
+constexpr int kLtRows = 128;
+constexpr int kLtGenWarps = 16;
+constexpr int kLtRW = kLtRows / kLtGenWarps;  // rows per generator warp (8)
+constexpr int kLtWarp0 = 2;  // first generator warp
+constexpr int kLtThreads = 32 * (kLtWarp0 + kLtGenWarps);
+constexpr int kLtStages = 4;
+constexpr int kLtMaxN = 64;
+constexpr float kLtScale = 16384.0f;  // 2^14 on both operands
+// TMEM accumulation drift: bin blocks go to fresh accumulators in groups of
+// 4 (48 MMA steps per chain, as K2 / K4), summed in order by the epilogue
+constexpr int kLtGroup = 4;
+__host__ __device__ inline int lt_tmem_cols(int nkb, int N) {
+  const int h = (nkb + 1) / 2;  // blocks of the larger CTA half
+  const int need = (h + kLtGroup - 1) / kLtGroup * N;
+  int c = 32;
+  while (c < need) c <<= 1;
+  return c;
+}
+
+struct LtSmem {
+  uint64_t full[kLtStages];
+  uint64_t empty[kLtStages];
+  uint64_t yfull[kLtStages];       // the stage's spectra tile landed
+  uint64_t acc_full;
+  uint32_t tmem_base;
+  int2 rows[kLtRows];              // (Y row of mic m, Y row of mic m') per tile row
+  float st_sum[2][kLtRows];        // per-row PHAT stats: [own, partner]
+  float st_min[2][kLtRows];
+  int st_bad[2][kLtRows];
+};
+
+// stage: A hi/lo (128 rows x 128 B), B hi/lo (N rows x 128 B), spectra tile
+// Y [nF frames][M mics][32 bins] complex64 (TMA, 3-D box)
+__host__ __device__ inline size_t lt_y_bytes(int nF, int M) { return size_t(nF) * M * 256; }
+__host__ __device__ inline size_t lt_stage_bytes(int N, int nF, int M) {
+  return (2 * 16384 + 2 * size_t(N) * 128 + lt_y_bytes(nF, M) + 1023) / 1024 * 1024;
+}
+__host__ __device__ inline size_t lt_smem_bytes(int N, int nF, int M, int S) {
+  return 1024 + S * lt_stage_bytes(N, nF, M) + 2 * size_t(kLtRows) * N * 4 /*own, partner C*/ +
+         sizeof(LtSmem);
+}
+// frames a 128-row tile spans
+inline int lt_frames(int P) { return (kLtRows - 1 + P - 1) / P + 1; }
+// stages that fit in 227 KB (0: the tile does not fit)
+inline int lt_stages(int N, int nF, int M) {
+  for (int S = kLtStages; S >= 2; --S)
+    if (lt_smem_bytes(N, nF, M, S) + 1024 <= 232448) return S;
+  return 0;
+}
+
+struct LtArgs {
+  const float2* Y;
+  int F, P, M, Kb, N, L, S, nF;
+  int dbg;  // experiments (SRPB_LT_DBG): 1 skip psi math, 2 skip MMAs, 4 skip output
+  const int32_t* pm;
+  const int32_t* pmp;
+  const int32_t* off;
+  const int32_t* reach;
+  int T_pad;
+  float* Xi;
+  __half* Xi_hi;
+  __half* Xi_lo;
+  float split_scale;
+  float* spec_sum;
+  float* spec_min;
+  int* spec_bad;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLtThreads, 1)
+lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
+                  const __grid_constant__ CUtensorMap tmB_lo,
+                  const __grid_constant__ CUtensorMap tmY, const LtArgs a) {
+  using namespace umma;
+  LTP_T(t_entry);
+  extern __shared__ __align__(1024) uint8_t lt_raw[];
+  uint8_t* smem = lt_raw + ((1024u - (smem_u32(lt_raw) & 1023u)) & 1023u);
+  const int N = a.N;
+  const int S = a.S;
+  const size_t stage_bytes = lt_stage_bytes(N, a.nF, a.M);
+  float* s_part = reinterpret_cast<float*>(smem + S * stage_bytes);  // [N][128] from CTA 1
+  float* s_own = s_part + kLtRows * N;                                // [N][128] this CTA
+  LtSmem* sm = reinterpret_cast<LtSmem*>(s_own + kLtRows * N);
+  auto a_hi = [&](int s) { return smem + s * stage_bytes; };
+  auto a_lo = [&](int s) { return smem + s * stage_bytes + 16384; };
+  auto b_hi = [&](int s) { return smem + s * stage_bytes + 32768; };
+  auto b_lo = [&](int s) { return smem + s * stage_bytes + 32768 + N * 128; };
+  auto y_st = [&](int s) { return smem + s * stage_bytes + 32768 + 2 * N * 128; };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int tile = blockIdx.x >> 1;
+  const long long R0 = static_cast<long long>(tile) * kLtRows;
+  const long long n_rows = static_cast<long long>(a.F) * a.P;
+  const int f_lo = static_cast<int>(R0 / a.P);  // first frame of the tile
+  // K split: rank 0 takes 32-bin blocks [0, h), rank 1 [h, nkb)
+  const int nkb = a.Kb / 32;
+  const int h = (nkb + 1) / 2;
+  const int kb0 = rank == 0 ? 0 : h, kb1 = rank == 0 ? h : nkb;
+  const int my_kb = kb1 - kb0;
+
+  for (int r = threadIdx.x; r < kLtRows; r += blockDim.x) {
+    const long long R = R0 + r;
+    // byte offsets of the row's two spectra in the stage's Y tile (rows past
+    // the end: tile row 0, never stored)
+    int2 v = make_int2(0, 0);
+    if (R < n_rows) {
+      const int f = static_cast<int>(R / a.P), p = static_cast<int>(R - static_cast<long long>(f) * a.P);
+      v = make_int2(((f - f_lo) * a.M + __ldg(a.pm + p)) * 256,
+                    ((f - f_lo) * a.M + __ldg(a.pmp + p)) * 256);
+    }
+    sm->rows[r] = v;
+  }
+  const int tcols = lt_tmem_cols(nkb, N);
+  if (warp == 1) tmem_alloc(&sm->tmem_base, tcols);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&sm->full[s], 1 + kLtGenWarps);
+      mbar_init(&sm->empty[s], 1);
+      mbar_init(&sm->yfull[s], 1);
+    }
+    mbar_init(&sm->acc_full, 1);
+    fence_mbar_init();
+    tma_prefetch(&tmB_hi);
+    tma_prefetch(&tmB_lo);
+    tma_prefetch(&tmY);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, sm->tmem_base, 0);
+  LTP_T(t_setup);
+#ifdef SRPB_TC_PROFILE
+  if (threadIdx.x == 0) {
+    LTP_ADD(0, t_setup - t_entry);
+    LTP_ADD(9, 1);
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    atomicMax(&g_lt_prof[10], ~gt);  // earliest start (complemented)
+    atomicMax(&g_lt_prof[12], gt);   // latest start
+  }
+#endif
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- B producer
+    for (int i = 0; i < my_kb; ++i) {
+      const int s = i % S;
+      mbar_wait(&sm->empty[s], ((i / S) & 1) ^ 1);
+      if (elect_one()) {
+        // spectra tile first: the generators wait on it
+        mbar_expect_tx(&sm->yfull[s], static_cast<uint32_t>(lt_y_bytes(a.nF, a.M)));
+        tma_load_3d(y_st(s), &tmY, &sm->yfull[s], (kb0 + i) * 64, 0, f_lo);
+        mbar_expect_tx(&sm->full[s], static_cast<uint32_t>(2 * N * 128));
+        tma_load_2d(b_hi(s), &tmB_hi, &sm->full[s], (kb0 + i) * 64, 0);
+        tma_load_2d(b_lo(s), &tmB_lo, &sm->full[s], (kb0 + i) * 64, 0);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ----------------------------------------------------------- MMA issuer
+    const uint32_t idesc = idesc_f16(kLtRows, N);
+    for (int i = 0; i < my_kb; ++i) {
+      const int s = i % S;
+      mbar_wait(&sm->full[s], (i / S) & 1);
+      tc_fence_after();
+      if (!(a.dbg & 2) && elect_one()) {
+        const uint64_t ah = sw128_kmajor_desc(smem_u32(a_hi(s)));
+        const uint64_t al = sw128_kmajor_desc(smem_u32(a_lo(s)));
+        const uint64_t bh = sw128_kmajor_desc(smem_u32(b_hi(s)));
+        const uint64_t bl = sw128_kmajor_desc(smem_u32(b_lo(s)));
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint32_t o = 2 * ks;  // 32 bytes of K per MMA
+          const uint32_t d = tmem + static_cast<uint32_t>((i / kLtGroup) * N);
+          mma_f16(d, al + o, bh + o, idesc, (i % kLtGroup > 0 || ks > 0) ? 1u : 0u);
+          mma_f16(d, ah + o, bl + o, idesc, 1u);
+          mma_f16(d, ah + o, bh + o, idesc, 1u);
+        }
+        mma_commit(&sm->empty[s]);
+        if (i == my_kb - 1) mma_commit(&sm->acc_full);
+      } else if ((a.dbg & 2) && elect_one()) {
+        mbar_arrive(&sm->empty[s]);
+        if (i == my_kb - 1) mbar_arrive(&sm->acc_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    // --------------------------------------------------------- psi generator
+    const int g = warp - kLtWarp0;  // rows kLtRW g .. kLtRW g + kLtRW - 1
+    // per-row PHAT statistics (PhatSpecStats over this CTA's bins): sum and
+    // min of |raw|^2 = pa pb over bins with both powers nonzero, and the
+    // extreme nonzero powers (range test at the end)
+    float ssum[kLtRW], smin[kLtRW], pmin[kLtRW], pmax[kLtRW];
+#pragma unroll
+    for (int q = 0; q < kLtRW; ++q) {
+      ssum[q] = 0.0f;
+      smin[q] = pmin[q] = 3.0e38f;
+      pmax[q] = 0.0f;
+    }
+    // swizzled 16-byte chunk of this lane's (Re, Im) pair in row r: depends
+    // on r & 7 only (rows kLtRW g + q: r & 7 = q & 7)
+    uint32_t xo[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      xo[q] = (static_cast<uint32_t>((lane >> 2) ^ q) << 4) + static_cast<uint32_t>(lane & 3) * 4u;
+    const int2* ro = sm->rows + kLtRW * g;  // byte offsets of the two spectra rows in the Y tile
+#ifdef SRPB_TC_PROFILE
+    long long w_y = 0;
+#endif
+    for (int i = 0; i < my_kb; ++i) {
+      const int s = i % S;
+      // the producer loads a stage only after its previous A was consumed
+      LTP_T(t_w0);
+      mbar_wait(&sm->yfull[s], (i / S) & 1);
+#ifdef SRPB_TC_PROFILE
+      w_y += clock64() - t_w0;
+#endif
+      const uint8_t* yk = y_st(s) + lane * 8;
+      float2 ya[kLtRW], yb[kLtRW];
+#pragma unroll
+      for (int q = 0; q < kLtRW; ++q) {
+        const int2 o = ro[q];
+        ya[q] = *reinterpret_cast<const float2*>(yk + o.x);
+        yb[q] = *reinterpret_cast<const float2*>(yk + o.y);
+      }
+      uint8_t* ahs = a_hi(s) + kLtRW * 128 * g;
+      uint8_t* als = a_lo(s) + kLtRW * 128 * g;
+#pragma unroll
+      for (int q = 0; q < kLtRW; ++q) {
+        if (a.dbg & 1) continue;
+        const float pa = fmaf(ya[q].x, ya[q].x, ya[q].y * ya[q].y);
+        const float pb = fmaf(yb[q].x, yb[q].x, yb[q].y * yb[q].y);
+        const float qq = pa * pb;
+        const float mp = fminf(pa, pb);
+        const bool nz = mp != 0.0f;
+        ssum[q] += qq;
+        smin[q] = fminf(smin[q], nz ? qq : 3.0e38f);
+        pmin[q] = fminf(pmin[q], nz ? mp : 3.0e38f);
+        pmax[q] = fmaxf(pmax[q], fmaxf(pa, pb));
+        // 1/|raw| = rsqrt(pa pb): exact to fp32 rounding for powers in the
+        // fast range; frames outside it are redone by the fix-up pass
+        const float sc = rsqrt_approx_ftz(fmaxf(qq, 1e-37f)) * kLtScale;
+        const float re = fmaf(ya[q].x, yb[q].x, ya[q].y * yb[q].y) * sc;
+        const float im = fmaf(ya[q].y, yb[q].x, -(ya[q].x * yb[q].y)) * sc;
+        const __half2 hi = __floats2half2_rn(re, im);
+        const float2 hf = __half22float2(hi);
+        const __half2 lo = __floats2half2_rn(re - hf.x, im - hf.y);
+        *reinterpret_cast<__half2*>(ahs + q * 128 + xo[q & 7]) = hi;
+        *reinterpret_cast<__half2*>(als + q * 128 + xo[q & 7]) = lo;
+      }
+      fence_proxy_async_smem();  // generic-proxy writes -> visible to the MMA
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm->full[s]);
+    }
+    uint32_t sbad = 0;
+#pragma unroll
+    for (int q = 0; q < kLtRW; ++q)
+      sbad |= (pmin[q] <= 1e-15f || pmax[q] >= 1e15f ? 1u : 0u) << q;
+#ifdef SRPB_TC_PROFILE
+    if (lane == 0) { LTP_ADD(3, clock64() - t_setup); LTP_ADD(4, w_y); }
+#endif
+    // rows past the end contributed garbage stats: dropped at the store
+    // per-row stats over this CTA's bins: fixed-order warp reduction
+#pragma unroll
+    for (int q = 0; q < kLtRW; ++q) {
+      float sum = ssum[q], mn = smin[q];
+      int bad = (sbad >> q) & 1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+      }
+      if (lane == 0) {
+        sm->st_sum[0][kLtRW * g + q] = sum;
+        sm->st_min[0][kLtRW * g + q] = mn;
+        sm->st_bad[0][kLtRW * g + q] = bad;
+      }
+    }
+  }
+
+  // ---------------------------------------------------------------- epilogue
+  const bool epi = warp >= 4 && warp < 8;
+  const int quarter = warp & 3;
+  const int row = 32 * quarter + lane;  // TMEM lane = tile row
+  if (epi) {
+    LTP_T(t_e0);
+    mbar_wait(&sm->acc_full, 0);
+#ifdef SRPB_TC_PROFILE
+    if (lane == 0) { LTP_ADD(5, clock64() - t_e0); LTP_ADD(2, clock64() - t_setup); }
+#endif
+    tc_fence_after();
+    const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
+    const int groups = (my_kb + kLtGroup - 1) / kLtGroup;
+    // CTA 0 keeps its partial C in s_own, CTA 1 sends it to CTA 0's s_part
+    // (column-major [N][128]: conflict-free), 16 columns at a time
+    const uint32_t dst = rank == 1 ? mapa(s_part, 0) + static_cast<uint32_t>(row) * 4u
+                                   : smem_u32(s_own) + static_cast<uint32_t>(row) * 4u;
+    for (int c = 0; c < N; c += 16) {
+      float acc[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
+      for (int gq = 0; gq < groups; ++gq) {
+        uint32_t r16[16];
+        tmem_ld16(t0 + static_cast<uint32_t>(gq * N + c), r16);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[e] += __uint_as_float(r16[e]);
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t ad = dst + 4u * kLtRows * (c + e);
+        if (rank == 1)
+          st_shared_cluster_u32(ad, __float_as_uint(acc[e]));
+        else
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ad), "r"(__float_as_uint(acc[e])) : "memory");
+      }
+    }
+  }
+  __syncthreads();  // stats of every generator warp are in sm->st_*[0]
+  if (rank == 1) {
+    for (int r = threadIdx.x; r < kLtRows; r += blockDim.x) {
+      st_shared_cluster_u32(mapa(&sm->st_sum[1][r], 0), __float_as_uint(sm->st_sum[0][r]));
+      st_shared_cluster_u32(mapa(&sm->st_min[1][r], 0), __float_as_uint(sm->st_min[0][r]));
+      st_shared_cluster_u32(mapa(&sm->st_bad[1][r], 0), static_cast<uint32_t>(sm->st_bad[0][r]));
+    }
+  }
+  tc_fence_before();
+  LTP_T(t_c0);
+  cluster_sync();  // CTA 1's partials landed in CTA 0
+  LTP_T(t_c1);
+#ifdef SRPB_TC_PROFILE
+  if (threadIdx.x == 0) LTP_ADD(6, t_c1 - t_c0);
+#endif
+  if (rank == 0) {
+    for (int r = threadIdx.x; r < kLtRows; r += blockDim.x) {
+      const long long R = R0 + r;
+      if (R < n_rows && a.spec_sum) {
+        a.spec_sum[R] = sm->st_sum[0][r] + sm->st_sum[1][r];
+        a.spec_min[R] = fminf(sm->st_min[0][r], sm->st_min[1][r]);
+        a.spec_bad[R] = sm->st_bad[0][r] | sm->st_bad[1][r];
+      }
+    }
+    // Xi rows of the tile's frames are staged in shared memory (the stage
+    // ring is idle now) and leave with coalesced stores: each tile row owns
+    // 2 reach_p + 1 scattered columns, which as direct 2-byte global stores
+    // cost one L2 sector write each
+    const int nF = a.nF, Tp = a.T_pad;
+    __half* xs_hi = reinterpret_cast<__half*>(smem);           // [nF][T_pad]
+    __half* xs_lo = xs_hi + static_cast<size_t>(nF) * Tp;
+    float* xs = reinterpret_cast<float*>(xs_lo + static_cast<size_t>(nF) * Tp);  // if a.Xi
+    if (epi && !(a.dbg & 12)) {
+      const long long R = R0 + row;
+      if (R < n_rows) {
+        const int f = static_cast<int>(R / a.P), p = static_cast<int>(R - static_cast<long long>(f) * a.P);
+        const int Rp = __ldg(a.reach + p);
+        const int col0 = (f - f_lo) * Tp + __ldg(a.off + p) + Rp;  // lag 0
+        const float out_scale = 2.0f / (kLtScale * kLtScale);
+        const float* part = s_part + row;
+        const float* own = s_own + row;
+        for (int c = a.L - Rp; c <= a.L + Rp; ++c) {
+          const int n = c - a.L;
+          {
+            const float v = (own[c * kLtRows] + part[c * kLtRows]) * out_scale;
+            const int idx = col0 + n;
+            if (a.Xi) xs[idx] = v;
+            const float x = v * a.split_scale;
+            const __half hh = __float2half_rn(x);
+            xs_hi[idx] = hh;
+            xs_lo[idx] = __float2half_rn(x - __half2float(hh));
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (!(a.dbg & 20)) {
+      const long long R_end = min(R0 + kLtRows, n_rows);  // rows [R0, R_end)
+      const int t_pad0 = __ldg(a.off + a.P);
+      for (int fl = 0; fl < nF; ++fl) {
+        const long long f = f_lo + fl;
+        const long long r_lo = max(R0, f * a.P), r_hi = min(R_end, (f + 1) * a.P);
+        if (r_lo >= r_hi) break;
+        const int p0 = static_cast<int>(r_lo - f * a.P), p1 = static_cast<int>(r_hi - f * a.P);
+        const int c0 = __ldg(a.off + p0);
+        const int c1 = p1 == a.P ? Tp : __ldg(a.off + p1);  // the last pair also owns the pad
+        const size_t g0 = static_cast<size_t>(f) * Tp;
+        for (int c = c0 + static_cast<int>(threadIdx.x); c < c1; c += blockDim.x) {
+          const bool pad = c >= t_pad0;
+          const int sidx = fl * Tp + c;
+          if (a.Xi) a.Xi[g0 + c] = pad ? 0.0f : xs[sidx];
+          if (a.Xi_hi) {
+            a.Xi_hi[g0 + c] = pad ? __float2half_rn(0.0f) : xs_hi[sidx];
+            a.Xi_lo[g0 + c] = pad ? __float2half_rn(0.0f) : xs_lo[sidx];
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+#ifdef SRPB_TC_PROFILE
+  if (threadIdx.x == 0) {
+    LTP_ADD(7, clock64() - t_c1);
+    LTP_ADD(8, clock64() - t_entry);
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    atomicMax(&g_lt_prof[11], gt);  // latest end
+  }
+#endif
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tcols);
+  }
+}
+
+#ifdef SRPB_TC_PROFILE
+extern "C" int srpb_lt_profile_read(unsigned long long* out) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_lt_prof, sizeof(unsigned long long) * 16);
+  unsigned long long z[16] = {};
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_lt_prof, z, sizeof(z));
+  return e == cudaSuccess ? 0 : 1;
+}
+#endif
+
+// B operand of the tensor-core lattice: rows c = lag slot (n = c - L),
+// K = 2 Kb interleaved (cos, -sin)(w_k n T) x 2^14, fp16 hi/lo split; rows
+// past 2L zero.  fp64 phases, like lattice_twiddle_kernel.
+__global__ void lattice_tc_twiddle_kernel(const double* __restrict__ omega, int Kb, double T,
+                                          int L, int N, __half* __restrict__ bh,
+                                          __half* __restrict__ bl) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < N * Kb; e += gridDim.x * blockDim.x) {
+    const int c = e / Kb, k = e - c * Kb;
+    double sn = 0.0, cs = 0.0;
+    if (c <= 2 * L) sincos(static_cast<double>(c - L) * T * omega[k], &sn, &cs);
+    const float x[2] = {static_cast<float>(cs * kLtScale), static_cast<float>(-sn * kLtScale)};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const __half hh = __float2half_rn(x[u]);
+      const size_t o = static_cast<size_t>(c) * 2 * Kb + 2 * k + u;
+      bh[o] = hh;
+      bl[o] = __float2half_rn(x[u] - __half2float(hh));
+    }
+  }
+}
+
+int lattice_tc_n(int L) { return (2 * L + 1 + 15) / 16 * 16; }
+
+cudaError_t launch_lattice_tc_twiddles(const double* omega, int Kb, double T, int L, void* bh,
+                                       void* bl, cudaStream_t stream) {
+  const int N = lattice_tc_n(L);
+  const int total = N * Kb;
+  const int blocks = (total + 255) / 256 < 4 * kNumSMs ? (total + 255) / 256 : 4 * kNumSMs;
+  lattice_tc_twiddle_kernel<<<blocks, 256, 0, stream>>>(omega, Kb, T, L, N,
+                                                        static_cast<__half*>(bh),
+                                                        static_cast<__half*>(bl));
+  return cudaGetLastError();
+}
+
+// whether the tensor-core lattice serves this shape
+bool lattice_tc_ok(int Kb, int L, float split_scale, const void* Xi_hi) {
+  return Kb % 32 == 0 && Kb >= 64 && lattice_tc_n(L) <= kLtMaxN && split_scale != 0.0f &&
+         Xi_hi != nullptr && getenv("SRPB_LATTICE_SIMT") == nullptr;
+}
+
+static cudaError_t launch_lattice_tc(const LatticeArgs& la, int L, const void* bh, const void* bl,
+                                     cudaStream_t stream) {
+  const int N = lattice_tc_n(L);
+  CUtensorMap mh, ml;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * la.Kb), static_cast<cuuint64_t>(N)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * la.Kb) * 2};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(N)};
+  cudaError_t e = encode_tensor_map(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, bh, dims, strides, box,
+                                    CU_TENSOR_MAP_SWIZZLE_128B);
+  if (e == cudaSuccess)
+    e = encode_tensor_map(&ml, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, bl, dims, strides, box,
+                          CU_TENSOR_MAP_SWIZZLE_128B);
+  if (e != cudaSuccess) return e;
+  const int nF = lt_frames(la.P);
+  const int S = lt_stages(N, nF, la.M);
+  // spectra as [F][M][2 Kb] floats; box = 32 bins x all mics x the tile's frames
+  CUtensorMap my;
+  {
+    cuuint64_t yd[3] = {static_cast<cuuint64_t>(2 * la.Kb), static_cast<cuuint64_t>(la.M),
+                        static_cast<cuuint64_t>(la.F)};
+    cuuint64_t ys[2] = {static_cast<cuuint64_t>(2 * la.Kb) * 4,
+                        static_cast<cuuint64_t>(2 * la.Kb) * 4 * la.M};
+    cuuint32_t yb[3] = {64, static_cast<cuuint32_t>(la.M), static_cast<cuuint32_t>(nF)};
+    e = encode_tensor_map(&my, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, la.src, yd, ys, yb,
+                          CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (e != cudaSuccess) return e;
+  }
+  LtArgs a{la.src, la.F, la.P, la.M, la.Kb, N, L, S, nF,
+           getenv("SRPB_LT_DBG") ? atoi(getenv("SRPB_LT_DBG")) : 0,
+           la.pm, la.pmp, la.off, la.reach, la.T_pad,
+           la.Xi, static_cast<__half*>(la.Xi_hi), static_cast<__half*>(la.Xi_lo), la.split_scale,
+           la.spec_sum, la.spec_min, la.spec_bad};
+  const size_t smem = lt_smem_bytes(N, nF, la.M, S);
+  e = cudaFuncSetAttribute(lattice_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const long long rows = static_cast<long long>(la.F) * la.P;
+  const int tiles = static_cast<int>((rows + kLtRows - 1) / kLtRows);
+  lattice_tc_kernel<<<2 * tiles, kLtThreads, smem, stream>>>(mh, ml, my, a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_t* pm,
                                         const int32_t* pmp, int P, int weighting,
                                         const double* floors, double abs_floor,
@@ -686,7 +1218,8 @@ cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, co
                                         int L, const int32_t* off, const int32_t* reach,
                                         int max_Tp, int T_pad, float* Xi, void* Xi_hi,
                                         void* Xi_lo, float split_scale, double floor_rel,
-                                        void* spec_scratch, cudaStream_t stream) {
+                                        void* spec_scratch, cudaStream_t stream,
+                                        const void* tc_bh, const void* tc_bl) {
   if (F == 0) return cudaSuccess;
   // PHAT with the relative floor and no precomputed floors: speculative
   // lattice + per-frame fix-up (scratch: 12 bytes per frame and pair)
@@ -707,7 +1240,15 @@ cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, co
   a.spec_sum = static_cast<float*>(scratch);
   a.spec_min = a.spec_sum + n;
   a.spec_bad = reinterpret_cast<int*>(a.spec_min + n);
-  e = launch_lattice_args(a, true, max_Tp, stream);
+  if (tc_bh && tc_bl && aligned16(Y) && lattice_tc_ok(Kb, L, split_scale, Xi_hi) &&
+      lt_frames(P) <= 256 && M <= 256 &&
+      lt_stages(lattice_tc_n(L), lt_frames(P), M) >= 2 &&  // the tile's spectra fit the stages
+      static_cast<size_t>(lt_frames(P)) * T_pad * 8 <=       // and its Xi rows fit the ring
+          lt_stages(lattice_tc_n(L), lt_frames(P), M) *
+              lt_stage_bytes(lattice_tc_n(L), lt_frames(P), M))
+    e = launch_lattice_tc(a, L, tc_bh, tc_bl, stream);
+  else
+    e = launch_lattice_args(a, true, max_Tp, stream);
   if (e == cudaSuccess) {
     lattice_fixup_kernel<<<F, kFixThreads, 0, stream>>>(a);
     e = cudaGetLastError();

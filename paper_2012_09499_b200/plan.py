@@ -210,6 +210,17 @@ class SrpPlan:
         s = N.stream_handle(dev)
         N.call("srpb_lattice_twiddles", N.ptr(self.omega_dev), self.Kb, T, self.L,
                N.ptr(self.twiddles), s)
+        # tensor-core lattice (PHAT, fp16 split): B = [cos; -sin] rows per lag
+        # slot, 3xFP16 (srpb_lattice_tc_twiddles); shapes it serves: Kb a
+        # multiple of 32, 2L + 1 <= 64 lag slots
+        self.tc_twiddles = None
+        n_tc = (2 * self.L + 1 + 15) // 16 * 16
+        if self.Kb % 32 == 0 and self.Kb >= 64 and n_tc <= 64:
+            self.tc_twiddles = tuple(torch.empty((n_tc, 2 * self.Kb), dtype=torch.float16,
+                                                 device=dev) for _ in range(2))
+            N.call("srpb_lattice_tc_twiddles", N.ptr(self.omega_dev), self.Kb, T, self.L,
+                   N.ptr(self.tc_twiddles[0]), N.ptr(self.tc_twiddles[1]), s)
+        self.lattice_tc = self.tc_twiddles is not None
         # sinc split x = tau / T (srp.py:310)
         if self._geom is not None:
             self.sx_i, self.sx_f = self._device_split(sinc=True)["sinc"]
@@ -322,11 +333,16 @@ class SrpPlan:
         spec = None
         if wcode == 0 and abs_floor <= 0:  # speculative floor statistics
             spec = torch.empty(3 * F * self.P, dtype=torch.float32, device=self.device)
-        self._main("srpb_lattice_from_spectra", N.ptr(Y), F, Y.shape[1], self.Kb,
-                   N.ptr(self.pair_m), N.ptr(self.pair_mp), self.P, wcode, N.ptr(floors),
-                   abs_floor, N.ptr(clean), N.ptr(self.twiddles), self.L, N.ptr(self.off),
-                   N.ptr(self.reach), self.T_pad, *(N.ptr(o) for o in outs), float(scale),
-                   DEFAULT_PHAT_FLOOR_REL, N.ptr(spec), s)
+        args = (N.ptr(Y), F, Y.shape[1], self.Kb, N.ptr(self.pair_m), N.ptr(self.pair_mp),
+                self.P, wcode, N.ptr(floors), abs_floor, N.ptr(clean), N.ptr(self.twiddles),
+                self.L, N.ptr(self.off), N.ptr(self.reach), self.T_pad,
+                *(N.ptr(o) for o in outs), float(scale), DEFAULT_PHAT_FLOOR_REL, N.ptr(spec))
+        if split == "f16" and self.lattice_tc and spec is not None:
+            # K1b + K3 as one tensor-core GEMM over (frame, pair) rows
+            self._main("srpb_lattice_from_spectra_tc", *args, N.ptr(self.tc_twiddles[0]),
+                       N.ptr(self.tc_twiddles[1]), s)
+        else:
+            self._main("srpb_lattice_from_spectra", *args, s)
         return outs[1:] if split else outs[0]
 
     def _use_tc(self, F, kind):

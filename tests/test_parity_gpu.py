@@ -214,6 +214,77 @@ def test_speculative_floor_fixup_frames():
     assert np.array_equal(fused[2], exact[2])  # an untouched frame: bitwise the exact path
 
 
+def _xi16(plan, Y):
+    hi, lo = plan.lattice_from_spectra(Y, split="f16")
+    return ((hi.double() + lo.double()) / plan.xi_scale16).cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2_subset", "random_small", "on_lattice"])
+def test_lattice_tensor_core_matches_simt_and_reference(name):
+    """K1b + K3 as one tcgen05 GEMM over (frame, pair) rows (PHAT, fp16
+    split output) vs the SIMT fused lattice and the reference lattice;
+    pad columns zero; bitwise repeatable."""
+    g = load_golden(name)
+    Y = dev(g["Y"])
+    for n_aux in g["n_aux"]:
+        plan = plan_from_golden(g, int(n_aux))
+        assert plan.lattice_tc, (name, plan.Kb, plan.L)
+        tc = _xi16(plan, Y)
+        assert np.array_equal(tc, _xi16(plan, Y))
+        plan.lattice_tc = False
+        simt = _xi16(plan, Y)
+        plan.lattice_tc = True
+        total = plan.total_samples
+        assert np.all(tc[:, total:] == 0.0)
+        for f in range(tc.shape[0]):
+            assert rel_l2(tc[f, :total], simt[f, :total]) <= 3e-6, (name, n_aux, f)
+            assert rel_l2(tc[f, :total], g[f"lattice_{n_aux}"][f]) <= REL_L2_TOL
+
+
+def test_lattice_tensor_core_fixup_frames_and_ragged_rows():
+    """Speculative-floor edge frames through the tensor-core lattice (the
+    fix-up pass redoes them exactly), F x P not a multiple of the 128-row
+    tile, odd bin-block count per CTA half."""
+    g = load_golden("random_small")
+    Y = g["Y"].astype(np.complex64).copy()          # [3, 5, 64]
+    Y = np.concatenate([Y, Y[:1], Y[:1]] + [Y] * 4)  # 17 frames x 10 pairs = 170 rows
+    Y[0, 1, 7] = 1e-13 + 0j
+    Y[0, 2, 7] = 1e-12 + 0j
+    Y[1, 0, 3] = 1e-20 + 1e-20j
+    Y[3] = 0
+    Y[4, :, 5] = 0
+    plan = plan_from_golden(g, 3)
+    assert plan.lattice_tc
+    Yd = dev(Y)
+    tc = _xi16(plan, Yd)
+    total = plan.total_samples
+    for f in range(Y.shape[0]):
+        ref = np.concatenate(O.gcc_lattice(O.cross_spectrum(Y[f].astype(complex), g["pair_m"],
+                                                            g["pair_mp"])[0],
+                                           g["omega"], g["bounds"], T, 3)[1])
+        if f == 3:
+            assert np.all(tc[f] == 0.0) and np.all(ref == 0.0)
+            continue
+        assert rel_l2(tc[f, :total], ref) <= REL_L2_TOL, f
+    # 3 bin blocks (Kb = 96): CTA halves of 2 and 1 blocks
+    rng = np.random.default_rng(3)
+    omega = np.arange(96) * (2 * np.pi * 16000.0 / 192.0)
+    pairs = O.canonical_pairs(4)
+    pm = np.array([a for a, _ in pairs], np.int32)
+    pmp = np.array([b for _, b in pairs], np.int32)
+    bounds = np.full(len(pairs), 5e-4)
+    tdoa = rng.uniform(-1, 1, (9, len(pairs))) * bounds
+    p2 = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=2)
+    assert p2.lattice_tc
+    Y2 = (rng.standard_normal((40, 4, 96)) + 1j * rng.standard_normal((40, 4, 96))).astype(
+        np.complex64)
+    xi = _xi16(p2, dev(Y2))
+    for f in (0, 21, 39):
+        psi = O.cross_spectrum(Y2[f].astype(complex), pm, pmp)[0]
+        ref = np.concatenate(O.gcc_lattice(psi, omega, bounds, T, 2)[1])
+        assert rel_l2(xi[f, : p2.total_samples], ref) <= REL_L2_TOL
+
+
 def test_lattice_from_spectra_odd_bins_and_ragged_tiles():
     """Odd Kb (partial bin chunk), F not a multiple of the 64-frame tile,
     reach > 32 lags (several lag tiles) vs the oracle."""
