@@ -542,6 +542,8 @@ constexpr int kFixThreads = 256;
 
 __global__ void __launch_bounds__(kFixThreads)
 lattice_fixup_kernel(const LatticeArgs a) {
+  umma::pdl_wait();  // the lattice kernel's stats and Xi are complete
+  umma::pdl_launch_dependents();
   const int f = blockIdx.x;
   __shared__ double s_red[kFixThreads / 32];
   __shared__ float s_mn[kFixThreads / 32];
@@ -836,6 +838,10 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, sm->tmem_base, 0);
+  // PDL: the prologue above (barriers, TMEM, row table from plan data)
+  // overlaps the previous kernel; spectra reads and Xi / stats writes wait
+  pdl_wait();
+  pdl_launch_dependents();
   LTP_T(t_setup);
 #ifdef SRPB_TC_PROFILE
   if (threadIdx.x == 0) {
@@ -1207,7 +1213,18 @@ static cudaError_t launch_lattice_tc(const LatticeArgs& la, int L, const void* b
   if (e != cudaSuccess) return e;
   const long long rows = static_cast<long long>(la.F) * la.P;
   const int tiles = static_cast<int>((rows + kLtRows - 1) / kLtRows);
-  lattice_tc_kernel<<<2 * tiles, kLtThreads, smem, stream>>>(mh, ml, my, a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * tiles);
+  cfg.blockDim = dim3(kLtThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, lattice_tc_kernel, mh, ml, my, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1250,8 +1267,17 @@ cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, co
   else
     e = launch_lattice_args(a, true, max_Tp, stream);
   if (e == cudaSuccess) {
-    lattice_fixup_kernel<<<F, kFixThreads, 0, stream>>>(a);
-    e = cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(F);
+    cfg.blockDim = dim3(kFixThreads);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, lattice_fixup_kernel, a);
+    if (e == cudaSuccess) e = cudaGetLastError();
   }
   const cudaError_t e2 = spec_scratch == nullptr ? cudaFreeAsync(scratch, stream) : cudaSuccess;
   return e != cudaSuccess ? e : e2;

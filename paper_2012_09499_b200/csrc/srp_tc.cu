@@ -799,6 +799,10 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
 #endif
   // make the TMEM base provably warp-uniform (it stays in a uniform register)
   const uint32_t tmem = __shfl_sync(0xffffffffu, bar->tmem_base, 0);
+  // PDL: setup above overlapped the previous kernel; operand loads, map /
+  // key writes and the item cursor wait for it to complete
+  pdl_wait();
+  pdl_launch_dependents();
   // barriers every CTA of the pair signals live in the leader
   const uint32_t full_addr0 = kPair ? mapa(&bar->full[0], 0) : smem_u32(&bar->full[0]);
   const uint32_t acc_empty_addr0 =
@@ -1297,13 +1301,15 @@ cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtens
   cfg.blockDim = dim3(kTcThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cta;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   // kernels without a staged epilogue never touch the maps map
   e = cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, maps_map ? *maps_map : bh, p);
   if (e != cudaSuccess) return e;
