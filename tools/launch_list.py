@@ -18,7 +18,12 @@ def main(path, skip=0):
     agg = collections.OrderedDict()
     for r in rows[1 + skip:]:
         name = r[kn].split("(")[0].strip()
-        us = float(r[mv].replace(",", "")) * scale.get(r[mu], 1.0)
+        try:
+            us = float(r[mv].replace(",", "")) * scale.get(r[mu], 1.0)
+        except ValueError:
+            continue
+        if us != us:  # nan: a launch ncu could not time
+            continue
         n, t = agg.get(name, (0, 0.0))
         agg[name] = (n + 1, t + us)
     total = sum(t for _, t in agg.values())
