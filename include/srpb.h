@@ -199,6 +199,11 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
  * srpb_lattice_from_spectra.  Arguments as there, plus
  *   tc_b_hi, tc_b_lo  [srpb_lattice_tc_cols(L), 2 Kb] fp16 from
  *                     srpb_lattice_tc_twiddles (both NULL: SIMT path).
+ *   frame_counters    [F] int32, zero on entry and left zero (or NULL): the
+ *                     tensor-core kernel then runs the speculative-floor
+ *                     fix-up itself -- the CTA completing a frame tests it and
+ *                     redoes it exactly if flagged -- instead of a second
+ *                     kernel.  Calls sharing the counters must be stream-ordered.
  */
 int srpb_lattice_from_spectra_tc(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
                                  const int32_t* pair_mp, int P, int weighting,
@@ -206,10 +211,14 @@ int srpb_lattice_from_spectra_tc(const float* Y, int F, int M, int Kb, const int
                                  const float* tw, int L, const int32_t* off, const int32_t* reach,
                                  int T_pad, float* Xi, void* Xi_hi, void* Xi_lo, float split_scale,
                                  double floor_rel, void* spec_scratch, const void* tc_b_hi,
-                                 const void* tc_b_lo, void* stream);
+                                 const void* tc_b_lo, int* frame_counters, void* stream);
 
 /* Lag slots of the tensor-core lattice: 2L + 1 rounded up to 16. */
 int srpb_lattice_tc_cols(int L);
+
+/* 1 when srpb_lattice_from_spectra_tc takes the tensor-core path for this
+ * shape (PHAT, relative floor, fp16 split output assumed), else 0. */
+int srpb_lattice_tc_supported(int M, int P, int Kb, int L, int T_pad);
 
 /*
  * Its B operand: row c (lag n = c - L, zero rows past 2L), K = 2 Kb

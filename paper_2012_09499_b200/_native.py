@@ -41,12 +41,13 @@ _SIGNATURES = {
                                   c_void_p, c_int, c_void_p, c_void_p, c_void_p, ctypes.c_float,
                                   c_double, c_void_p, c_void_p],
     "srpb_lattice_tc_cols": [c_int],
+    "srpb_lattice_tc_supported": [c_int, c_int, c_int, c_int, c_int],
     "srpb_lattice_tc_twiddles": [c_void_p, c_int, c_double, c_int, c_void_p, c_void_p, c_void_p],
     "srpb_lattice_from_spectra_tc": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
                                      c_int, c_void_p, c_double, c_void_p, c_void_p, c_int,
                                      c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
                                      ctypes.c_float, c_double, c_void_p, c_void_p, c_void_p,
-                                     c_void_p],
+                                     c_void_p, c_void_p],
     "srpb_sinc_table": [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p,
                         c_void_p],
     "srpb_interp": [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p],
@@ -127,7 +128,9 @@ def stream_handle(device=None):
     return torch.cuda.current_stream(device).cuda_stream
 
 
-_LAUNCHING = {n for n in _SIGNATURES if n not in ("srpb_abi_version", "srpb_last_error")}
+_LAUNCHING = {n for n in _SIGNATURES if n not in ("srpb_abi_version", "srpb_last_error",
+                                                   "srpb_lattice_tc_cols",
+                                                   "srpb_lattice_tc_supported")}
 # entry points that launch more than one kernel (floor/fill pass + psi pass;
 # speculative-floor lattice + its fix-up pass)
 _KERNELS_PER_CALL = {"srpb_gcc_phat": 2, "srpb_lattice_from_spectra": 2,
@@ -138,6 +141,18 @@ _launches = 0
 def launch_count() -> int:
     """Kernel launches issued through the C ABI by this process so far."""
     return _launches
+
+
+def note_launches(n: int) -> None:
+    """Correct the launch tally for an entry whose kernel count depends on
+    its arguments (added to the per-call default)."""
+    global _launches
+    _launches += int(n)
+
+
+def query(name, *args) -> int:
+    """Call a non-launching query entry and return its integer result."""
+    return int(getattr(load(), name)(*args))
 
 
 def call(name, *args):

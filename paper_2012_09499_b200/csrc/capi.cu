@@ -20,8 +20,9 @@ cudaError_t launch_lattice_from_spectra(const float*, int, int, int, const int32
                                         const int32_t*, int, int, const double*, double,
                                         const int32_t*, const float*, int, const int32_t*,
                                         const int32_t*, int, int, float*, void*, void*, float,
-                                        double, void*, cudaStream_t, const void*, const void*);
+                                        double, void*, cudaStream_t, const void*, const void*, int*);
 int lattice_tc_n(int L);
+bool lattice_tc_shape_ok(int M, int P, int Kb, int L, int T_pad);
 cudaError_t launch_lattice_tc_twiddles(const double*, int, double, int, void*, void*,
                                        cudaStream_t);
 cudaError_t launch_conventional(const float*, int, int, int, int, const int32_t*, const float*,
@@ -102,7 +103,7 @@ static bool pow2_scale(float s) {
   return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
 }
 
-int srpb_abi_version(void) { return 11; }
+int srpb_abi_version(void) { return 12; }
 
 const char* srpb_last_error(void) { return g_err; }
 
@@ -222,7 +223,7 @@ static int lattice_from_spectra(const float* Y, int F, int M, int Kb, const int3
                                 const float* tw, int L, const int32_t* off, const int32_t* reach,
                                 int T_pad, float* Xi, void* Xi_hi, void* Xi_lo, float split_scale,
                                 double floor_rel, void* spec_scratch, const void* tc_b_hi,
-                                const void* tc_b_lo, void* stream) {
+                                const void* tc_b_lo, int* frame_counters, void* stream) {
   REQUIRE(F >= 0 && M >= 1 && P >= 1 && Kb >= 1 && L >= 0 && T_pad >= 1,
           "srpb_lattice_from_spectra: bad shape");
   REQUIRE(weighting == SRPB_WEIGHT_PHAT || weighting == SRPB_WEIGHT_IDENTITY,
@@ -242,7 +243,8 @@ static int lattice_from_spectra(const float* Y, int F, int M, int Kb, const int3
                                                   floors, abs_floor, clean, tw, L, off, reach,
                                                   2 * L + 1,
                                                   T_pad, Xi, Xi_hi, Xi_lo, split_scale, floor_rel,
-                                                  spec_scratch, S(stream), tc_b_hi, tc_b_lo),
+                                                  spec_scratch, S(stream), tc_b_hi, tc_b_lo,
+                                                  frame_counters),
                 "srpb_lattice_from_spectra");
 }
 
@@ -254,10 +256,17 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
                               void* spec_scratch, void* stream) {
   return lattice_from_spectra(Y, F, M, Kb, pair_m, pair_mp, P, weighting, floors, abs_floor,
                               clean, tw, L, off, reach, T_pad, Xi, Xi_hi, Xi_lo, split_scale,
-                              floor_rel, spec_scratch, nullptr, nullptr, stream);
+                              floor_rel, spec_scratch, nullptr, nullptr, nullptr, stream);
 }
 
 int srpb_lattice_tc_cols(int L) { return L >= 0 ? srpb::lattice_tc_n(L) : -1; }
+
+int srpb_lattice_tc_supported(int M, int P, int Kb, int L, int T_pad) {
+  return M >= 1 && L >= 0 && T_pad >= 1 && getenv("SRPB_LATTICE_SIMT") == nullptr &&
+                 srpb::lattice_tc_shape_ok(M, P, Kb, L, T_pad)
+             ? 1
+             : 0;
+}
 
 int srpb_lattice_tc_twiddles(const double* omega, int Kb, double sample_period, int L, void* b_hi,
                              void* b_lo, void* stream) {
@@ -276,13 +285,13 @@ int srpb_lattice_from_spectra_tc(const float* Y, int F, int M, int Kb, const int
                                  const float* tw, int L, const int32_t* off, const int32_t* reach,
                                  int T_pad, float* Xi, void* Xi_hi, void* Xi_lo, float split_scale,
                                  double floor_rel, void* spec_scratch, const void* tc_b_hi,
-                                 const void* tc_b_lo, void* stream) {
+                                 const void* tc_b_lo, int* frame_counters, void* stream) {
   REQUIRE(!tc_b_hi == !tc_b_lo, "srpb_lattice_from_spectra_tc: tc_b_hi and tc_b_lo go together");
   REQUIRE(((reinterpret_cast<uintptr_t>(tc_b_hi) | reinterpret_cast<uintptr_t>(tc_b_lo)) & 15) == 0,
           "srpb_lattice_from_spectra_tc: tensor-core twiddles must be 16-byte aligned");
   return lattice_from_spectra(Y, F, M, Kb, pair_m, pair_mp, P, weighting, floors, abs_floor,
                               clean, tw, L, off, reach, T_pad, Xi, Xi_hi, Xi_lo, split_scale,
-                              floor_rel, spec_scratch, tc_b_hi, tc_b_lo, stream);
+                              floor_rel, spec_scratch, tc_b_hi, tc_b_lo, frame_counters, stream);
 }
 
 int srpb_sinc_table(const int32_t* sx_i, const float* sx_f, int J, int P, const int32_t* off,

@@ -540,22 +540,47 @@ lattice_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant
 // exactly the floored ones.
 constexpr int kFixThreads = 256;
 
-__global__ void __launch_bounds__(kFixThreads)
-lattice_fixup_kernel(const LatticeArgs a) {
-  umma::pdl_wait();  // the lattice kernel's stats and Xi are complete
-  umma::pdl_launch_dependents();
-  const int f = blockIdx.x;
-  __shared__ double s_red[kFixThreads / 32];
-  __shared__ float s_mn[kFixThreads / 32];
-  __shared__ int s_flag;
+// Exact redo of frame f (all kThreads threads of the CTA): fp64 floor over
+// all pairs and bins, checked PHAT; s_red [kThreads / 32] doubles.
+template <int kThreads>
+__device__ void lattice_redo_frame(const LatticeArgs& a, int f, double* s_red);
+
+// Flag test of frame f by one warp (lane 0's return value): the relative
+// floor changes the frame iff some nonzero |raw|^2 < 1.01 floor^2, or a
+// power left the fast PHAT range.
+__device__ __forceinline__ bool lattice_frame_flag_warp(const LatticeArgs& a, int f, int lane) {
   double sum = 0.0;
   float mn = 3.0e38f;
   int bad = 0;
-  for (int p = threadIdx.x; p < a.P; p += kFixThreads) {
+  for (int p = lane; p < a.P; p += 32) {
     const size_t o = static_cast<size_t>(f) * a.P + p;
-    sum += static_cast<double>(a.spec_sum[o]);
-    mn = fminf(mn, a.spec_min[o]);
-    bad |= a.spec_bad[o];
+    sum += static_cast<double>(__ldcg(a.spec_sum + o));
+    mn = fminf(mn, __ldcg(a.spec_min + o));
+    bad |= __ldcg(a.spec_bad + o);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  const double floor2 = a.floor_rel * a.floor_rel * sum / (static_cast<double>(a.P) * a.Kb);
+  return bad || static_cast<double>(mn) < 1.01 * floor2;
+}
+
+// Flag test + exact redo of one frame (all threads of the CTA, kThreads of
+// them): s_red [kThreads / 32] doubles, s_mn [kThreads / 32] floats, s_flag.
+template <int kThreads>
+__device__ void lattice_fixup_frame(const LatticeArgs& a, int f, double* s_red, float* s_mn,
+                                    int* s_flag) {
+  double sum = 0.0;
+  float mn = 3.0e38f;
+  int bad = 0;
+  for (int p = threadIdx.x; p < a.P; p += kThreads) {
+    const size_t o = static_cast<size_t>(f) * a.P + p;
+    sum += static_cast<double>(__ldcg(a.spec_sum + o));
+    mn = fminf(mn, __ldcg(a.spec_min + o));
+    bad |= __ldcg(a.spec_bad + o);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -571,20 +596,25 @@ lattice_fixup_kernel(const LatticeArgs a) {
   if (threadIdx.x == 0) {
     double t = 0.0;
     float m = 3.0e38f;
-    for (int w = 0; w < kFixThreads / 32; ++w) {
+    for (int w = 0; w < kThreads / 32; ++w) {
       t += s_red[w];
       m = fminf(m, s_mn[w]);
     }
     const double floor2 = a.floor_rel * a.floor_rel * t / (static_cast<double>(a.P) * a.Kb);
-    s_flag = bad || static_cast<double>(m) < 1.01 * floor2;
+    *s_flag = bad || static_cast<double>(m) < 1.01 * floor2;
   }
   __syncthreads();
-  if (!s_flag) return;
+  const int flagged = *s_flag;
+  __syncthreads();  // s_red / s_flag reusable
+  if (!flagged) return;
+  lattice_redo_frame<kThreads>(a, f, s_red);
+}
 
-  // exact redo of frame f: fp64 floor over all pairs and bins
+template <int kThreads>
+__device__ void lattice_redo_frame(const LatticeArgs& a, int f, double* s_red) {
   const float2* y = a.src + static_cast<size_t>(f) * a.M * a.Kb;
   double acc = 0.0;
-  for (int k = threadIdx.x; k < a.Kb; k += kFixThreads)
+  for (int k = threadIdx.x; k < a.Kb; k += kThreads)
     for (int p = 0; p < a.P; ++p) {
       const float2 u = y[static_cast<size_t>(__ldg(a.pm + p)) * a.Kb + k];
       const float2 v = y[static_cast<size_t>(__ldg(a.pmp + p)) * a.Kb + k];
@@ -596,10 +626,11 @@ lattice_fixup_kernel(const LatticeArgs a) {
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
   __syncthreads();
   double t = 0.0;
-  for (int w = 0; w < kFixThreads / 32; ++w) t += s_red[w];
+  for (int w = 0; w < kThreads / 32; ++w) t += s_red[w];
+  __syncthreads();  // s_red reusable
   const PhatFloor fl = make_phat_floor(a.floor_rel * sqrt(t / (static_cast<double>(a.P) * a.Kb)));
   const int total = __ldg(a.off + a.P);
-  for (int col = threadIdx.x; col < total; col += kFixThreads) {
+  for (int col = threadIdx.x; col < total; col += kThreads) {
     int p = 0;
     while (__ldg(a.off + p + 1) <= col) ++p;
     const int R = __ldg(a.reach + p);
@@ -616,6 +647,16 @@ lattice_fixup_kernel(const LatticeArgs a) {
     }
     lattice_store(a, static_cast<size_t>(f) * a.T_pad + col, 2.0f * re);
   }
+}
+
+__global__ void __launch_bounds__(kFixThreads)
+lattice_fixup_kernel(const LatticeArgs a) {
+  umma::pdl_wait();  // the lattice kernel's stats and Xi are complete
+  umma::pdl_launch_dependents();
+  __shared__ double s_red[kFixThreads / 32];
+  __shared__ float s_mn[kFixThreads / 32];
+  __shared__ int s_flag;
+  lattice_fixup_frame<kFixThreads>(a, blockIdx.x, s_red, s_mn, &s_flag);
 }
 
 cudaError_t launch_lattice_twiddles(const double* omega, int Kb, double T, int L, float* tw,
@@ -738,6 +779,11 @@ struct LtSmem {
   float st_sum[2][kLtRows];        // per-row PHAT stats: [own, partner]
   float st_min[2][kLtRows];
   int st_bad[2][kLtRows];
+  // in-kernel floor fix-up (frame counters): reduction scratch, completed frames
+  double fx_red[32];
+  float fx_mn[32];
+  int fx_flag, fx_n;
+  int fx_done[kLtRows + 1];
 };
 
 // stage: A hi/lo (128 rows x 128 B), B hi/lo (N rows x 128 B), spectra tile
@@ -775,6 +821,10 @@ struct LtArgs {
   float* spec_sum;
   float* spec_min;
   int* spec_bad;
+  // speculative-floor fix-up inside the kernel: per-frame arrival counters
+  // (zero before and after each call); NULL -> separate lattice_fixup_kernel
+  int* frame_cnt;
+  LatticeArgs la;  // what the exact redo of a flagged frame reads and writes
 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kLtThreads, 1)
@@ -1108,6 +1158,44 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
         }
       }
     }
+    if (a.frame_cnt) {
+      // floor fix-up without a second kernel: the CTA that completes a frame
+      // (its rows can span two tiles) checks the frame's statistics and, if
+      // flagged, redoes the frame exactly (threadfence-reduction ordering)
+      __threadfence();  // this CTA's Xi rows and statistics, device-wide
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const long long R_end = min(R0 + kLtRows, n_rows);
+        int nd = 0;
+        for (int fl = 0; fl < nF; ++fl) {
+          const long long f = f_lo + fl;
+          const long long r_lo = max(R0, f * a.P), r_hi = min(R_end, (f + 1) * a.P);
+          if (r_lo >= r_hi) break;
+          const int rows = static_cast<int>(r_hi - r_lo);
+          if (atomicAdd(a.frame_cnt + f, rows) + rows == a.P) sm->fx_done[nd++] = static_cast<int>(f);
+        }
+        sm->fx_n = nd;
+        __threadfence();  // the other tile's rows of the completed frames
+      }
+      __syncthreads();
+      // flag test: one warp per completed frame (no CTA barriers); counters
+      // reset for the next call
+      const int nd = sm->fx_n;
+      int any = 0;
+      for (int i = warp; i < nd; i += kLtThreads / 32) {
+        const int f = sm->fx_done[i];
+        const bool flag = lattice_frame_flag_warp(a.la, f, lane);
+        if (lane == 0) {
+          sm->fx_done[i] = flag ? f : -1;
+          a.frame_cnt[f] = 0;
+        }
+        any |= flag;
+      }
+      if (__syncthreads_or(any)) {  // rare: exact redo of the flagged frames
+        for (int i = 0; i < nd; ++i)
+          if (sm->fx_done[i] >= 0) lattice_redo_frame<kLtThreads>(a.la, sm->fx_done[i], sm->fx_red);
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1175,8 +1263,18 @@ bool lattice_tc_ok(int Kb, int L, float split_scale, const void* Xi_hi) {
          Xi_hi != nullptr && getenv("SRPB_LATTICE_SIMT") == nullptr;
 }
 
+// shapes the tensor-core lattice serves (besides PHAT + fp16 split output)
+bool lattice_tc_shape_ok(int M, int P, int Kb, int L, int T_pad) {
+  if (Kb % 32 != 0 || Kb < 64 || lattice_tc_n(L) > kLtMaxN || M > 256 || P < 1) return false;
+  const int nF = lt_frames(P);
+  if (nF > 256) return false;
+  const int S = lt_stages(lattice_tc_n(L), nF, M);
+  return S >= 2 &&  // the tile's spectra fit the stages, and its Xi rows the ring
+         static_cast<size_t>(nF) * T_pad * 8 <= S * lt_stage_bytes(lattice_tc_n(L), nF, M);
+}
+
 static cudaError_t launch_lattice_tc(const LatticeArgs& la, int L, const void* bh, const void* bl,
-                                     cudaStream_t stream) {
+                                     int* frame_cnt, cudaStream_t stream) {
   const int N = lattice_tc_n(L);
   CUtensorMap mh, ml;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * la.Kb), static_cast<cuuint64_t>(N)};
@@ -1206,7 +1304,7 @@ static cudaError_t launch_lattice_tc(const LatticeArgs& la, int L, const void* b
            getenv("SRPB_LT_DBG") ? atoi(getenv("SRPB_LT_DBG")) : 0,
            la.pm, la.pmp, la.off, la.reach, la.T_pad,
            la.Xi, static_cast<__half*>(la.Xi_hi), static_cast<__half*>(la.Xi_lo), la.split_scale,
-           la.spec_sum, la.spec_min, la.spec_bad};
+           la.spec_sum, la.spec_min, la.spec_bad, frame_cnt, la};
   const size_t smem = lt_smem_bytes(N, nF, la.M, S);
   e = cudaFuncSetAttribute(lattice_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem));
@@ -1236,7 +1334,7 @@ cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, co
                                         int max_Tp, int T_pad, float* Xi, void* Xi_hi,
                                         void* Xi_lo, float split_scale, double floor_rel,
                                         void* spec_scratch, cudaStream_t stream,
-                                        const void* tc_bh, const void* tc_bl) {
+                                        const void* tc_bh, const void* tc_bl, int* frame_cnt) {
   if (F == 0) return cudaSuccess;
   // PHAT with the relative floor and no precomputed floors: speculative
   // lattice + per-frame fix-up (scratch: 12 bytes per frame and pair)
@@ -1257,16 +1355,16 @@ cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, co
   a.spec_sum = static_cast<float*>(scratch);
   a.spec_min = a.spec_sum + n;
   a.spec_bad = reinterpret_cast<int*>(a.spec_min + n);
+  bool fixed_in_kernel = false;
   if (tc_bh && tc_bl && aligned16(Y) && lattice_tc_ok(Kb, L, split_scale, Xi_hi) &&
-      lt_frames(P) <= 256 && M <= 256 &&
-      lt_stages(lattice_tc_n(L), lt_frames(P), M) >= 2 &&  // the tile's spectra fit the stages
-      static_cast<size_t>(lt_frames(P)) * T_pad * 8 <=       // and its Xi rows fit the ring
-          lt_stages(lattice_tc_n(L), lt_frames(P), M) *
-              lt_stage_bytes(lattice_tc_n(L), lt_frames(P), M))
-    e = launch_lattice_tc(a, L, tc_bh, tc_bl, stream);
-  else
+      lattice_tc_shape_ok(M, P, Kb, L, T_pad))
+  {
+    e = launch_lattice_tc(a, L, tc_bh, tc_bl, frame_cnt, stream);
+    fixed_in_kernel = frame_cnt != nullptr;
+  } else {
     e = launch_lattice_args(a, true, max_Tp, stream);
-  if (e == cudaSuccess) {
+  }
+  if (e == cudaSuccess && !fixed_in_kernel) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(F);
     cfg.blockDim = dim3(kFixThreads);

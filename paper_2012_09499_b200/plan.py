@@ -21,6 +21,7 @@ All per-frame work goes through ``libsrpb.so``; nothing here computes maps.
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -220,7 +221,12 @@ class SrpPlan:
                                                  device=dev) for _ in range(2))
             N.call("srpb_lattice_tc_twiddles", N.ptr(self.omega_dev), self.Kb, T, self.L,
                    N.ptr(self.tc_twiddles[0]), N.ptr(self.tc_twiddles[1]), s)
-        self.lattice_tc = self.tc_twiddles is not None
+        self.lattice_tc = self.tc_twiddles is not None  # user toggle (A/B tests)
+        # floor fix-up inside the tensor-core lattice (frame counters) or as
+        # its own kernel: measured, the separate kernel overlapped by PDL is
+        # ~2 us faster per C2 step (the in-kernel completion adds a fence +
+        # atomics + flag test to every tile's tail); SRPB_FIXUP_FUSED=1 flips it
+        self.lattice_fixup_fused = os.environ.get("SRPB_FIXUP_FUSED", "0") == "1"
         # sinc split x = tau / T (srp.py:310)
         if self._geom is not None:
             self.sx_i, self.sx_f = self._device_split(sinc=True)["sinc"]
@@ -254,6 +260,16 @@ class SrpPlan:
             # done counter [0] and the dynamic item cursor [1]
             st[F] = (torch.zeros(F, dtype=torch.int64, device=self.device),
                      torch.zeros(2, dtype=torch.int32, device=self.device))
+        return st[F]
+
+    def _frame_counters(self, F):
+        """Persistent zeroed per-frame counters of the in-kernel floor fix-up
+        (the kernel leaves them zero)."""
+        st = getattr(self, "_fc_state", None)
+        if st is None:
+            st = self._fc_state = {}
+        if F not in st:
+            st[F] = torch.zeros(F, dtype=torch.int32, device=self.device)
         return st[F]
 
     def _keys(self, F):
@@ -337,10 +353,17 @@ class SrpPlan:
                 self.P, wcode, N.ptr(floors), abs_floor, N.ptr(clean), N.ptr(self.twiddles),
                 self.L, N.ptr(self.off), N.ptr(self.reach), self.T_pad,
                 *(N.ptr(o) for o in outs), float(scale), DEFAULT_PHAT_FLOOR_REL, N.ptr(spec))
-        if split == "f16" and self.lattice_tc and spec is not None:
-            # K1b + K3 as one tensor-core GEMM over (frame, pair) rows
+        # the tensor-core path also needs the tile's spectra and Xi rows to
+        # fit its shared-memory ring: the C side decides, ask it
+        if (split == "f16" and self.lattice_tc and spec is not None and N.query(
+                "srpb_lattice_tc_supported", Y.shape[1], self.P, self.Kb, self.L, self.T_pad)):
+            # K1b + K3 as one tensor-core GEMM over (frame, pair) rows; the
+            # floor fix-up runs inside it (persistent zeroed frame counters)
+            cnt = self._frame_counters(F) if self.lattice_fixup_fused else None
             self._main("srpb_lattice_from_spectra_tc", *args, N.ptr(self.tc_twiddles[0]),
-                       N.ptr(self.tc_twiddles[1]), s)
+                       N.ptr(self.tc_twiddles[1]), N.ptr(cnt), s)
+            if cnt is not None:
+                N.note_launches(-1)  # the fix-up ran inside the lattice kernel
         else:
             self._main("srpb_lattice_from_spectra", *args, s)
         return outs[1:] if split else outs[0]

@@ -229,6 +229,10 @@ def test_lattice_tensor_core_matches_simt_and_reference(name):
     for n_aux in g["n_aux"]:
         plan = plan_from_golden(g, int(n_aux))
         assert plan.lattice_tc, (name, plan.Kb, plan.L)
+        from paper_2012_09499_b200 import _native as NN
+        served = NN.query("srpb_lattice_tc_supported", Y.shape[1], plan.P, plan.Kb, plan.L,
+                          plan.T_pad)
+        assert served or name == "random_small", name  # random_small: N = 64, 14-frame tiles
         tc = _xi16(plan, Y)
         assert np.array_equal(tc, _xi16(plan, Y))
         plan.lattice_tc = False
@@ -588,3 +592,41 @@ def test_candidate_sharding_batch1(path):
         assert torch.equal(torch.cat(maps, dim=1), m_full)
         red = D.keys_from_signed(torch.maximum(keys[0], keys[1]))
         assert torch.equal(D.keys_index(red).to(torch.int32), a_full)
+
+
+def test_lattice_tensor_core_in_kernel_fixup():
+    """The speculative-floor fix-up run inside the tensor-core lattice (the
+    CTA completing a frame tests it and redoes it exactly) equals the
+    separate fix-up kernel bitwise, leaves its frame counters zero, and
+    matches the oracle on edge frames."""
+    g = load_golden("c2_subset")
+    Y = g["Y"].astype(np.complex64)                  # [3, 8, 512]
+    Y = np.concatenate([Y] * 4)                      # 12 frames x 28 pairs: 3 row tiles
+    Y[0, 1, 7] = 1e-13 + 0j                          # |raw| below the floor, powers in range
+    Y[0, 2, 7] = 1e-12 + 0j
+    Y[1, 0, 3] = 1e-20 + 1e-20j                      # power out of the fast range
+    Y[2] = 0                                         # all-zero frame
+    Y[3, :, 5] = 0                                   # exact-zero bin
+    Y[9, 4, 100] = 1e-14 + 0j                        # a frame straddling two row tiles
+    n_aux = int(g["n_aux"][-1])
+    plan = plan_from_golden(g, n_aux)
+    from paper_2012_09499_b200 import _native as NN
+    assert NN.query("srpb_lattice_tc_supported", Y.shape[1], plan.P, plan.Kb, plan.L, plan.T_pad)
+    Yd = dev(Y)
+    plan.lattice_fixup_fused = True
+    fused = _xi16(plan, Yd)
+    assert np.array_equal(fused, _xi16(plan, Yd))
+    assert int(plan._frame_counters(Y.shape[0]).abs().sum().item()) == 0
+    plan.lattice_fixup_fused = False
+    sep = _xi16(plan, Yd)
+    plan.lattice_fixup_fused = True
+    assert np.array_equal(fused, sep)
+    total = plan.total_samples
+    for f in range(Y.shape[0]):
+        ref = np.concatenate(O.gcc_lattice(O.cross_spectrum(Y[f].astype(complex), g["pair_m"],
+                                                            g["pair_mp"])[0],
+                                           g["omega"], g["bounds"], T, n_aux)[1])
+        if f == 2:
+            assert np.all(fused[f] == 0.0) and np.all(ref == 0.0)
+            continue
+        assert rel_l2(fused[f, :total], ref) <= REL_L2_TOL, f
