@@ -950,15 +950,17 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
   } else {
     // --------------------------------------------------------- psi generator
     const int g = warp - kLtWarp0;  // rows kLtRW g .. kLtRW g + kLtRW - 1
-    // per-row PHAT statistics (PhatSpecStats over this CTA's bins): sum and
-    // min of |raw|^2 = pa pb over bins with both powers nonzero, and the
-    // extreme nonzero powers (range test at the end)
-    float ssum[kLtRW], smin[kLtRW], pmin[kLtRW], pmax[kLtRW];
+    // per-row PHAT statistics over this CTA's bins: sum and min of
+    // |raw|^2 = pa pb over bins with both powers nonzero (the floor test),
+    // and its maximum: the fast path below needs pa pb inside (1e-30, 1e30)
+    // (rsqrt of a normal float, no overflow in the products), so a row whose
+    // min or max leaves that range is flagged for the exact fix-up
+    float ssum[kLtRW], smin[kLtRW], smax[kLtRW];
 #pragma unroll
     for (int q = 0; q < kLtRW; ++q) {
       ssum[q] = 0.0f;
-      smin[q] = pmin[q] = 3.0e38f;
-      pmax[q] = 0.0f;
+      smin[q] = 3.0e38f;
+      smax[q] = 0.0f;
     }
     // swizzled 16-byte chunk of this lane's (Re, Im) pair in row r: depends
     // on r & 7 only (rows kLtRW g + q: r & 7 = q & 7)
@@ -970,11 +972,11 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
 #ifdef SRPB_TC_PROFILE
     long long w_y = 0;
 #endif
-    for (int i = 0; i < my_kb; ++i) {
-      const int s = i % S;
+    int s = 0, ph = 0;  // stage ring position (no divisions in the loop)
+    for (int i = 0; i < my_kb; ++i, s = s + 1 == S ? 0 : s + 1, ph ^= (s == 0)) {
       // the producer loads a stage only after its previous A was consumed
       LTP_T(t_w0);
-      mbar_wait(&sm->yfull[s], (i / S) & 1);
+      mbar_wait(&sm->yfull[s], ph);
 #ifdef SRPB_TC_PROFILE
       w_y += clock64() - t_w0;
 #endif
@@ -994,14 +996,12 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
         const float pa = fmaf(ya[q].x, ya[q].x, ya[q].y * ya[q].y);
         const float pb = fmaf(yb[q].x, yb[q].x, yb[q].y * yb[q].y);
         const float qq = pa * pb;
-        const float mp = fminf(pa, pb);
-        const bool nz = mp != 0.0f;
+        const bool nz = fminf(pa, pb) != 0.0f;  // pa pb may underflow: test the factors
         ssum[q] += qq;
         smin[q] = fminf(smin[q], nz ? qq : 3.0e38f);
-        pmin[q] = fminf(pmin[q], nz ? mp : 3.0e38f);
-        pmax[q] = fmaxf(pmax[q], fmaxf(pa, pb));
-        // 1/|raw| = rsqrt(pa pb): exact to fp32 rounding for powers in the
-        // fast range; frames outside it are redone by the fix-up pass
+        smax[q] = fmaxf(smax[q], qq);
+        // 1/|raw| = rsqrt(pa pb): exact to fp32 rounding in the range above;
+        // frames outside it are redone by the fix-up pass
         const float sc = rsqrt_approx_ftz(fmaxf(qq, 1e-37f)) * kLtScale;
         const float re = fmaf(ya[q].x, yb[q].x, ya[q].y * yb[q].y) * sc;
         const float im = fmaf(ya[q].y, yb[q].x, -(ya[q].x * yb[q].y)) * sc;
@@ -1018,7 +1018,7 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
     uint32_t sbad = 0;
 #pragma unroll
     for (int q = 0; q < kLtRW; ++q)
-      sbad |= (pmin[q] <= 1e-15f || pmax[q] >= 1e15f ? 1u : 0u) << q;
+      sbad |= (smin[q] <= 1e-30f || !(smax[q] < 1e30f) ? 1u : 0u) << q;
 #ifdef SRPB_TC_PROFILE
     if (lane == 0) { LTP_ADD(3, clock64() - t_setup); LTP_ADD(4, w_y); }
 #endif

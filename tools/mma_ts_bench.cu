@@ -1,0 +1,90 @@
+// Microbenchmark: single-CTA tcgen05.mma kind::f16 (M = 128) issue rate with
+// A from TMEM (TS, as K2 issues it) vs A from shared memory (SS), N = 160.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/mma_ts_bench tools/mma_ts_bench.cu
+#include <cstdio>
+
+#include "../paper_2012_09499_b200/csrc/umma.cuh"
+
+using namespace srpb::umma;
+
+template <bool kTS>
+__global__ void __launch_bounds__(128, 1) bench(int N, int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5;
+  const int a_bytes = 128 * 128, b_bytes = N * 128;
+  const int stage = a_bytes + b_bytes;
+  for (int i = threadIdx.x; i < 4 * stage / 4; i += blockDim.x) {
+    uint32_t h = (i + 1) * 2654435761u;
+    h ^= h >> 13;
+    reinterpret_cast<uint32_t*>(smem)[i] = (h & 0x83FF83FFu) | 0x34003400u;
+  }
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  if (threadIdx.x == 32) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  long long t0 = clock64();
+  if (warp == 1) {
+    const uint32_t idesc = idesc_f16(128, N);
+    for (int it = 0; it < iters; ++it) {
+      const int s = it & 3;
+      const uint64_t da = sw128_kmajor_desc(smem_u32(smem + s * stage));
+      const uint64_t db = sw128_kmajor_desc(smem_u32(smem + s * stage + a_bytes));
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint32_t o = 2 * ks;
+          if (kTS)  // A: 8 TMEM columns (32 bytes of K) per MMA, columns 2N..
+            mma_f16_ts(tmem + (it & 1) * N, tmem + 2 * N + 32 * (it & 1) + 8 * ks, db + o, idesc,
+                       (it > 1 || ks > 0) ? 1u : 0u);
+          else
+            mma_f16(tmem + (it & 1) * N, da + o, db + o, idesc, (it > 1 || ks > 0) ? 1u : 0u);
+        }
+      }
+      __syncwarp();
+    }
+    if (elect_one()) mma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (threadIdx.x == 32) atomicAdd(out, static_cast<unsigned long long>(t1 - t0));
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 8);
+  for (int N : {128, 160}) {
+    const int stage = 128 * 128 + N * 128;
+    const size_t smem = 1024 + 4 * size_t(stage);
+    cudaFuncSetAttribute(bench<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(bench<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int iters = 4000;
+    for (int ts = 0; ts < 2; ++ts)
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaMemset(d, 0, 8);
+        if (ts)
+          bench<true><<<148, 128, smem>>>(N, iters, d);
+        else
+          bench<false><<<148, 128, smem>>>(N, iters, d);
+        cudaError_t e = cudaDeviceSynchronize();
+        unsigned long long h = 0;
+        cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+        if (rep == 1)
+          printf("%s N=%3d: %6.1f cycles/MMA (floor %.0f) %s\n", ts ? "TS" : "SS", N,
+                 double(h) / 148.0 / (4.0 * iters), 128.0 * N / 256.0, cudaGetErrorString(e));
+      }
+  }
+  return 0;
+}
