@@ -649,14 +649,23 @@ __device__ void lattice_redo_frame(const LatticeArgs& a, int f, double* s_red) {
   }
 }
 
+// One warp tests one frame (no CTA barrier in the common, unflagged case);
+// a CTA redoes its flagged frames together afterwards.
+constexpr int kFixFrames = kFixThreads / 32;
+
 __global__ void __launch_bounds__(kFixThreads)
 lattice_fixup_kernel(const LatticeArgs a) {
   umma::pdl_wait();  // the lattice kernel's stats and Xi are complete
   umma::pdl_launch_dependents();
   __shared__ double s_red[kFixThreads / 32];
-  __shared__ float s_mn[kFixThreads / 32];
-  __shared__ int s_flag;
-  lattice_fixup_frame<kFixThreads>(a, blockIdx.x, s_red, s_mn, &s_flag);
+  __shared__ int s_flag[kFixFrames];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f = blockIdx.x * kFixFrames + w;
+  const bool flag = f < a.F && lattice_frame_flag_warp(a, f, lane);
+  if (lane == 0) s_flag[w] = flag;
+  if (!__syncthreads_or(flag)) return;
+  for (int i = 0; i < kFixFrames; ++i)
+    if (s_flag[i]) lattice_redo_frame<kFixThreads>(a, blockIdx.x * kFixFrames + i, s_red);
 }
 
 cudaError_t launch_lattice_twiddles(const double* omega, int Kb, double T, int L, float* tw,
@@ -1366,7 +1375,7 @@ cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, co
   }
   if (e == cudaSuccess && !fixed_in_kernel) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(F);
+    cfg.gridDim = dim3((F + kFixFrames - 1) / kFixFrames);
     cfg.blockDim = dim3(kFixThreads);
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
