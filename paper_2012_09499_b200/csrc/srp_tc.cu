@@ -61,7 +61,7 @@ namespace srpb {
 using namespace umma;
 
 constexpr int kTcThreads = 384;
-constexpr int kTcMaxStages = 4;
+constexpr int kTcMaxStages = 8;
 constexpr int kTcM = 128;            // candidate rows per CTA
 constexpr int kTcMaxN = 160;
 constexpr int kTcKBlock = 32;        // tf32 elements per K block = one 128-B swizzle row
@@ -114,6 +114,7 @@ struct TcParams {
   int total_items;    // full_items + 2 * (num_items - full_items)
   int num_kb;         // K blocks of 32 per tile
   int maps_tma;       // staged epilogue: maps stored by TMA (J % 4 == 0), else st.global
+  int stages;         // K4 (A by TMA): smem stages that fit the tile width
   int dbg;            // experiments only (SRPB_TC_DBG): 1 = A rows mod 2048
   int b_box;          // rows per B TMA box: this CTA's full B buffer (N, or N/2 per pair)
   int kb_per_group;   // TMEM drain period (K blocks)
@@ -642,7 +643,10 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
               const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
               const __grid_constant__ CUtensorMap tmMaps, const TcParams p) {
   using Cfg = TcCfg<kAMode, kPair, kF16>;
-  constexpr int S = Cfg::kStages;
+  // K4: as many smem stages as the tile width leaves room for (narrow tiles,
+  // e.g. batch 1, get more look-ahead on the W stream); generator modes:
+  // their TMEM A ring
+  const int S = Cfg::kASmem ? p.stages : Cfg::kStages;
   constexpr bool kASmem = Cfg::kASmem;
   constexpr int KBE = Cfg::kKbElems;
   constexpr int kCta = kPair ? 2 : 1;
@@ -813,6 +817,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // warp-wide loop, one elected lane issues (uniform operands, no per-issue
     // register broadcasts)
     int kg = 0;
+    int ps = 0, pph = 0;  // stage ring position (no divisions)
     TCP_DECL(w_empty);
     TCP_DECL(t_all);
     { TCP_T0();
@@ -835,10 +840,10 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       const uint32_t tx = static_cast<uint32_t>(kCta) *
                           (((p.dbg & 4) ? 1 : 2) * static_cast<uint32_t>(nbox * p.b_box) * 128 +
                            (kASmem ? ((p.dbg & 2) ? 1 : 2) * kABytes : 0));
-      for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
-        const int s = kg % S;
+      for (int kb = 0; kb < p.num_kb; ++kb, ++kg, ps = ps + 1 == S ? 0 : ps + 1, pph ^= (ps == 0)) {
+        const int s = ps;
         { TCP_T0();
-        mbar_wait(&bar->empty[s], ((kg / S) & 1) ^ 1);
+        mbar_wait(&bar->empty[s], pph ^ 1);
         TCP_ACC(w_empty); }
         if (elect_one()) {
           const uint32_t fb = full_addr0 + 8u * s;
@@ -872,7 +877,8 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       }
     }
     // tail: every stage's last release has landed before this CTA may exit
-    for (int t = 0; t < S; ++t, ++kg) mbar_wait(&bar->empty[kg % S], ((kg / S) & 1) ^ 1);
+    for (int t = 0; t < S; ++t, ps = ps + 1 == S ? 0 : ps + 1, pph ^= (ps == 0))
+      mbar_wait(&bar->empty[ps], pph ^ 1);
     TCP_ACC(t_all); }
     if (lane == 0) {
       TCP_FLUSH(3, w_empty);
@@ -889,6 +895,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       const uint32_t stage16 = static_cast<uint32_t>(stage_bytes >> 4);
       const uint32_t b16 = b_bytes >> 4, a16 = kABytes >> 4;
       int kg = 0;
+      int ms = 0, mph = 0;  // stage ring position
       TCP_DECL(w_full);
       TCP_DECL(w_acc);
       TCP_DECL(t_all);
@@ -899,8 +906,8 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
         const int nc = item_of(gid).nc;
         item_release(it);
         const uint32_t idesc = kF16 ? idesc_f16(kTcM * kCta, nc) : idesc_tf32(kTcM * kCta, nc);
-        for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
-          const int s = kg % S;
+        for (int kb = 0; kb < p.num_kb; ++kb, ++kg, ms = ms + 1 == S ? 0 : ms + 1, mph ^= (ms == 0)) {
+          const int s = ms;
           const int gl = kb / p.kb_per_group;                 // group within the tile
           const int g = it * p.groups_per_tile + gl;          // global group
           const int in_group = kb - gl * p.kb_per_group;
@@ -912,7 +919,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
             tc_fence_after();
           }
           { TCP_T0();
-          mbar_wait(&bar->full[s], (kg / S) & 1);
+          mbar_wait(&bar->full[s], mph);
           TCP_ACC(w_full); }
           tc_fence_after();
           const uint64_t bh = db0 + static_cast<uint64_t>(s * stage16);
@@ -1288,7 +1295,15 @@ cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtens
                       const CUtensorMap& bl, const TcParams& p, cudaStream_t stream,
                       const CUtensorMap* maps_map = nullptr) {
   using Cfg = TcCfg<kAMode, kPair, kF16>;
-  const size_t smem = tc_smem_bytes(p.N, Cfg::kASmem, kPair, Cfg::kStages, Cfg::kEpiStage) +
+  TcParams q = p;
+  int S = Cfg::kStages;
+  if (Cfg::kASmem) {  // K4: fill the 227 KB (static 1 KB included)
+    S = kTcMaxStages;
+    while (S > Cfg::kStages && tc_smem_bytes(p.N, true, kPair, S, Cfg::kEpiStage) + 1024 > 232448)
+      --S;
+  }
+  q.stages = S;
+  const size_t smem = tc_smem_bytes(p.N, Cfg::kASmem, kPair, S, Cfg::kEpiStage) +
                       (kAMode == kASinc ? sizeof(int2) * static_cast<size_t>(p.P) : 0);
   auto kern = srp_tc_kernel<kAMode, kPair, kF16>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1311,7 +1326,7 @@ cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtens
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   // kernels without a staged epilogue never touch the maps map
-  e = cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, maps_map ? *maps_map : bh, p);
+  e = cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, maps_map ? *maps_map : bh, q);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
