@@ -1269,6 +1269,14 @@ int num_sms() {
   return n;
 }
 
+// Generator modes fold one 16-column accumulator chunk per generated K block;
+// a drain period shorter than a group's chunk count (N / 32) + 1 would leave
+// the MMA waiting for a buffer the blocked generator warps must release.
+void enforce_fold_window(TcParams& p) {
+  p.kb_per_group = max(p.kb_per_group, p.N / 32 + 1);
+  p.groups_per_tile = (p.num_kb + p.kb_per_group - 1) / p.kb_per_group;
+}
+
 void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16) {
   p.N = pick_n(p.F);
   p.n_tiles = (p.F + p.N - 1) / p.N;
@@ -1348,6 +1356,7 @@ static cudaError_t conventional_tc(const void* psi_hi, const void* psi_lo, bool 
   p.num_kb = P * p.kb_per_pair;
   const bool pair = use_pair((J + kTcM - 1) / kTcM, false);
   finish_params(p, kb_per_group, pair, f16);
+  enforce_fold_window(p);
   p.scale = f16 ? 2.0f / (kF16PhaseScale * psi_scale) : 2.0f;
   p.maps = maps;
   p.keys = keys;
@@ -1435,6 +1444,7 @@ cudaError_t launch_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, 
   p.J = J;
   p.num_kb = (T_pad + kTcKBlock16 - 1) / kTcKBlock16;
   finish_params(p, kb_per_group, false, true);
+  enforce_fold_window(p);
   p.scale = 1.0f / (kF16PhaseScale * xi_scale);
   p.maps = maps;
   p.keys = keys;

@@ -630,3 +630,32 @@ def test_lattice_tensor_core_in_kernel_fixup():
             assert np.all(fused[f] == 0.0) and np.all(ref == 0.0)
             continue
         assert rel_l2(fused[f, :total], ref) <= REL_L2_TOL, f
+
+
+@pytest.mark.parametrize("kbg", [1, 4])
+def test_conventional_generator_short_drain_periods_full_width(kbg):
+    """K2's phase generators fold accumulator chunks while generating; drain
+    periods shorter than a group's chunk count must not stall the ring
+    (the launcher widens them): full-width frame tiles (F = 311 -> N = 160),
+    tf32 and fp16 operand splits, vs the oracle on a candidate subset."""
+    scene = scenes.make_c2()
+    pairs = O.canonical_pairs(8)
+    pm = np.array([a for a, _ in pairs], np.int32)
+    pmp = np.array([b for _, b in pairs], np.int32)
+    bounds = np.array([np.linalg.norm(scene.mic_pos[a] - scene.mic_pos[b]) / 343.0
+                       for a, b in pairs])
+    tdoa = O.tdoa_table_nearfield(scene.mic_pos, scene.grid[::25], pairs, 343.0)  # J = 2000
+    omega = O.bin_frequencies(16000.0, 1024)
+    Y = dev(scene.Y)
+    ref = None
+    for precision in ("auto", "tf32"):
+        plan = SrpPlan(tdoa, pm, pmp, bounds, omega, backend="tc", precision=precision,
+                       kb_per_group=kbg)
+        maps, am = plan.run(Y, "conventional")
+        m = maps.cpu().numpy()
+        if ref is None:
+            sel = [0, 155, 310]
+            psi = np.stack([O.cross_spectrum(scene.Y[f].astype(complex), pm, pmp)[0] for f in sel])
+            ref = O.conventional_frames(psi, omega, tdoa)
+        for i, f in enumerate(sel):
+            assert rel_l2(m[f], ref[i]) <= REL_L2_TOL, (precision, kbg, f)
