@@ -94,6 +94,18 @@ struct TcCfg {
 // per-role cycle counters; compiled out of libsrpb.so.
 #ifdef SRPB_TC_PROFILE
 __device__ unsigned long long g_tc_prof[24];
+// per-CTA event timeline (globaltimer ns): [cta][5 item + e], e = 0 producer
+// starts the item, 1 first stage ready at the MMA, 2 last MMA issued, 3 drain
+// starts (accumulator full), 4 item written; [cta][60] entry, [61] exit
+__device__ unsigned long long g_tc_trace[160][64];
+__device__ __forceinline__ void tc_trace(int it, int e) {
+  if (it < 12) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_tc_trace[blockIdx.x][it * 5 + e] = t;
+  }
+}
+#define TCT(it, e) tc_trace(it, e)
 #define TCP_DECL(v) long long v = 0
 #define TCP_T0() const long long _tcp0 = clock64()
 #define TCP_ACC(v) (v += clock64() - _tcp0)
@@ -103,6 +115,7 @@ __device__ unsigned long long g_tc_prof[24];
 #define TCP_T0()
 #define TCP_ACC(v)
 #define TCP_FLUSH(i, v)
+#define TCT(it, e)
 #endif
 
 struct TcParams {
@@ -831,6 +844,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       const Item t = item_of(gid);
       if (!leader) item_release(it);
       if (leader) gid_next = item_fetch(it + 1);
+      if (lane == 0) TCT(it, 0);
       const int m0 = (p.dbg & 1) ? t.m0 % 2048 : t.m0;
       const int rows = kPair ? t.nc / 2 : t.nc;    // this CTA's B rows (multiple of 16)
       const int nb = t.n0 + rank * rows;
@@ -921,6 +935,8 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
           { TCP_T0();
           mbar_wait(&bar->full[s], mph);
           TCP_ACC(w_full); }
+          if (kb == 0 && lane == 0) TCT(it, 1);
+          if (kb == p.num_kb - 1 && lane == 0) TCT(it, 2);
           tc_fence_after();
           const uint64_t bh = db0 + static_cast<uint64_t>(s * stage16);
           const uint64_t bl = bh + b16;
@@ -1078,6 +1094,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       { TCP_T0();
       tc_drain(p, bar, !leader, acc_empty_addr0, tmem, drained, t.nc, quarter, half, tot);
       TCP_ACC(c_drain); }
+      if (warp == kEpiWarp0 && lane == 0) TCT(d_it, 3);
       if (d_gl == p.groups_per_tile - 1) {
         TCP_T0();
         if constexpr (Cfg::kEpiStage)
@@ -1086,6 +1103,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
         else
           tc_write_tile(p, tile_keys, t.m0, t.n0, t.nc, quarter, half, lane, tot);
         TCP_ACC(c_write);
+        if (warp == kEpiWarp0 && lane == 0) TCT(d_it, 4);
         item_release(d_it);
         ++d_it;
         d_gl = 0;
@@ -1204,6 +1222,8 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     atomicAdd(&g_tc_prof[19], 1ull);
     unsigned long long g_exit;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+    g_tc_trace[blockIdx.x][60] = g_entry;
+    g_tc_trace[blockIdx.x][61] = g_exit;
     atomicMax(&g_tc_prof[20], ~g_entry);  // earliest entry (complemented)
     atomicMax(&g_tc_prof[21], g_exit);    // latest exit
     atomicMax(&g_tc_prof[22], ~g_exit);   // earliest exit (complemented)
@@ -1551,6 +1571,10 @@ cudaError_t launch_tf32_split(const float* x, size_t n, float* hi, float* lo, cu
 
 #ifdef SRPB_TC_PROFILE
 // instrumentation build only: copy out and clear the 16 role counters
+extern "C" int srpb_tc_trace_read(unsigned long long* host) {
+  cudaError_t e = cudaMemcpyFromSymbol(host, srpb::g_tc_trace, sizeof(unsigned long long) * 160 * 64);
+  return static_cast<int>(e);
+}
 extern "C" int srpb_tc_profile_read(unsigned long long* host16) {
   cudaError_t e = cudaMemcpyFromSymbol(host16, srpb::g_tc_prof, sizeof(unsigned long long) * 24);
   unsigned long long zero[24] = {};
