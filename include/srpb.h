@@ -95,6 +95,19 @@ int srpb_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
                   double abs_floor, float* Psi, double* floor_out, void* stream);
 
 /*
+ * Same cross-spectra (PHAT only) written as the fp16 operand split of the
+ * tensor-core K2 -- hi = fp16(s psi), lo = fp16(s psi - hi), s = split_scale
+ * (a power of two) -- into Psi_hi / Psi_lo [F, 2 P Kb] (K index p 2Kb + 2k +
+ * {re, im}, the layout srpb_f16_split gives the float view of Psi); Psi
+ * [F, P, Kb] complex64 is written too when non-NULL.  Kb even; Y and Psi
+ * 16-byte, Psi_hi / Psi_lo 8-byte aligned.
+ */
+int srpb_gcc_phat_split16(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                          const int32_t* pair_mp, int P, int weighting, double floor_rel,
+                          double abs_floor, float* Psi, void* Psi_hi, void* Psi_lo,
+                          float split_scale, double* floor_out, void* stream);
+
+/*
  * K1a: the per-frame PHAT floor alone, floor_rel * sqrt(mean_{p,k} |raw|^2)
  * accumulated in fp64 (spectral.py:268-275), and per-frame range flags;
  * feeds srpb_lattice_from_spectra.

@@ -34,6 +34,9 @@ _SIGNATURES = {
     "srpb_lattice_twiddles": [c_void_p, c_int, c_double, c_int, c_void_p, c_void_p],
     "srpb_lattice": [c_void_p, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_void_p, c_int,
                      c_void_p, c_void_p],
+    "srpb_gcc_phat_split16": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
+                              c_double, c_double, c_void_p, c_void_p, c_void_p, ctypes.c_float,
+                              c_void_p, c_void_p],
     "srpb_gcc_floor": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_double,
                        c_void_p, c_void_p, c_void_p],
     "srpb_lattice_from_spectra": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
@@ -133,7 +136,7 @@ _LAUNCHING = {n for n in _SIGNATURES if n not in ("srpb_abi_version", "srpb_last
                                                    "srpb_lattice_tc_supported")}
 # entry points that launch more than one kernel (floor/fill pass + psi pass;
 # speculative-floor lattice + its fix-up pass)
-_KERNELS_PER_CALL = {"srpb_gcc_phat": 2, "srpb_lattice_from_spectra": 2,
+_KERNELS_PER_CALL = {"srpb_gcc_phat": 2, "srpb_gcc_phat_split16": 2, "srpb_lattice_from_spectra": 2,
                      "srpb_lattice_from_spectra_tc": 2, "srpb_map_error": 2}
 _launches = 0
 

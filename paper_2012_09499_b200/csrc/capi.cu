@@ -9,7 +9,7 @@
 
 namespace srpb {
 cudaError_t launch_gcc_phat(const float*, int, int, int, const int32_t*, const int32_t*, int, int,
-                            double, double, float*, double*, cudaStream_t);
+                            double, double, float*, double*, cudaStream_t, void* = nullptr, void* = nullptr, float = 0.0f);
 cudaError_t launch_stft(const float*, int, int, int, int, int, int, float*, cudaStream_t);
 cudaError_t launch_tdoa_split(const double*, const double*, int, const int32_t*, const int32_t*,
                               int, int, double, double, int, double, const double*, double,
@@ -160,6 +160,30 @@ int srpb_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
   return status(srpb::launch_gcc_phat(Y, F, M, Kb, pair_m, pair_mp, P, weighting, floor_rel,
                                       abs_floor, Psi, floor_out, S(stream)),
                 "srpb_gcc_phat");
+}
+
+int srpb_gcc_phat_split16(const float* Y, int F, int M, int Kb, const int32_t* pair_m,
+                          const int32_t* pair_mp, int P, int weighting, double floor_rel,
+                          double abs_floor, float* Psi, void* Psi_hi, void* Psi_lo,
+                          float split_scale, double* floor_out, void* stream) {
+  REQUIRE(F >= 0 && M >= 1 && Kb >= 2 && P >= 1,
+          "srpb_gcc_phat_split16: bad shape F=%d M=%d Kb=%d P=%d", F, M, Kb, P);
+  REQUIRE(Kb % 2 == 0, "srpb_gcc_phat_split16: Kb must be even, got %d", Kb);
+  REQUIRE(M <= 64, "srpb_gcc_phat_split16: at most 64 channels supported, got %d", M);
+  REQUIRE(P <= 2016, "srpb_gcc_phat_split16: at most 2016 pairs supported, got %d", P);
+  REQUIRE(weighting == SRPB_WEIGHT_PHAT,
+          "srpb_gcc_phat_split16: the fp16 split needs PHAT-bounded psi (weighting %d)", weighting);
+  REQUIRE(pow2_scale(split_scale), "srpb_gcc_phat_split16: split_scale must be a power of two");
+  REQUIRE(F == 0 || (Y && Psi_hi && Psi_lo && pair_m && pair_mp),
+          "srpb_gcc_phat_split16: null pointer");
+  REQUIRE(((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(Psi)) & 15) == 0 &&
+              ((reinterpret_cast<uintptr_t>(Psi_hi) | reinterpret_cast<uintptr_t>(Psi_lo)) & 7) == 0,
+          "srpb_gcc_phat_split16: Y / Psi must be 16-byte and Psi_hi / Psi_lo 8-byte aligned");
+  REQUIRE(static_cast<long long>(F) * P <= 2147483647LL, "srpb_gcc_phat_split16: F*P too large");
+  return status(srpb::launch_gcc_phat(Y, F, M, Kb, pair_m, pair_mp, P, weighting, floor_rel,
+                                      abs_floor, Psi, floor_out, S(stream), Psi_hi, Psi_lo,
+                                      split_scale),
+                "srpb_gcc_phat_split16");
 }
 
 int srpb_gcc_floor(const float* Y, int F, int M, int Kb, const int32_t* pair_m,

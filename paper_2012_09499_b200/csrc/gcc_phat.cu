@@ -17,6 +17,8 @@
 // Algorithmic traffic: 8 (M + P) Kb bytes per frame.
 #include "common.cuh"
 
+#include <cuda_fp16.h>
+
 namespace srpb {
 
 constexpr int kFloorThreads = 512;
@@ -84,21 +86,42 @@ __global__ void fill_kernel(double* __restrict__ out, int n, double v) {
 // two bins of y_m and y_m' (L2-resident after K1a) and a 16-byte psi store.
 constexpr int kPsiThreads = 128;
 
+// fp16 operand split of scale * psi for the tensor-core K2 (hi = fp16(x),
+// lo = fp16(x - hi)), written next to / instead of psi: the K2 operand
+// without a separate split pass over Psi
+__device__ __forceinline__ void psi_split16(float2 v, float scale, uint32_t& hi, uint32_t& lo) {
+  const float xr = v.x * scale, xi = v.y * scale;
+  const __half2 h = __floats2half2_rn(xr, xi);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(xr - hf.x, xi - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+template <bool kSplit>
 __global__ void __launch_bounds__(kPsiThreads)
 gcc_psi_kernel(const float4* __restrict__ Y, int M, int Kb2, const int32_t* __restrict__ pm,
                const int32_t* __restrict__ pmp, int P, int weighting,
-               const double* __restrict__ floors, double const_floor, float4* __restrict__ Psi) {
+               const double* __restrict__ floors, double const_floor, float4* __restrict__ Psi,
+               uint2* __restrict__ Psi_hi, uint2* __restrict__ Psi_lo, float scale) {
   const int row = blockIdx.x;  // f * P + p
   const int f = row / P, p = row - f * P;
   const float4* ya = Y + (static_cast<size_t>(f) * M + __ldg(pm + p)) * Kb2;
   const float4* yb = Y + (static_cast<size_t>(f) * M + __ldg(pmp + p)) * Kb2;
   const PhatFloor fl = make_phat_floor(floors ? __ldg(floors + f) : const_floor);
-  float4* out = Psi + static_cast<size_t>(row) * Kb2;
+  const size_t o = static_cast<size_t>(row) * Kb2;
   for (int k2 = threadIdx.x; k2 < Kb2; k2 += kPsiThreads) {
     const float4 a = __ldg(ya + k2), b = __ldg(yb + k2);
     const float2 o0 = phat_one(make_float2(a.x, a.y), make_float2(b.x, b.y), weighting, fl);
     const float2 o1 = phat_one(make_float2(a.z, a.w), make_float2(b.z, b.w), weighting, fl);
-    out[k2] = make_float4(o0.x, o0.y, o1.x, o1.y);
+    if (!kSplit || Psi) Psi[o + k2] = make_float4(o0.x, o0.y, o1.x, o1.y);
+    if constexpr (kSplit) {
+      uint2 h, l;
+      psi_split16(o0, scale, h.x, l.x);
+      psi_split16(o1, scale, h.y, l.y);
+      Psi_hi[o + k2] = h;
+      Psi_lo[o + k2] = l;
+    }
   }
 }
 
@@ -129,7 +152,7 @@ cudaError_t launch_gcc_floor(const float* Y, int F, int M, int Kb, const int32_t
 cudaError_t launch_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t* pm,
                             const int32_t* pmp, int P, int weighting, double floor_rel,
                             double abs_floor, float* Psi, double* floor_out,
-                            cudaStream_t stream) {
+                            cudaStream_t stream, void* Psi_hi, void* Psi_lo, float split_scale) {
   if (F == 0) return cudaSuccess;
   // relative floor: per-frame values from K1a (into floor_out, or into a
   // stream-ordered scratch when the caller passed none); explicit floor and
@@ -152,12 +175,19 @@ cudaError_t launch_gcc_phat(const float* Y, int F, int M, int Kb, const int32_t*
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const bool vec = Kb % 2 == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0 &&
-                   (reinterpret_cast<uintptr_t>(Psi) & 15) == 0;
+                   (reinterpret_cast<uintptr_t>(Psi) & 15) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(Psi_hi) | reinterpret_cast<uintptr_t>(Psi_lo)) & 7) == 0;
   const int rows = F * P;
-  if (vec)
-    gcc_psi_kernel<<<rows, kPsiThreads, 0, stream>>>(reinterpret_cast<const float4*>(Y), M, Kb / 2,
-                                                     pm, pmp, P, weighting, floors, const_floor,
-                                                     reinterpret_cast<float4*>(Psi));
+  if (Psi_hi != nullptr && !vec) return cudaErrorInvalidValue;  // split needs the 2-bin path
+  if (vec && Psi_hi != nullptr)
+    gcc_psi_kernel<true><<<rows, kPsiThreads, 0, stream>>>(
+        reinterpret_cast<const float4*>(Y), M, Kb / 2, pm, pmp, P, weighting, floors, const_floor,
+        reinterpret_cast<float4*>(Psi), static_cast<uint2*>(Psi_hi), static_cast<uint2*>(Psi_lo),
+        split_scale);
+  else if (vec)
+    gcc_psi_kernel<false><<<rows, kPsiThreads, 0, stream>>>(
+        reinterpret_cast<const float4*>(Y), M, Kb / 2, pm, pmp, P, weighting, floors, const_floor,
+        reinterpret_cast<float4*>(Psi), nullptr, nullptr, 0.0f);
   else
     gcc_psi1_kernel<<<rows, kPsiThreads, 0, stream>>>(reinterpret_cast<const float2*>(Y), M, Kb,
                                                       pm, pmp, P, weighting, floors, const_floor,

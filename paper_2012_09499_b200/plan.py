@@ -447,13 +447,7 @@ class SrpPlan:
         s = N.stream_handle(self.device)
         if self._use_tc(F, "conv") and self._f16_ok("conv", _bounded):
             hi, lo = self.split_f16(psi, self.F16_UNIT_SCALE)
-            keys, done = self._argmax_state(F)
-            idx = torch.empty(F, dtype=torch.int32, device=self.device)
-            self._main("srpb_conventional_tc16", N.ptr(hi), N.ptr(lo), self.F16_UNIT_SCALE, F,
-                       self.P, self.Kb, self.period, N.ptr(self.conv_ti), N.ptr(self.conv_tf),
-                       self.J, N.ptr(out), N.ptr(keys), self.kb_per_group16, N.ptr(idx),
-                       N.ptr(done), s)
-            return out, idx
+            return self._conventional_tc16(hi, lo, F, maps, out)
         keys = self._keys(F)
         if self._use_tc(F, "conv"):
             hi, lo = self.split_tf32(psi)
@@ -467,6 +461,19 @@ class SrpPlan:
             self._main("srpb_conventional_general", N.ptr(psi), F, self.P, self.Kb,
                    N.ptr(self.omega_dev), N.ptr(self.tau_dev), self.J, N.ptr(out), N.ptr(keys), s)
         return out, self.keys_to_index(keys)
+
+    def _conventional_tc16(self, hi, lo, F, maps=True, out=None):
+        """K2 on the fp16 operand split of psi (x F16_UNIT_SCALE), argmax
+        finished in-kernel."""
+        if maps and out is None:
+            out = torch.empty((F, self.J), dtype=torch.float32, device=self.device)
+        keys, done = self._argmax_state(F)
+        idx = torch.empty(F, dtype=torch.int32, device=self.device)
+        self._main("srpb_conventional_tc16", N.ptr(hi), N.ptr(lo), self.F16_UNIT_SCALE, F,
+                   self.P, self.Kb, self.period, N.ptr(self.conv_ti), N.ptr(self.conv_tf),
+                   self.J, N.ptr(out if maps else None), N.ptr(keys), self.kb_per_group16,
+                   N.ptr(idx), N.ptr(done), N.stream_handle(self.device))
+        return (out if maps else None), idx
 
     def lattice(self, psi, out=None):
         """K3: Psi [F, P, Kb] -> Xi [F, T_pad] fp32 (pad columns zero)."""
@@ -550,6 +557,20 @@ class SrpPlan:
         weighting the contractions run in 3xFP16 (bounded operands)."""
         bounded = weighting == "phat"
         if path == "conventional":
+            F = Y.shape[0]
+            if (bounded and self._conv_ready and self.harmonic and self.Kb % 2 == 0
+                    and self._use_tc(F, "conv") and self._f16_ok("conv", True)):
+                # K1 writes the fp16 operand split of psi directly (no psi
+                # round trip through HBM, no split pass)
+                F, wcode, abs_floor = self._check_spectra(Y, weighting, phat_floor)
+                hi = torch.empty((F, 2 * self.P * self.Kb), dtype=torch.float16, device=self.device)
+                lo = torch.empty_like(hi)
+                floors = torch.empty(F, dtype=torch.float64, device=self.device)
+                self._main("srpb_gcc_phat_split16", N.ptr(Y), F, Y.shape[1], self.Kb,
+                           N.ptr(self.pair_m), N.ptr(self.pair_mp), self.P, wcode,
+                           DEFAULT_PHAT_FLOOR_REL, abs_floor, None, N.ptr(hi), N.ptr(lo),
+                           self.F16_UNIT_SCALE, N.ptr(floors), N.stream_handle(self.device))
+                return self._conventional_tc16(hi, lo, F, maps)
             psi, _ = self.cross_spectra(Y, weighting, phat_floor)
             return self.conventional(psi, maps, _bounded=bounded)
         if path == "approx":

@@ -659,3 +659,22 @@ def test_conventional_generator_short_drain_periods_full_width(kbg):
             ref = O.conventional_frames(psi, omega, tdoa)
         for i, f in enumerate(sel):
             assert rel_l2(m[f], ref[i]) <= REL_L2_TOL, (precision, kbg, f)
+
+
+def test_conventional_fused_split_equals_two_step():
+    """run(..., "conventional") has K1 write the fp16 operand split directly
+    (srpb_gcc_phat_split16); it must equal psi -> srpb_f16_split -> K2 bit
+    for bit, and the launch count drops by the split pass."""
+    from paper_2012_09499_b200 import _native as NN
+    g = load_golden("c2_subset")
+    plan = plan_from_golden(g, 4, backend="tc")
+    Y = dev(np.concatenate([g["Y"]] * 12).astype(np.complex64))  # 36 frames: tensor-core K2
+    n0 = NN.launch_count()
+    m1, a1 = plan.run(Y, "conventional")
+    fused = NN.launch_count() - n0
+    psi, _ = plan.cross_spectra(Y)
+    n0 = NN.launch_count()
+    m2, a2 = plan.conventional(psi, _bounded=True)  # PHAT psi: the 3xFP16 K2 as well
+    two = NN.launch_count() - n0
+    assert torch.equal(m1, m2) and torch.equal(a1, a2)
+    assert fused == 3 and two == 2  # floor + psi16 + K2 vs split + K2 (after K1's 2)
