@@ -123,8 +123,9 @@ struct TcParams {
   int n_tiles;        // frame tiles
   int num_items;      // n_tiles * candidate tiles (of 128, or 256 per pair)
   int full_items;     // items run at full width; the tail wave's items are split
-  int n_piece0;       // frames of a split item's first piece (second: N - n_piece0)
-  int total_items;    // full_items + 2 * (num_items - full_items)
+  int n_piece0;       // frames of a split item's pieces (the last: N - (k - 1) n_piece0)
+  int n_pieces;       // pieces k per split item
+  int total_items;    // full_items + k * (num_items - full_items)
   int num_kb;         // K blocks of 32 per tile
   int maps_tma;       // staged epilogue: maps stored by TMA (J % 4 == 0), else st.global
   int stages;         // K4 (A by TMA): smem stages that fit the tile width
@@ -710,17 +711,17 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   auto item_of = [&](int g) {
     int b = g, piece = -1;
     if (g >= p.full_items) {
-      b = p.full_items + ((g - p.full_items) >> 1);
-      piece = (g - p.full_items) & 1;
+      const int q = g - p.full_items;
+      b = p.full_items + q / p.n_pieces;
+      piece = q - (q / p.n_pieces) * p.n_pieces;
     }
     Item r;
     r.m0 = ((b / p.n_tiles) * kCta + rank) * kTcM;
     r.n0 = (b % p.n_tiles) * p.N;
     r.nc = p.N;
-    if (piece == 0) r.nc = p.n_piece0;
-    if (piece == 1) {
-      r.n0 += p.n_piece0;
-      r.nc = p.N - p.n_piece0;
+    if (piece >= 0) {
+      r.n0 += piece * p.n_piece0;
+      r.nc = piece < p.n_pieces - 1 ? p.n_piece0 : p.N - (p.n_pieces - 1) * p.n_piece0;
     }
     return r;
   };
@@ -1311,6 +1312,7 @@ void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16) {
   const bool split = p.N >= 64 && p.n_piece0 < p.N && p.num_items > units &&
                      p.num_items % units != 0 && getenv("SRPB_TC_NOSPLIT") == nullptr;
   p.full_items = split ? p.num_items / units * units : p.num_items;
+  p.n_pieces = 2;
   p.total_items = p.full_items + 2 * (p.num_items - p.full_items);
   p.kb_per_group = max(f16 ? 2 : 4, kb_per_group);
   p.b_box = getenv("SRPB_TC_BOX16") ? 16 : (pair ? p.N / 2 : p.N);
@@ -1415,6 +1417,17 @@ static cudaError_t interp_tc(const void* w_hi, const void* w_lo, const void* xi_
   p.num_kb = (T_pad + kbe - 1) / kbe;  // partial last block: TMA zero-fills
   const bool pair = use_pair((J + kTcM - 1) / kTcM, true);
   finish_params(p, kb_per_group, pair, f16);
+  // K4's pieces cost only their MMAs (W is re-read, mostly from L2): split
+  // the tail items finer than the generator kernels can afford
+  if (p.full_items < p.num_items) {
+    const char* e = getenv("SRPB_TC_SPLITK");
+    const int k = e ? atoi(e) : 2;
+    if (k > 2) {
+      p.n_piece0 = max(32, (p.N / k + 31) / 32 * 32);
+      p.n_pieces = (p.N + p.n_piece0 - 1) / p.n_piece0;
+      p.total_items = p.full_items + p.n_pieces * (p.num_items - p.full_items);
+    }
+  }
   p.scale = scale;
   p.maps = maps;
   p.keys = keys;
