@@ -380,6 +380,14 @@ int srpb_argmax_keys_reset(unsigned long long* keys, int F, void* stream);
 /* idx[f] = candidate index held by keys[f] (int32). */
 int srpb_keys_to_index(const unsigned long long* keys, int F, int32_t* idx, void* stream);
 
+/*
+ * Strided host -> device copy of `rows` rows of `row_bytes` (one DMA
+ * request, cudaMemcpy2DAsync): a frame range of multichannel audio [M, L]
+ * is a column block of the host array.  Pinned src for an async copy.
+ */
+int srpb_copy_rows_h2d(void* dst, size_t dst_pitch, const void* src, size_t src_pitch,
+                       size_t row_bytes, int rows, void* stream);
+
 /* ---- device-side cross-checks ---------------------- */
 
 /*

@@ -75,6 +75,8 @@ _SIGNATURES = {
     "srpb_argmax_f64": [c_void_p, c_int, c_int, c_void_p, c_void_p],
     "srpb_argmax_keys_reset": [c_void_p, c_int, c_void_p],
     "srpb_keys_to_index": [c_void_p, c_int, c_void_p, c_void_p],
+    "srpb_copy_rows_h2d": [c_void_p, ctypes.c_size_t, c_void_p, ctypes.c_size_t,
+                           ctypes.c_size_t, c_int, c_void_p],
     "srpb_srp_quadform": [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
                           c_void_p, c_void_p, c_void_p, c_void_p],
     "srpb_map_error": [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p,
@@ -133,7 +135,8 @@ def stream_handle(device=None):
 
 _LAUNCHING = {n for n in _SIGNATURES if n not in ("srpb_abi_version", "srpb_last_error",
                                                    "srpb_lattice_tc_cols",
-                                                   "srpb_lattice_tc_supported")}
+                                                   "srpb_lattice_tc_supported",
+                                                   "srpb_copy_rows_h2d")}
 # entry points that launch more than one kernel (floor/fill pass + psi pass;
 # speculative-floor lattice + its fix-up pass)
 _KERNELS_PER_CALL = {"srpb_gcc_phat": 2, "srpb_gcc_phat_split16": 2, "srpb_lattice_from_spectra": 2,

@@ -471,6 +471,17 @@ int srpb_keys_to_index(const unsigned long long* keys, int F, int32_t* idx, void
   return status(srpb::launch_keys_to_index(keys, F, idx, S(stream)), "srpb_keys_to_index");
 }
 
+int srpb_copy_rows_h2d(void* dst, size_t dst_pitch, const void* src, size_t src_pitch,
+                       size_t row_bytes, int rows, void* stream) {
+  REQUIRE(rows >= 0 && row_bytes <= dst_pitch && row_bytes <= src_pitch,
+          "srpb_copy_rows_h2d: bad geometry");
+  REQUIRE(rows == 0 || row_bytes == 0 || (dst && src), "srpb_copy_rows_h2d: null pointer");
+  if (rows == 0 || row_bytes == 0) return 0;
+  return status(cudaMemcpy2DAsync(dst, dst_pitch, src, src_pitch, row_bytes,
+                                  static_cast<size_t>(rows), cudaMemcpyHostToDevice, S(stream)),
+                "srpb_copy_rows_h2d");
+}
+
 int srpb_srp_quadform(const float* Psi, int F, int P, int Kb, const double* omega,
                       const double* tau_rel, int J, int M, const int32_t* pair_m,
                       const int32_t* pair_mp, double* maps, void* stream) {

@@ -79,9 +79,16 @@ class ChunkedRunner:
                 if not self._first:  # previous call's compute has read the input
                     self.s_in.wait_event(self.ev_comp[c])
                 if self.audio is not None:
+                    # the chunk's sample span of every channel: one strided
+                    # DMA (a column block of the host [M, L] array)
                     a, b = self.spans[c]
-                    for m in range(st.x.shape[0]):  # contiguous pinned rows
-                        st.x[m].copy_(Y_host[m, a:b], non_blocking=True)
+                    M = st.x.shape[0]
+                    if Y_host.stride(1) != 1 or Y_host.dtype != st.x.dtype:
+                        raise ValueError("audio must be a row-major float32 [M, L] host array")
+                    es = Y_host.element_size()
+                    N.call("srpb_copy_rows_h2d", N.ptr(st.x), st.x.stride(0) * es,
+                           Y_host.data_ptr() + a * es, Y_host.stride(0) * es, (b - a) * es, M,
+                           self.s_in.cuda_stream)
                 else:
                     st.Y.copy_(Y_host[lo:hi], non_blocking=True)
                 self.ev_in[c].record(self.s_in)
