@@ -1121,16 +1121,19 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
     __half* xs_hi = reinterpret_cast<__half*>(smem);           // [nF][T_pad]
     __half* xs_lo = xs_hi + static_cast<size_t>(nF) * Tp;
     float* xs = reinterpret_cast<float*>(xs_lo + static_cast<size_t>(nF) * Tp);  // if a.Xi
-    if (epi && !(a.dbg & 12)) {
-      const long long R = R0 + row;
+    // 4 threads per tile row (the generator warps), lags interleaved
+    const int gt = static_cast<int>(threadIdx.x) - 32 * kLtWarp0;
+    if (gt >= 0 && !(a.dbg & 12)) {
+      const int orow = gt >> 2, sub = gt & 3;
+      const long long R = R0 + orow;
       if (R < n_rows) {
         const int f = static_cast<int>(R / a.P), p = static_cast<int>(R - static_cast<long long>(f) * a.P);
         const int Rp = __ldg(a.reach + p);
         const int col0 = (f - f_lo) * Tp + __ldg(a.off + p) + Rp;  // lag 0
         const float out_scale = 2.0f / (kLtScale * kLtScale);
-        const float* part = s_part + row;
-        const float* own = s_own + row;
-        for (int c = a.L - Rp; c <= a.L + Rp; ++c) {
+        const float* part = s_part + orow;
+        const float* own = s_own + orow;
+        for (int c = a.L - Rp + sub; c <= a.L + Rp; c += 4) {
           const int n = c - a.L;
           {
             const float v = (own[c * kLtRows] + part[c * kLtRows]) * out_scale;
