@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace srpb {
 
@@ -197,6 +198,35 @@ __device__ __forceinline__ float sinc_weight_fast(int i, float f, float spi, int
   const float w = __uint_as_float(__float_as_uint(spi * rcp_approx_ftz(static_cast<float>(d) + f)) ^
                                   (static_cast<uint32_t>(d & 1) << 31));
   return f == 0.0f ? (d == 0 ? 1.0f : 0.0f) : w;
+}
+
+// Programmatic dependent launch on the lattice -> fix-up -> K4 chain (default
+// on).  SRPB_NO_PDL=1 launches them as plain stream-ordered kernels: ncu's
+// per-node profiling of captured graphs rejects the programmatic edges
+// (LaunchFailed), so launch lists of graph replays are taken with it set.
+inline int pdl_attr_value() {
+  static const int v = getenv("SRPB_NO_PDL") ? 0 : 1;
+  return v;
+}
+
+// Opt a kernel into dynamic shared memory.  The attribute is raised to the
+// device's whole opt-in budget rather than to this launch's size: it is per
+// function, and a captured graph node replayed after another launch of the
+// same kernel lowered it would otherwise be refused (ncu's per-node replay of
+// graphs does exactly that).  The launch's own dynamicSmemBytes still decides
+// the carveout.
+template <typename Kern>
+inline cudaError_t allow_dynamic_smem(Kern kern, size_t need) {
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+  if (e != cudaSuccess) return e;
+  int dev = 0, optin = 0;
+  e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  const int cap = optin - static_cast<int>(fa.sharedSizeBytes);
+  if (need > static_cast<size_t>(cap)) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
 }
 
 }  // namespace srpb

@@ -103,8 +103,7 @@ static cudaError_t launch_quadform_fb(const float2* psi, int F, int P, int Kb, c
   int kc = (kQfSmem - fixed) / per_bin;
   kc = kc < 1 ? 1 : (kc > 32 ? 32 : kc);
   const int smem = fixed + kc * per_bin;
-  cudaError_t e = cudaFuncSetAttribute(quadform_kernel<kFB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = allow_dynamic_smem(quadform_kernel<kFB>, smem);
   if (e != cudaSuccess) return e;
   dim3 grid((J + kQfThreads - 1) / kQfThreads, (F + kFB - 1) / kFB);
   quadform_kernel<kFB><<<grid, kQfThreads, smem, stream>>>(psi, F, P, Kb, omega, tau_rel, J, M,

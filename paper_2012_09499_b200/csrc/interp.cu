@@ -164,9 +164,7 @@ cudaError_t launch_interp_onthefly(const int32_t* sx_i, const float* sx_f, int P
   dim3 grid((J + kTileJ - 1) / kTileJ, (F + kTileF - 1) / kTileF);
   const size_t smem = sizeof(int32_t) * (2 * P + 1);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(interp_simt_kernel<true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = allow_dynamic_smem(interp_simt_kernel<true>, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
   interp_simt_kernel<true><<<grid, kGemmThreads, smem, stream>>>(

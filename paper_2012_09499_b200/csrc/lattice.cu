@@ -680,9 +680,7 @@ static cudaError_t launch_lattice_kernel(const CUtensorMap& tm_src, const CUtens
                                          const LatticeArgs& a, dim3 grid, cudaStream_t stream) {
   constexpr int smem = static_cast<int>(LatGeom<kTma>::kSmem);
   static_assert(2 * LatGeom<kTma>::kSmem <= 227 * 1024, "two CTAs per SM");
-  // per launch: the attribute is per device, and setting it is cheap
-  cudaError_t e = cudaFuncSetAttribute(lattice_kernel<kFromY, kTma>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = allow_dynamic_smem(lattice_kernel<kFromY, kTma>, smem);
   if (e != cudaSuccess) return e;
   lattice_kernel<kFromY, kTma><<<grid, kLatThreads, smem, stream>>>(tm_src, tm_tw, a);
   return cudaGetLastError();
@@ -1318,8 +1316,7 @@ static cudaError_t launch_lattice_tc(const LatticeArgs& la, int L, const void* b
            la.Xi, static_cast<__half*>(la.Xi_hi), static_cast<__half*>(la.Xi_lo), la.split_scale,
            la.spec_sum, la.spec_min, la.spec_bad, frame_cnt, la};
   const size_t smem = lt_smem_bytes(N, nF, la.M, S);
-  e = cudaFuncSetAttribute(lattice_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem));
+  e = allow_dynamic_smem(lattice_tc_kernel, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const long long rows = static_cast<long long>(la.F) * la.P;
   const int tiles = static_cast<int>((rows + kLtRows - 1) / kLtRows);
@@ -1330,7 +1327,7 @@ static cudaError_t launch_lattice_tc(const LatticeArgs& la, int L, const void* b
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_attr_value();
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   e = cudaLaunchKernelEx(&cfg, lattice_tc_kernel, mh, ml, my, a);
@@ -1383,7 +1380,7 @@ cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, co
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_attr_value();
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     e = cudaLaunchKernelEx(&cfg, lattice_fixup_kernel, a);

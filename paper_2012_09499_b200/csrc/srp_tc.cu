@@ -1336,8 +1336,7 @@ cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtens
   const size_t smem = tc_smem_bytes(p.N, Cfg::kASmem, kPair, S, Cfg::kEpiStage) +
                       (kAMode == kASinc ? sizeof(int2) * static_cast<size_t>(p.P) : 0);
   auto kern = srp_tc_kernel<kAMode, kPair, kF16>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = allow_dynamic_smem(kern, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   constexpr int cta = kPair ? 2 : 1;
   const int units = min(p.total_items, num_sms() / cta);
@@ -1352,7 +1351,7 @@ cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtens
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_attr_value();
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   // kernels without a staged epilogue never touch the maps map

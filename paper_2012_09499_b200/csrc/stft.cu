@@ -150,8 +150,7 @@ cudaError_t launch_stft(const float* x, int M, int L, int N, int hop, int window
   if (F == 0) return cudaSuccess;
   if ((N & (N - 1)) != 0 || N < 4) {
     const int smem = static_cast<int>(sizeof(float2) * N + sizeof(float) * N);
-    cudaError_t e = cudaFuncSetAttribute(stft_dft_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = allow_dynamic_smem(stft_dft_kernel, smem);
     if (e != cudaSuccess) return e;
     stft_dft_kernel<<<dim3(F, M), kStftThreads, smem, stream>>>(x, M, L, N, hop, window,
                                                                 reinterpret_cast<float2*>(Y));
@@ -159,8 +158,7 @@ cudaError_t launch_stft(const float* x, int M, int L, int N, int hop, int window
   }
   const int H = N / 2;
   const int smem = static_cast<int>(sizeof(float2)) * 3 * H;  // a, b, twiddles
-  cudaError_t e = cudaFuncSetAttribute(stft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem);
+  cudaError_t e = allow_dynamic_smem(stft_kernel, smem);
   if (e != cudaSuccess) return e;
   // one thread per radix-4 butterfly (H/4), 32 ... 256 threads
   const int threads = H / 4 < 32 ? 32 : (H / 4 > kStftThreads ? kStftThreads : H / 4);
