@@ -435,6 +435,23 @@ def test_captured_step_and_chunked_runner_match_eager():
         assert torch.equal(mh, ref_maps.cpu()) and torch.equal(ah, ref_am.cpu())
 
 
+def test_graph_replay_after_launches_of_other_widths():
+    """A captured step replays unchanged after eager launches of the same
+    kernels with other frame counts (other tile widths, stage counts and
+    dynamic shared memory sizes)."""
+    g = load_golden("c2_subset")
+    Y = np.concatenate([g["Y"]] * 60)  # 180 frames: two frame tiles
+    plan = plan_from_golden(g, 4, weights="stored", backend="tc")
+    for path in ("approx", "conventional"):
+        ref_maps, ref_am = plan.run(dev(Y), path)
+        cap = plan.capture(Y.shape[0], Y.shape[1], path)
+        for f in (1, 7, 33):
+            plan.run(dev(Y[:f]), path)
+        m, a = cap.replay(dev(Y))
+        torch.cuda.synchronize()
+        assert torch.equal(m, ref_maps) and torch.equal(a, ref_am)
+
+
 def test_argmax_only_mode_matches_maps_mode():
     g = load_golden("c2_subset")
     plan = plan_from_golden(g, 4)
