@@ -53,7 +53,11 @@ def parse():
                     help="frames in the CPU approx sample (0 = the whole 311-frame workload)")
     ap.add_argument("--cpu-conv-frames", type=int, default=2,
                     help="frames in the CPU conventional sample (~8 s each on 16 threads)")
-    ap.add_argument("--e2e-chunks", type=int, default=6,
+    ap.add_argument("--am-chunks", type=int, default=2,
+                    help="frame chunks of the argmax-only end-to-end runner (spectra in)")
+    ap.add_argument("--audio-am-chunks", type=int, default=1,
+                    help="frame chunks of the argmax-only end-to-end runner (audio in)")
+    ap.add_argument("--e2e-chunks", type=int, default=4,
                     help="frame chunks pipelined by the end-to-end runner")
     return ap.parse_args()
 
@@ -340,7 +344,7 @@ def run_ours(args):
                "conventional": ChunkedRunner(plan, F, Y.shape[1], "conventional", chunks=2)}
     # argmax-only serving (maps never leave the device; the drop-in's SrpMap
     # fetches values lazily, so a caller reading only argmax_candidate pays this)
-    runner_am = ChunkedRunner(plan, F, Y.shape[1], "approx", chunks=3, maps=False)
+    runner_am = ChunkedRunner(plan, F, Y.shape[1], "approx", chunks=args.am_chunks, maps=False)
 
     # audio-input end to end: pinned host audio of the
     # C2 shape (8 x 160,000 samples -> the same 311 frames), K0 STFT inside
@@ -350,7 +354,7 @@ def run_ours(args):
         (Y.shape[1], L_audio)).astype(np.float32)).pin_memory()
     # streaming localisation (audio in, per-frame argmax out; maps stay on
     # the device): the smallest host traffic the API allows
-    runner_audio_am = ChunkedRunner(plan, F, Y.shape[1], "approx", chunks=3, maps=False,
+    runner_audio_am = ChunkedRunner(plan, F, Y.shape[1], "approx", chunks=args.audio_am_chunks, maps=False,
                                     audio=(2 * Kb, Kb, "sqrt_hann"))
     runner_audio = ChunkedRunner(plan, F, Y.shape[1], "approx", chunks=args.e2e_chunks,
                                  audio=(2 * Kb, Kb, "sqrt_hann"))
@@ -457,14 +461,14 @@ def run_ours(args):
         "e2e_argmax_only": {"value": units / (e2e_m * 1e-3), "unit": UNIT,
                             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": F * 4,
                             "ms_per_step": e2e_m,
-                            "api": "ChunkedRunner(maps=False, 3 chunks): pinned host Y -> "
-                                   "pinned host argmax; maps not materialised"},
+                            "api": ("ChunkedRunner(maps=False, %d chunks): pinned host Y -> "
+                                    "pinned host argmax; maps not materialised" % args.am_chunks)},
         "e2e_audio_argmax_only": {"value": units / (e2e_xm * 1e-3), "unit": UNIT,
                                   "h2d_bytes_per_step": int(x_host.numel() * 4),
                                   "d2h_bytes_per_step": F * 4, "ms_per_step": e2e_xm,
-                                  "api": "ChunkedRunner(audio=..., maps=False, 3 chunks): pinned "
-                                         "host audio -> K0 STFT + approx path -> pinned host "
-                                         "argmax"},
+                                  "api": ("ChunkedRunner(audio=..., maps=False, %d chunks): pinned "
+                                          "host audio -> K0 STFT + approx path -> pinned host "
+                                          "argmax" % args.audio_am_chunks)},
         "gpu_launches": launches_a,
         "roofline": roof_a,
         "conventional": {"value": units / (ms_c * 1e-3), "unit": UNIT, "ms_per_step": ms_c,

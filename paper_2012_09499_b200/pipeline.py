@@ -72,7 +72,9 @@ class ChunkedRunner:
         """Enqueue one pass: Y_host [F, M, Kb] complex64 (or [M, L] float32
         audio) in pinned memory -> maps_host [F, J] float32 and argmax_host
         [F] int32 (pinned).  Asynchronous with respect to the host; the
-        caller's current stream waits for the last device->host copy."""
+        caller's current stream waits for the last device->host copy, and
+        the first host->device copy waits for the caller's prior work."""
+        self.s_in.wait_stream(torch.cuda.current_stream(self.plan.device))
         for c, (lo, hi) in enumerate(self.bounds):
             st = self.steps[c]
             with torch.cuda.stream(self.s_in):
