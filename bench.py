@@ -1,22 +1,34 @@
 #!/usr/bin/env python
 """Benchmark of the SRP-map hot path (BASELINE.json metric) on B200.
 
-Workload (config.workload): BASELINE configs[1] "C2" -- UCA M=8 (P=28 pairs),
-fs=16 kHz, frame length 1024 (512 bins), 10 s scene -> F=311 frames,
-J=50,000 candidates (50x50x20 over 5x5x2 m), N_aux=4 for the approximate
-path.  A step = one pass of the hot path over the 311-frame batch:
-GCC-PHAT -> lattice IDFT -> sinc interpolation (maps + fused argmax) for the
-headline ``value`` (Nyquist-approximate path), and GCC-PHAT -> conventional
-map (+ fused argmax) reported under ``conventional``.
+Headline workload (``config.workload``): BASELINE configs[3] "C4", the
+largest single-GPU configuration (BASELINE.json quotes its metric on no
+particular config): M=32 microphones at seeded uniform positions in a
+6x5x3 m room (P=496 pairs), 2 equal-power white sources, 10 dB SNR, frame
+1024 / hop 512 (Kb=512), 4096 frames, 120x100x50 grid (J=600,000), N_aux=2
+(sum T_p = 143,692 lattice samples).  A step = one pass of the hot path over
+the whole 4096-frame batch with inputs resident in HBM:
 
-Timing: W untimed warm-ups, then K timed steps, each bracketed by CUDA
-events on the launching stream; L2 (126 MB) is flushed before every timed
-step by writing a 256 MiB buffer (outside the events).  Multi-GPU
-(torchrun): one process per GPU, every rank runs its own seeded scene (weak
-scaling, frames are independent -- no data-path collective); barrier +
-synchronize around the timed region and the max over ranks of the device
-time.  ``--impl reference`` times the reference's CPU algorithm (the oracle
-port in ``oracle/``) on the host cores, on bounded frame samples.
+* ``value``: Nyquist-approximate path -- GCC-PHAT fused into the lattice
+  IDFT, then sinc interpolation on the tensor cores with the weights
+  generated in TMEM (the dense table would be 345 GB) -> maps [F, J] fp32 +
+  fused per-frame argmax;
+* ``conventional``: GCC-PHAT -> conventional map (steering phases generated
+  in TMEM) + fused argmax, the same frames and candidates.
+
+Extra lines: C2 (configs[1]) N_aux {0, 2, 4}, C3 (configs[2]) N_aux 0..8,
+C5 (configs[4]) batch {1, 16, 256, 4096, 65536}; each says its own steps.
+
+Timing: W untimed warm-ups, then K timed steps bracketed by CUDA events on
+the launching stream; a 256 MiB buffer write flushes L2 before every timed
+step (outside the events; the C4 inputs are larger than L2 anyway).
+Multi-GPU (``--gpus N``; spawned through torch.distributed.run when
+WORLD_SIZE is unset): strong scaling -- the 4096 frames are split into
+contiguous ranges (one per rank, geometry replicated), and every timed step
+ends with the NCCL all-gather of the per-frame maps and argmaxes; barrier +
+synchronize around the timed region, max over ranks.  ``--impl reference``
+times the reference's CPU algorithm (the oracle port in ``oracle/``) on the
+host cores, on bounded samples of the same workload.
 """
 
 from __future__ import annotations
@@ -24,6 +36,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -39,7 +52,8 @@ METRIC = "SRP frames·candidates/sec (conv & Nyquist-approx), % of HBM/tensor ro
 UNIT = "frames*candidates/s"
 FS = 16000.0
 T = 1.0 / FS
-N_AUX = 4
+C_SOUND = 343.0
+DTYPE = "3xfp16-split operands, fp32 accumulate (fp32-accurate maps)"
 
 
 def parse():
@@ -48,51 +62,72 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=4096, help="C4 frames (BASELINE: 4096)")
+    ap.add_argument("--conv-steps", type=int, default=3,
+                    help="timed steps of the C4 conventional line (~6 s each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-frames", type=int, default=0,
-                    help="frames in the CPU approx sample (0 = the whole 311-frame workload)")
-    ap.add_argument("--cpu-conv-frames", type=int, default=2,
-                    help="frames in the CPU conventional sample (~8 s each on 16 threads)")
-    ap.add_argument("--am-chunks", type=int, default=2,
-                    help="frame chunks of the argmax-only end-to-end runner (spectra in)")
-    ap.add_argument("--audio-am-chunks", type=int, default=1,
-                    help="frame chunks of the argmax-only end-to-end runner (audio in)")
-    ap.add_argument("--e2e-chunks", type=int, default=4,
-                    help="frame chunks pipelined by the end-to-end runner")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-sweeps", action="store_true")
+    ap.add_argument("--cpu-frames", type=int, default=2,
+                    help="C4 frames in the CPU sample (per process)")
+    ap.add_argument("--cpu-cands", type=int, default=512,
+                    help="C4 candidates in the CPU interpolation sample")
+    ap.add_argument("--cpu-conv-cands", type=int, default=1024,
+                    help="C4 candidates in the CPU conventional sample")
     return ap.parse_args()
 
 
-# ----------------------------------------------------------------- workload
-def workload(rank=0):
+# ----------------------------------------------------------------- workloads
+def c4_scene(num_frames):
     from paper_2012_09499_b200 import scenes
-    from oracle import srp_oracle as O  # geometry helpers only (host constants)
 
-    scene = scenes.make_c2(scene_index=rank)
-    pairs = O.canonical_pairs(8)
-    pm = np.array([m for m, _ in pairs], np.int32)
-    pmp = np.array([mp for _, mp in pairs], np.int32)
-    bounds = np.array([np.linalg.norm(scene.mic_pos[m] - scene.mic_pos[mp]) / 343.0
-                       for m, mp in pairs])
-    tdoa = O.tdoa_table_nearfield(scene.mic_pos, scene.grid, pairs, 343.0)
-    omega = 2.0 * np.pi * np.arange(512) * FS / 1024
-    return scene, pm, pmp, bounds, tdoa, omega
+    return scenes.make_c4(scene_index=0, num_frames=num_frames)
 
 
-def config_dict(F, J, P, Kb, total_samples):
+def omega_of(frame_length):
+    return 2.0 * np.pi * np.arange(frame_length // 2) * FS / frame_length
+
+
+def canonical(mic_pos):
+    """Pair rows and TDOA bounds in the reference's canonical order
+    (geometry.py:141-176), from the package's own geometry helpers."""
+    from paper_2012_09499_b200.geometry import enumerate_pairs
+
+    pairs = enumerate_pairs(mic_pos, C_SOUND)
+    return (np.array([p.index_m for p in pairs], np.int32),
+            np.array([p.index_m_prime for p in pairs], np.int32),
+            np.array([p.tdoa_bound for p in pairs]))
+
+
+def build_plan(scene, n_aux, dev, weights="auto", conventional=True):
+    """Product plan from the scene geometry (device TDOAs and splits)."""
+    from paper_2012_09499_b200.plan import SrpPlan
+
+    return SrpPlan.from_geometry(scene.mic_pos, scene.grid, omega_of(scene.frame_length),
+                                 speed_of_sound=C_SOUND, sample_period=T, n_aux=n_aux,
+                                 weights=weights, conventional=conventional, device=dev)
+
+
+def c4_config(F, plan, world):
     return {
-        "workload": "C2 (BASELINE configs[1]): UCA M=8 r=0.1 m, fs=16 kHz, frame 1024/hop 512, "
-                    "10 s white source + 6 image sources + diffuse noise 5 dB, 50x50x20 grid",
-        "frames": F, "candidates": J, "pairs": P, "bins": Kb, "n_aux": N_AUX,
-        "lattice_samples": total_samples, "value_path": "approx (GCC-PHAT + lattice + interp "
-        "+ argmax)", "l2": "flushed before every timed step (256 MiB write)",
-        "parallelism": "frame-parallel replicas (one seeded scene per rank)",
+        "workload": "C4 (BASELINE configs[3], the largest single-GPU config): M=32 seeded "
+                    "uniform mics in a 6x5x3 m room, 2 equal-power white sources, 10 dB SNR, "
+                    "frame 1024 / hop 512, 4096 frames, 120x100x50 grid",
+        "frames": F, "candidates": plan.J, "pairs": plan.P, "bins": plan.Kb, "n_aux": plan.n_aux,
+        "lattice_samples": plan.total_samples, "weights": plan.weight_mode,
+        "value_path": "approx (GCC-PHAT fused into the lattice IDFT -> tcgen05 sinc "
+                      "interpolation, weights generated in TMEM -> maps + fused argmax)",
+        "l2": "flushed before every timed step (256 MiB write); inputs also exceed L2",
+        "parallelism": (f"frame-sharded over {world} GPUs (contiguous frame ranges, geometry "
+                        "replicated, NCCL all-gather of maps + argmax in every step)"
+                        if world > 1 else "1 GPU"),
     }
 
 
 # -------------------------------------------------------------- clocks probe
 class ClockSampler:
     """SM clock and clock-event (throttle) reasons sampled every ~1 ms during
-    the timed regions (NVML; nvidia-smi -lms 100 as the fallback).  Call
+    the timed regions (NVML; nvidia-smi as the fallback).  Call
     resume()/pause() around each timed region; stop() summarises."""
 
     REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
@@ -164,62 +199,155 @@ class ClockSampler:
             return None
 
 
-# --------------------------------------------------------------- CPU baseline
-def cpu_sample(scene, pm, pmp, bounds, tdoa, omega, n_frames, conv_frames):
-    """Time the reference algorithm (oracle port) on host cores.
+# --------------------------------------------------------------- CPU samples
+def _cpu_worker(job):
+    """One process of the CPU sample (1 BLAS thread when sharded): GCC-PHAT +
+    lattice per frame, interpolation and conventional over a candidate
+    subset.  Returns per-stage seconds."""
+    from oracle import srp_oracle as O
 
-    approx: cross_spectrum + build_gcc_lattice + srp_approx + argmax per frame
-    (sinc table precomputed and excluded, as the reference does,
-    experiment.py:339-344); conventional: cross_spectrum +
-    srp_conventional_frames + argmax (phase generation included, srp.py:421).
-    Returns f.c/s for both paths.
+    Y, pm, pmp, bounds, omega, tdoa_sub, tdoa_conv, n_aux = job
+    _, weights = O.sinc_table(tdoa_sub, bounds, T, n_aux)  # untimed precompute (as the reference)
+    t_lat = t_int = t_conv = 0.0
+    psis = []
+    for f in range(Y.shape[0]):
+        t0 = time.perf_counter()
+        psi, _ = O.cross_spectrum(Y[f], pm, pmp)
+        _, rows = O.gcc_lattice(psi, omega, bounds, T, n_aux)
+        t1 = time.perf_counter()
+        O.argmax(O.approx_map(weights, rows))
+        t2 = time.perf_counter()
+        t_lat += t1 - t0
+        t_int += t2 - t1
+        psis.append(psi)
+    t0 = time.perf_counter()
+    maps = O.conventional_frames(np.stack(psis), omega, tdoa_conv)
+    [O.argmax(m) for m in maps]
+    t_conv = time.perf_counter() - t0
+    return t_lat, t_int, t_conv
+
+
+def cpu_sample(scene, n_frames, n_cands, n_aux, procs=1, pool=None, conv_cands=4096):
+    """The reference algorithm (oracle port) on the host cores, on a bounded
+    sample of the workload, extrapolated to the full J x F.
+
+    approx: cross_spectrum + build_gcc_lattice per frame (J-independent) and
+    srp_approx + argmax over ``n_cands`` candidates (sinc table precomputed
+    and excluded, as the reference does, experiment.py:339-344); the full-J
+    cost per frame is t_lattice + J * t_interp / n_cands (cost is exactly
+    linear in J, srp.py:343-344).  conventional: srp_conventional_frames
+    (phase generation included, srp.py:421) over the candidate subset,
+    linear in J x F (srp.py:423-424).  ``procs`` > 1 shards the frames over
+    that many processes with one BLAS thread each (experiment.py:631-641);
+    procs = 1 is one process with all BLAS threads.
     """
     from oracle import srp_oracle as O
 
-    J = tdoa.shape[0]
-    Y = scene.Y.astype(np.complex128)
-    _, w = O.sinc_table(tdoa, bounds, T, N_AUX)  # untimed precompute
+    Y = scene.Y[: max(1, n_frames * procs)].astype(np.complex128)
+    pm, pmp, bounds = canonical(scene.mic_pos)
+    pairs = list(zip(pm.tolist(), pmp.tolist()))
+    J = scene.grid.shape[0]
+    sub = np.random.default_rng(7).choice(J, size=min(n_cands, J), replace=False)
+    sub.sort()
+    tdoa_sub = O.tdoa_table_nearfield(scene.mic_pos, scene.grid[sub], pairs, C_SOUND)
+    csub = np.sort(np.random.default_rng(8).choice(J, size=min(conv_cands, J), replace=False))
+    tdoa_conv = O.tdoa_table_nearfield(scene.mic_pos, scene.grid[csub], pairs, C_SOUND)
+    omega = omega_of(scene.frame_length)
+    jobs = [(Y[i * n_frames:(i + 1) * n_frames], pm, pmp, bounds, omega, tdoa_sub, tdoa_conv,
+             n_aux) for i in range(procs)]
     t0 = time.perf_counter()
-    for f in range(n_frames):
-        psi, _ = O.cross_spectrum(Y[f], pm, pmp)
-        _, rows = O.gcc_lattice(psi, omega, bounds, T, N_AUX)
-        O.argmax(O.approx_map(w, rows))
-    t_approx = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    psis = np.stack([O.cross_spectrum(Y[f], pm, pmp)[0] for f in range(conv_frames)])
-    maps = O.conventional_frames(psis, omega, tdoa, candidate_chunk=8192)
-    [O.argmax(m) for m in maps]
-    t_conv = time.perf_counter() - t0
-    return n_frames * J / t_approx, conv_frames * J / t_conv, t_approx, t_conv
+    if procs == 1:
+        res = [_cpu_worker(jobs[0])]
+    elif pool is not None:
+        res = pool.map(_cpu_worker, jobs)
+    else:
+        with single_thread_pool(procs) as pl:
+            res = pl.map(_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    t_lat = float(np.mean([r[0] for r in res])) / n_frames     # s per frame per process
+    t_int = float(np.mean([r[1] for r in res])) / (n_frames * len(sub))  # s per f.c
+    t_conv = float(np.mean([r[2] for r in res])) / (n_frames * len(csub))
+    approx = procs / (t_lat / J + t_int)                        # f.c/s, all processes
+    conv = procs / t_conv
+    return {"approx": approx, "conventional": conv, "wall_s": wall, "procs": procs,
+            "s_per_frame_lattice": t_lat, "s_per_fc_interp": t_int, "s_per_fc_conv": t_conv,
+            "frames": n_frames * procs, "cands": int(len(sub)), "conv_cands": int(len(csub))}
+
+
+class single_thread_pool:
+    """Process pool whose workers run numpy with one BLAS thread (spawned
+    with OPENBLAS/OMP_NUM_THREADS=1), as the reference's scene-level
+    ProcessPoolExecutor (experiment.py:631-641)."""
+
+    def __init__(self, procs):
+        self.procs = procs
+
+    def __enter__(self):
+        import multiprocessing as mp
+
+        old = {v: os.environ.get(v) for v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS")}
+        for v in old:
+            os.environ[v] = "1"
+        try:
+            self.pool = mp.get_context("spawn").Pool(self.procs)
+        finally:
+            for v, x in old.items():
+                if x is None:
+                    os.environ.pop(v, None)
+                else:
+                    os.environ[v] = x
+        return self.pool
+
+    def __exit__(self, *exc):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_baseline(scene, args, n_aux):
+    """Settings (i) one process, all BLAS threads and (ii) frames sharded
+    over the host cores with one BLAS thread each; the better is reported."""
+    cores = os.cpu_count() or 1
+    one = cpu_sample(scene, args.cpu_frames, args.cpu_cands, n_aux, procs=1,
+                     conv_cands=args.cpu_conv_cands)
+    shard = cpu_sample(scene, 1, args.cpu_cands, n_aux, procs=min(cores, 16),
+                       conv_cands=args.cpu_conv_cands)
+    best = max((one, shard), key=lambda r: r["approx"])
+    return best, one, shard, cores
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return  # the reference arm runs on rank 0 only
-    scene, pm, pmp, bounds, tdoa, omega = workload(0)
-    nf = args.cpu_frames or scene.Y.shape[0]
-    cf = 1
-    for _ in range(args.warmup):
-        cpu_sample(scene, pm, pmp, bounds, tdoa, omega, 1, 1)
-    vals, convs, ts = [], [], []
-    for _ in range(args.steps):
-        a, c, ta, tc = cpu_sample(scene, pm, pmp, bounds, tdoa, omega, nf, cf)
-        vals.append(a)
-        convs.append(c)
-        ts.append(ta)
+    scene = c4_scene(max(args.cpu_frames, 16))
+    n_aux = 2
+    cores = os.cpu_count() or 1
+    procs = min(cores, 16)
+    vals, convs, walls = [], [], []
+    with single_thread_pool(procs) as pool:
+        for _ in range(max(0, min(args.warmup, 1))):
+            cpu_sample(scene, 1, 64, n_aux, procs=procs, pool=pool, conv_cands=64)
+        for _ in range(args.steps):
+            r = cpu_sample(scene, 1, args.cpu_cands, n_aux, procs=procs, pool=pool,
+                           conv_cands=args.cpu_conv_cands)
+            vals.append(r["approx"])
+            convs.append(r["conventional"])
+            walls.append(r["wall_s"])
     value = float(np.median(vals))
-    cores = os.cpu_count()
-    sample = (f"{nf} C2 frames x {tdoa.shape[0]} candidates per step (approx); {cf} frame "
-              "per step (conventional); numpy/OpenBLAS, all host threads")
+    J = scene.grid.shape[0]
+    sample = (f"per step: {procs} C4 frames (one per process, 1 BLAS thread each, "
+              f"experiment.py:631-641 sharding) x lattice of all 496 pairs + interpolation "
+              f"over {args.cpu_cands} and conventional over {args.cpu_conv_cands} of the {J} "
+              "candidates; full-J cost "
+              "extrapolated linearly (srp.py:343-344, 423-424); sinc table precomputed")
     out = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * float(np.median(ts)), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(scene.Y.shape[0], tdoa.shape[0], len(pm), omega.size,
-                              int(sum(2 * (int(np.floor(b / T)) + N_AUX) + 1 for b in bounds))),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "ms_per_step": 1e3 * float(np.median(walls)), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C4 (BASELINE configs[3]), as the GPU arm", "frames": 4096,
+                   "candidates": J, "n_aux": n_aux},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "conventional": {"value": float(np.median(convs)), "unit": UNIT},
@@ -231,263 +359,409 @@ def run_reference(args):
 FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # SIMT FMA pipe, nominal
 
 
-def roofline_entry(kms, plan, F, J, P, Kb, peaks, path):
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+def roofline_entry(kms, plan, F, path, peaks, traffic_file="r2_traffic.json"):
     """Roofline of the dominant kernel of a step, from its CUDA-event time.
 
-    Algorithmic work per unit: K4 2*sum(T_p) flops and K2
-    4*P*Kb flops per frame.candidate; K3 4*sum(T_p)*Kb flops per frame.
-    Tensor-core kernels are rated against the fp32-accurate rate derived
-    from the measured bf16 peak: 3xFP16 = fp16 (= bf16) rate / 3 MMAs per
-    product, 3xTF32 = bf16 / 2 (TF32 rate) / 3.
+    Algorithmic work per unit: K4 2 sum(T_p) flops and K2
+    4 P Kb flops per frame.candidate.  Tensor-core kernels are rated against
+    the fp32-accurate rate derived from the measured bf16 peak (fp16 rate =
+    bf16 rate): 3xFP16 = bf16 / 3 MMAs per product; 3xTF32 = bf16 / 2 / 3.
     """
     bf16 = peaks.get("bf16_tflops") or 1590.0
-    names = {"approx": ("srpb_interp_tc16", "srpb_interp_tc", "srpb_interp",
-                        "srpb_interp_onthefly"),
+    names = {"approx": ("srpb_interp_tc16_onthefly", "srpb_interp_tc16", "srpb_interp_tc",
+                        "srpb_interp", "srpb_interp_onthefly"),
              "conventional": ("srpb_conventional_tc16", "srpb_conventional_tc",
                               "srpb_conventional", "srpb_conventional_general")}[path]
     name = next((n for n in names if n in kms), None)
     if name is None:
         return None
-    per_unit = 2.0 * plan.total_samples if path == "approx" else 4.0 * P * Kb
-    achieved = per_unit * F * J / (kms[name] * 1e-3) / 1e12
-    tc16 = name.endswith("_tc16")
+    per_unit = 2.0 * plan.total_samples if path == "approx" else 4.0 * plan.P * plan.Kb
+    achieved = per_unit * F * plan.J / (kms[name] * 1e-3) / 1e12
+    tc16 = "_tc16" in name
     tc = tc16 or name.endswith("_tc")
-    tc_peak = bf16 / 3.0 if tc16 else bf16 / 2.0 / 3.0
-    src = ("measured bf16 burst %.1f TF/s (MEASURED_PEAKS.json; fp16 rate = bf16 rate) / 3 "
-           "(3xFP16 passes)" % bf16) if tc16 else (
-           "measured bf16 burst %.1f TF/s (MEASURED_PEAKS.json) / 2 (TF32 rate) / 3 "
-           "(3xTF32 passes)" % bf16)
+    peak = bf16 / 3.0 if tc16 else (bf16 / 6.0 if tc else FP32_NOMINAL_TFLOPS)
     entry = {
-        "kernel": name, "bound": "tensor" if tc else "fp32", "achieved": achieved,
-        "peak": tc_peak if tc else FP32_NOMINAL_TFLOPS, "unit": "TFLOP/s", "traffic": None,
-        "peak_source": src if tc else
-                       "nominal FP32 SIMT 148 SM x 128 lanes x 2 x 1.965 GHz (none measured)",
-        "flops_per_unit": per_unit, "units_per_launch": F * J, "kernel_ms": kms[name],
+        "kernel": name, "bound": "tensor" if tc else "fp32", "achieved": achieved, "peak": peak,
+        "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+        "peak_source": ("measured bf16 burst %.1f TF/s (MEASURED_PEAKS.json; fp16 rate = bf16 "
+                        "rate) / 3 (3xFP16 passes)" % bf16) if tc16 else (
+                        "measured bf16 / 2 (TF32) / 3 (3xTF32)" if tc else "nominal FP32 SIMT"),
+        "flops_per_unit": per_unit, "units_per_launch": F * plan.J, "kernel_ms": kms[name],
         "kernels_ms": kms,
+        "timing": "CUDA events around each launch on the launching stream, un-captured "
+                  "step queued behind a GPU sleep",
     }
-    entry["frac"] = achieved / entry["peak"]
-    # DRAM bytes per launch from the committed ncu --set full capture
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", traffic_file)) as fh:
             tr = json.load(fh)
-        if name in tr:
-            entry["traffic"] = tr[name]
-            entry["traffic_unit"] = "bytes/launch (profiles/r1_traffic.json)"
+        key = f"{name}@{path}"
+        if key in tr or name in tr:
+            entry["traffic"] = tr.get(key, tr.get(name))
+            entry["traffic_unit"] = f"DRAM bytes/launch (profiles/{traffic_file}, ncu --set full)"
     except (OSError, ValueError):
         pass
     return entry
 
 
+# ------------------------------------------------------------------ parity
+def parity_block(maps_dev, am_dev, scene, plan, frames, n_cands, path, n_aux, seed=11):
+    """GPU maps vs the oracle (fp64 reference algorithm) on ``frames`` x a
+    seeded candidate subset: worst per-frame rel-L2 (tolerance 1e-5),
+    argmax agreement over the subset, the reference's smallest top-2 margin,
+    and the full-J argmax consistency of the fused kernel argmax with the
+    stored maps."""
+    import torch
+
+    from oracle import srp_oracle as O
+
+    J = plan.J
+    frames = [int(f) for f in frames]
+    if n_cands >= J:
+        sub = np.arange(J)
+    else:
+        sub = np.sort(np.random.default_rng(seed).choice(J, size=n_cands, replace=False))
+    idx = torch.as_tensor(sub, device=maps_dev.device)
+    g = maps_dev[frames][:, idx].double().cpu().numpy()
+    full_am = am_dev[frames].cpu().numpy()
+    rows_am = torch.argmax(maps_dev[frames], dim=1).cpu().numpy()  # lowest index among maxima
+    pm, pmp, bounds = canonical(scene.mic_pos)
+    pairs = list(zip(pm.tolist(), pmp.tolist()))
+    omega = omega_of(scene.frame_length)
+    Y = scene.Y[frames].astype(np.complex128)
+    psi = np.stack([O.cross_spectrum(Y[i], pm, pmp)[0] for i in range(len(frames))])
+    ref = np.zeros((len(frames), len(sub)))
+    chunk = 256 if path == "approx" else 4096
+    if path == "approx":
+        lattices = [O.gcc_lattice(psi[i], omega, bounds, T, n_aux)[1] for i in range(len(frames))]
+    for lo in range(0, len(sub), chunk):
+        tdoa = O.tdoa_table_nearfield(scene.mic_pos, scene.grid[sub[lo:lo + chunk]], pairs, C_SOUND)
+        if path == "approx":
+            _, w = O.sinc_table(tdoa, bounds, T, n_aux)
+            for i in range(len(frames)):
+                ref[i, lo:lo + chunk] = O.approx_map(w, lattices[i])
+        else:
+            ref[:, lo:lo + chunk] = O.conventional_frames(psi, omega, tdoa)
+    errs = np.linalg.norm(g - ref, axis=1) / np.maximum(np.linalg.norm(ref, axis=1), 1e-300)
+    am_ref = np.argmax(ref, axis=1)
+    am_gpu = np.argmax(g, axis=1)
+    srt = np.sort(ref, axis=1)
+    margin = (srt[:, -1] - srt[:, -2]) / np.maximum(np.max(np.abs(ref), axis=1), 1e-300)
+    return {
+        "oracle": "oracle/srp_oracle.py (fp64 restatement of srpfast, pinned to golden vectors "
+                  "of the reference itself)",
+        "frames": frames, "candidates": int(len(sub)),
+        "candidate_subset": "all" if len(sub) == J else f"seeded random {len(sub)} of {J}",
+        "rel_l2_worst": float(errs.max()), "rel_l2_tolerance": 1e-5,
+        "argmax_mismatches": int(np.sum(am_ref != am_gpu)),
+        "min_top2_margin": float(margin.min()),
+        "fused_argmax_equals_map_argmax": bool(np.array_equal(full_am, rows_am)),
+        "pass": bool(errs.max() <= 1e-5 and np.all(am_ref == am_gpu)
+                     and np.array_equal(full_am, rows_am)),
+    }
+
+
 # ------------------------------------------------------------------ our arm
+class KernelTimer:
+    """CUDA events around each main kernel launch (``SrpPlan.kernel_timer``
+    hook), recorded on the launching stream."""
+
+    def __init__(self, stream):
+        import torch
+
+        self.torch, self.stream = torch, stream
+        self.pending, self.pairs = {}, []
+
+    def _ev(self):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        return e
+
+    def before(self, name):
+        self.pending[name] = self._ev()
+
+    def after(self, name):
+        self.pairs.append((name, self.pending.pop(name), self._ev()))
+
+    def totals(self):
+        out = {}
+        for name, a, b in self.pairs:
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
+
+
+class Timer:
+    """W warm-ups + K timed steps, CUDA events on the launching stream, L2
+    flushed before each timed step, barrier + synchronize around the timed
+    region, max over ranks; clocks sampled inside."""
+
+    def __init__(self, dev, world, clocks):
+        import torch
+
+        self.torch, self.dev, self.world, self.clocks = torch, dev, world, clocks
+        self.flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > L2
+
+    def __call__(self, fn, steps, warmup, plan=None, profile=False):
+        torch = self.torch
+        import torch.distributed as dist
+
+        stream = torch.cuda.current_stream(self.dev)
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        if self.world > 1:
+            dist.barrier()
+        kt = KernelTimer(stream) if profile else None
+        if plan is not None:
+            plan.kernel_timer = kt
+        tot = 0.0
+        self.clocks.resume()
+        for _ in range(steps):
+            self.flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            if profile:  # the host enqueues every launch before the first kernel starts
+                torch.cuda._sleep(2_000_000)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        torch.cuda.synchronize()
+        self.clocks.pause()
+        if plan is not None:
+            plan.kernel_timer = None
+        ms = tot / max(steps, 1)
+        if self.world > 1:
+            t = torch.tensor([ms], device=self.dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        kms = {k: v / steps for k, v in kt.totals().items()} if kt else {}
+        return ms, kms
+
+
+def sweep_lines(timer, dev, args):
+    """Driver-visible lines for the other BASELINE configs (graph replay,
+    inputs resident, 2 warm-ups + a few timed steps each)."""
+    import torch
+
+    from paper_2012_09499_b200 import scenes
+
+    out = {}
+    # C2 (configs[1]): N_aux {0, 2, 4}, 311 frames x 50k candidates
+    sc = scenes.make_c2()
+    Y = torch.from_numpy(sc.Y).to(dev)
+    c2 = {}
+    for n_aux in (0, 2, 4):
+        plan = build_plan(sc, n_aux, dev, weights="stored", conventional=(n_aux == 4))
+        cap = plan.capture(Y.shape[0], Y.shape[1], "approx")
+        cap.Y.copy_(Y)
+        ms, _ = timer(cap.replay, 10, 2)
+        c2[f"approx_naux{n_aux}"] = {"value": Y.shape[0] * plan.J / (ms * 1e-3), "ms": ms,
+                                     "lattice_samples": plan.total_samples, "steps": 10}
+        if n_aux == 4:
+            capc = plan.capture(Y.shape[0], Y.shape[1], "conventional")
+            capc.Y.copy_(Y)
+            ms, _ = timer(capc.replay, 5, 2)
+            c2["conventional"] = {"value": Y.shape[0] * plan.J / (ms * 1e-3), "ms": ms, "steps": 5}
+            del capc
+        del cap, plan
+    out["C2"] = {"frames": int(Y.shape[0]), "candidates": 50000, "unit": UNIT, **c2}
+    del Y
+    torch.cuda.empty_cache()
+    # C3 (configs[2]): N_aux 0..8, 936 frames x 500k candidates
+    sc = scenes.make_c3()
+    Y = torch.from_numpy(sc.Y).to(dev)
+    c3 = {}
+    for n_aux in range(9):
+        plan = build_plan(sc, n_aux, dev, weights="stored", conventional=(n_aux == 0))
+        cap = plan.capture(Y.shape[0], Y.shape[1], "approx")
+        cap.Y.copy_(Y)
+        ms, _ = timer(cap.replay, 5, 2)
+        c3[f"approx_naux{n_aux}"] = {"value": Y.shape[0] * plan.J / (ms * 1e-3), "ms": ms,
+                                     "lattice_samples": plan.total_samples, "steps": 5}
+        if n_aux == 0:
+            capc = plan.capture(Y.shape[0], Y.shape[1], "conventional")
+            capc.Y.copy_(Y)
+            ms, _ = timer(capc.replay, 3, 1)
+            c3["conventional"] = {"value": Y.shape[0] * plan.J / (ms * 1e-3), "ms": ms, "steps": 3}
+            del capc
+        del cap, plan
+        torch.cuda.empty_cache()
+    out["C3"] = {"frames": int(Y.shape[0]), "candidates": 500000, "unit": UNIT, **c3}
+    del Y
+    torch.cuda.empty_cache()
+    # C5 (configs[4]): batch {1, 16, 256, 4096, 65536}, 200k candidates, N_aux 4
+    sc = scenes.make_c5(65536)
+    plan = build_plan(sc, 4, dev, weights="stored")
+    c5 = {}
+    for B in (1, 16, 256, 4096, 65536):
+        big = B == 65536
+        Yb = torch.from_numpy(sc.Y[:B]).to(dev)
+        row = {}
+        for path in ("approx", "conventional"):
+            cap = plan.capture(B, 8, path, maps=not big)
+            cap.Y.copy_(Yb)
+            steps = 10 if B <= 256 else 3
+            ms, _ = timer(cap.replay, steps, 2 if B <= 4096 else 1)
+            row[path] = {"ms": ms, "value": B * plan.J / (ms * 1e-3), "steps": steps,
+                         "maps": not big}
+            del cap
+            torch.cuda.empty_cache()
+        c5[str(B)] = row
+        del Yb
+    out["C5"] = {"candidates": plan.J, "n_aux": 4, "unit": UNIT,
+                 "note": "latency = ms per batch (CUDA-graph replay, inputs resident); batch "
+                         "65536 argmax-only (maps not materialised)", "batches": c5}
+    del plan
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2012_09499_b200 import _native
-    from paper_2012_09499_b200.plan import SrpPlan
+    from paper_2012_09499_b200.distributed import frame_ranges, gather_frames
+    from paper_2012_09499_b200.pipeline import ChunkedRunner
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but {torch.cuda.device_count()} GPUs")
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-
-    scene, pm, pmp, bounds, tdoa, omega = workload(rank)
-    plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=N_AUX, weights="stored",
-                   device=dev)
-    F, J, P, Kb = scene.Y.shape[0], plan.J, plan.P, plan.Kb
-    Y_host = torch.from_numpy(scene.Y).pin_memory()
-    Y = Y_host.to(dev)
-    maps_host = torch.empty((F, J), dtype=torch.float32).pin_memory()
-    am_host = torch.empty((F,), dtype=torch.int32).pin_memory()
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > L2
-    stream = torch.cuda.current_stream(dev)
-
-    def ev():
-        return torch.cuda.Event(enable_timing=True)
-
-    class KernelTimer:
-        """CUDA events around each main kernel launch (plan.kernel_timer hook),
-        recorded on the launching stream."""
-
-        def __init__(self):
-            self.pending, self.pairs = {}, []
-
-        def before(self, name):
-            e = ev()
-            e.record(stream)
-            self.pending[name] = e
-
-        def after(self, name):
-            e = ev()
-            e.record(stream)
-            self.pairs.append((name, self.pending.pop(name), e))
-
-        def totals(self):
-            out = {}
-            for name, a, b in self.pairs:
-                out[name] = out.get(name, 0.0) + a.elapsed_time(b)
-            return out
-
-    # the product step: one CUDA-graph replay of plan.run (inputs resident)
-    from paper_2012_09499_b200.pipeline import ChunkedRunner
-
-    graphs = {path: plan.capture(F, Y.shape[1], path) for path in ("approx", "conventional")}
-    for g in graphs.values():
-        g.Y.copy_(Y)
-    # chunks: K4 is cheap, so many small chunks start the maps' D2H early;
-    # K2 keeps one 160-frame tile per chunk (its phase generation is paid
-    # per candidate tile, independent of the frames in it)
-    runners = {"approx": ChunkedRunner(plan, F, Y.shape[1], "approx", chunks=args.e2e_chunks),
-               "conventional": ChunkedRunner(plan, F, Y.shape[1], "conventional", chunks=2)}
-    # argmax-only serving (maps never leave the device; the drop-in's SrpMap
-    # fetches values lazily, so a caller reading only argmax_candidate pays this)
-    runner_am = ChunkedRunner(plan, F, Y.shape[1], "approx", chunks=args.am_chunks, maps=False)
-
-    # audio-input end to end (SURVEY 8(f) rank 1): pinned host audio of the
-    # C2 shape (8 x 160,000 samples -> the same 311 frames), K0 STFT inside
-    # the captured chunks
-    L_audio = (F - 1) * (2 * Kb // 2) + 2 * Kb
-    x_host = torch.from_numpy(np.random.default_rng(rank).standard_normal(
-        (Y.shape[1], L_audio)).astype(np.float32)).pin_memory()
-    # streaming localisation (audio in, per-frame argmax out; maps stay on
-    # the device): the smallest host traffic the API allows
-    runner_audio_am = ChunkedRunner(plan, F, Y.shape[1], "approx", chunks=args.audio_am_chunks, maps=False,
-                                    audio=(2 * Kb, Kb, "sqrt_hann"))
-    runner_audio = ChunkedRunner(plan, F, Y.shape[1], "approx", chunks=args.e2e_chunks,
-                                 audio=(2 * Kb, Kb, "sqrt_hann"))
-
-    def step(path):
-        return graphs[path].replay()
-
-    def e2e_audio_step(path):
-        runner_audio.run(x_host, maps_host, am_host)
-
-    def eager_step(path):
-        # per-kernel device times (plan.kernel_timer events) come from the
-        # un-captured step; timed() first queues a GPU sleep so the host has
-        # enqueued every launch before the first kernel starts and the
-        # events bracket back-to-back kernels, not host gaps
-        return plan.run(Y, path)
-
-    def e2e_step(path):
-        runners[path].run(Y_host, maps_host, am_host)
-
-    def e2e_argmax_step(path):
-        runner_am.run(Y_host, None, am_host)
-
-    def e2e_audio_argmax_step(path):
-        runner_audio_am.run(x_host, None, am_host)
-
-    def timed(fn, path, profile=False):
-        for _ in range(args.warmup):
-            fn(path)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        tot = 0.0
-        kt = KernelTimer() if profile else None
-        plan.kernel_timer = kt
-        launches0 = _native.launch_count()
-        clocks.resume()
-        for _ in range(args.steps):
-            flush.zero_()
-            a, b = ev(), ev()
-            if profile:
-                torch.cuda._sleep(2_000_000)
-            a.record(stream)
-            fn(path)
-            b.record(stream)
-            b.synchronize()
-            tot += a.elapsed_time(b)
-        torch.cuda.synchronize()
-        clocks.pause()
-        plan.kernel_timer = None
-        launches = _native.launch_count() - launches0
-        ms = tot / args.steps
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-            dist.barrier()
-        kms = {k: v / args.steps for k, v in kt.totals().items()} if kt else {}
-        return ms, kms, launches
-
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     clocks = ClockSampler(local)
     clocks.start()
-    ms_a, _, _ = timed(step, "approx")
-    ms_c, _, _ = timed(step, "conventional")
-    _, kms_a, _ = timed(eager_step, "approx", profile=True)
-    _, kms_c, _ = timed(eager_step, "conventional", profile=True)
-    launches_a, launches_c = graphs["approx"].launches, graphs["conventional"].launches
-    e2e_a, _, _ = timed(e2e_step, "approx")
-    e2e_c, _, _ = timed(e2e_step, "conventional")
-    e2e_x, _, _ = timed(e2e_audio_step, "approx")
-    e2e_m, _, _ = timed(e2e_argmax_step, "approx")
-    e2e_xm, _, _ = timed(e2e_audio_argmax_step, "approx")
-    clk = clocks.stop()
+    timer = Timer(dev, world, clocks)
+    peaks = load_peaks()
 
-    units = F * J * world
-    value = units / (ms_a * 1e-3)
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            peaks = json.load(fh)
-    except OSError:
-        pass
-    roof_a = roofline_entry(kms_a, plan, F, J, P, Kb, peaks, "approx")
-    roof_c = roofline_entry(kms_c, plan, F, J, P, Kb, peaks, "conventional")
-    h2d = F * scene.Y.shape[1] * Kb * 8
-    d2h = F * J * 4 + F * 4
+    # --- C4: every rank renders the same seeded scene and runs its frames
+    scene = c4_scene(args.frames)
+    F = scene.Y.shape[0]
+    lo, hi = frame_ranges(F, world)[rank]
+    Fl = hi - lo
+    t0 = time.perf_counter()
+    plan = build_plan(scene, 2, dev)
+    torch.cuda.synchronize()
+    plan_s = time.perf_counter() - t0
+    J = plan.J
+    Y_host = torch.from_numpy(scene.Y[lo:hi]).pin_memory()
+    M = Y_host.shape[1]
+    graphs = {}
+    for path in ("approx", "conventional"):
+        g = plan.capture(Fl, M, path)
+        g.Y.copy_(Y_host, non_blocking=True)
+        graphs[path] = g
+    torch.cuda.synchronize()
+
+    def step(path):
+        def run():
+            maps, am = graphs[path].replay()
+            if world > 1:  # results of all ranks on every rank (NVLink all-gather)
+                gather_frames(am.to(torch.int64), F)
+                gather_frames(maps, F)
+        return run
+
+    n0 = _native.launch_count()
+    ms_a, _ = timer(step("approx"), args.steps, args.warmup)
+    launches_a = graphs["approx"].launches
+    ms_c, _ = timer(step("conventional"), args.conv_steps, 1)
+    # per-kernel device times (un-captured eager step, events per launch)
+    _, kms_a = timer(lambda: plan.run(graphs["approx"].Y, "approx"), 1, 0, plan=plan,
+                     profile=True)
+    _, kms_c = timer(lambda: plan.run(graphs["conventional"].Y, "conventional"), 1, 0,
+                     plan=plan, profile=True)
+    del n0
+
+    # --- end to end through the public API: pinned host Y in, pinned host
+    # maps + argmax out, H2D / compute / D2H overlapped over frame chunks
+    sizes = [1280, 1280, 1280, 256] if Fl == 4096 else None
+    maps_host = torch.empty((Fl, J), dtype=torch.float32).pin_memory()
+    am_host = torch.empty((Fl,), dtype=torch.int32).pin_memory()
+    runner = ChunkedRunner(plan, Fl, M, "approx", chunks=4, sizes=sizes)
+    e2e_a, _ = timer(lambda: runner.run(Y_host, maps_host, am_host), args.steps, 1)
+    del runner
+    torch.cuda.empty_cache()
+    runner_c = ChunkedRunner(plan, Fl, M, "conventional", chunks=4, sizes=sizes)
+    e2e_c, _ = timer(lambda: runner_c.run(Y_host, maps_host, am_host), min(2, args.steps), 1)
+    del runner_c
+    torch.cuda.empty_cache()
+    runner_m = ChunkedRunner(plan, Fl, M, "approx", chunks=2, maps=False,
+                             sizes=[2560, 1536] if Fl == 4096 else None)
+    e2e_m, _ = timer(lambda: runner_m.run(Y_host, None, am_host), args.steps, 1)
+    del runner_m
+    torch.cuda.empty_cache()
+
+    units = F * J  # the whole job (strong scaling: every rank holds F / world frames)
+    h2d = Fl * M * plan.Kb * 8
+    d2h = Fl * J * 4 + Fl * 4
     out = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_a, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "fp32",
-        "data": "synthetic (seeded C2 scenes, one per rank; reference publishes no dataset)",
-        "config": config_dict(F, J, P, Kb, plan.total_samples),
+        "metric": METRIC, "value": units / (ms_a * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_a,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
+        "data": "synthetic (seeded C4 scene, scenes.make_c4; the reference publishes no dataset)",
+        "config": c4_config(F, plan, world),
         "e2e": {"value": units / (e2e_a * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_a,
-                "api": "ChunkedRunner (%d frame chunks, H2D / graph-replayed plan.run / "
-                       "D2H on three streams) on pinned host Y -> pinned host maps + "
-                       "argmax" % len(runners["approx"].bounds)},
-        "e2e_audio": {"value": units / (e2e_x * 1e-3), "unit": UNIT,
-                      "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": d2h,
-                      "ms_per_step": e2e_x,
-                      "api": "ChunkedRunner(audio=...) on pinned host audio [8, %d] (seeded "
-                             "white noise of the C2 shape): K0 STFT + approx path per chunk"
-                             % L_audio},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_a, "steps": args.steps,
+                "api": "ChunkedRunner (frame chunks %s, H2D / graph-replayed SrpPlan.run / D2H "
+                       "on three streams): pinned host Y -> pinned host maps + argmax"
+                       % (sizes or 4)},
         "e2e_argmax_only": {"value": units / (e2e_m * 1e-3), "unit": UNIT,
-                            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": F * 4,
-                            "ms_per_step": e2e_m,
-                            "api": ("ChunkedRunner(maps=False, %d chunks): pinned host Y -> "
-                                    "pinned host argmax; maps not materialised" % args.am_chunks)},
-        "e2e_audio_argmax_only": {"value": units / (e2e_xm * 1e-3), "unit": UNIT,
-                                  "h2d_bytes_per_step": int(x_host.numel() * 4),
-                                  "d2h_bytes_per_step": F * 4, "ms_per_step": e2e_xm,
-                                  "api": ("ChunkedRunner(audio=..., maps=False, %d chunks): pinned "
-                                          "host audio -> K0 STFT + approx path -> pinned host "
-                                          "argmax" % args.audio_am_chunks)},
+                            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": Fl * 4,
+                            "ms_per_step": e2e_m, "steps": args.steps,
+                            "api": "ChunkedRunner(maps=False): pinned host Y -> pinned host "
+                                   "argmax; maps never leave the device"},
         "gpu_launches": launches_a,
-        "roofline": roof_a,
-        "conventional": {"value": units / (ms_c * 1e-3), "unit": UNIT, "ms_per_step": ms_c,
-                         "e2e": {"value": units / (e2e_c * 1e-3), "unit": UNIT,
-                                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                                 "ms_per_step": e2e_c},
-                         "gpu_launches": launches_c, "roofline": roof_c},
-        "clocks": clk,
+        "roofline": roofline_entry(kms_a, plan, Fl, "approx", peaks),
+        "conventional": {
+            "value": units / (ms_c * 1e-3), "unit": UNIT, "ms_per_step": ms_c,
+            "steps": args.conv_steps, "warmup": 1,
+            "e2e": {"value": units / (e2e_c * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_c, "steps": min(2, args.steps)},
+            "gpu_launches": graphs["conventional"].launches,
+            "roofline": roofline_entry(kms_c, plan, Fl, "conventional", peaks)},
+        "plan_build_s": plan_s,
         "peaks_used": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained")},
     }
+    if rank == 0 and not args.no_parity:
+        frames = [0, 1, Fl // 2, Fl - 1]
+        out["parity"] = {
+            "approx": parity_block(graphs["approx"].maps, graphs["approx"].argmax, scene, plan,
+                                   frames, 2048, "approx", 2),
+            "conventional": parity_block(graphs["conventional"].maps,
+                                         graphs["conventional"].argmax, scene, plan, frames,
+                                         2048, "conventional", 2),
+        }
+    del graphs
+    torch.cuda.empty_cache()
+    if world == 1 and not args.no_sweeps:
+        out["sweeps"] = sweep_lines(timer, dev, args)
+    out["clocks"] = clocks.stop()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        nf = args.cpu_frames or F
-        a, c, ta, tc = cpu_sample(scene, pm, pmp, bounds, tdoa, omega, nf, args.cpu_conv_frames)
+        best, one, shard, cores = cpu_baseline(scene, args, 2)
         out["cpu_baseline"] = {
-            "value": a, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{nf} C2 frames x {J} candidates (approx path, oracle port of the "
-                      f"reference, {ta:.2f} s); conventional {args.cpu_conv_frames} frames: "
-                      f"{c:.3e} f.c/s ({tc:.2f} s)",
-            "conventional_value": c,
+            "value": best["approx"], "unit": UNIT,
+            "cores": cores if best is shard else os.cpu_count(), "kind": "port",
+            "sample": (f"C4, oracle port of the reference (fp64 numpy): {best['frames']} frames "
+                       f"x lattice of all pairs + interpolation over {best['cands']} candidates, "
+                       f"extrapolated to J={J} (cost linear in J); setting "
+                       f"{'(ii) frames sharded over %d processes, 1 BLAS thread each' % best['procs'] if best is shard else '(i) one process, all BLAS threads'}"
+                       " (the better of (i) and (ii))"),
+            "conventional_value": max(one["conventional"], shard["conventional"]),
+            "settings": {"i_one_process": one, "ii_sharded": shard},
         }
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -495,8 +769,25 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this script under torch.distributed.run
+        import torch
+
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} requested but only {n} CUDA devices are visible")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -193,11 +193,15 @@ __device__ __forceinline__ float rcp_approx_ftz(float x) {
 __device__ __forceinline__ float sinc_spi(float f) {
   return sinpif(f) * 0.318309886183790671538f;  // sin(pi f) / pi
 }
+// Exact-node test: f == 0 (an integer argument, snapped by the reference),
+// and |f| < 1e-30, where sin(pi f) / (pi f) is 1 and sin(pi f) / (pi d) is 0
+// to fp64 rounding (and the fp32 reciprocal would see a denormal).
+__device__ __forceinline__ bool sinc_is_node(float f) { return fabsf(f) < 1e-30f; }
 __device__ __forceinline__ float sinc_weight_fast(int i, float f, float spi, int n) {
   const int d = i - n;
   const float w = __uint_as_float(__float_as_uint(spi * rcp_approx_ftz(static_cast<float>(d) + f)) ^
                                   (static_cast<uint32_t>(d & 1) << 31));
-  return f == 0.0f ? (d == 0 ? 1.0f : 0.0f) : w;
+  return sinc_is_node(f) ? (d == 0 ? 1.0f : 0.0f) : w;
 }
 
 // Programmatic dependent launch on the lattice -> fix-up -> K4 chain (default

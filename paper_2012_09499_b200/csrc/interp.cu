@@ -18,7 +18,7 @@ namespace srpb {
 
 __device__ __forceinline__ float sinc_split(int i, float fr, float sin_pi_f, int n) {
   const int d = i - n;
-  if (fr == 0.0f) return d == 0 ? 1.0f : 0.0f;
+  if (sinc_is_node(fr)) return d == 0 ? 1.0f : 0.0f;
   const float num = (d & 1) ? -sin_pi_f : sin_pi_f;
   return num / (3.14159265358979323846f * (static_cast<float>(d) + fr));
 }

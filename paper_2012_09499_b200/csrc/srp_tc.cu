@@ -88,6 +88,9 @@ struct TcCfg {
   static constexpr bool kEpiStage = kAMode == kAFromTma && kPair;
   static constexpr bool kASmem = kAMode == kAFromTma;
   static constexpr int kKbElems = kF16 ? kTcKBlock16 : kTcKBlock;  // elements per K block
+  // generator modes keep the folded running totals in shared memory
+  // (registers go to the A generator)
+  static constexpr bool kTotSmem = kAMode != kAFromTma;
 };
 
 // Instrumentation build only (make prof -> libsrpb_prof.so, tools/tc_probe.py):
@@ -132,7 +135,12 @@ struct TcParams {
   int dbg;            // experiments only (SRPB_TC_DBG): 1 = A rows mod 2048
   int b_box;          // rows per B TMA box: this CTA's full B buffer (N, or N/2 per pair)
   int kb_per_group;   // TMEM drain period (K blocks)
-  int groups_per_tile;
+  int groups_per_tile;  // num_kb / kb_per_group: the last group also takes the
+                        // remainder (a short tail group could stall the
+                        // generator modes' fold, see enforce_fold_window)
+  int m_units;        // candidate tiles (of 128, or 256 per pair)
+  int m_fast;         // item order: 1 = candidate tile fastest (all CTAs share a
+                      // frame tile's B rows in L2), 0 = frame tile fastest
   float scale;
   float* maps;
   unsigned long long* keys;
@@ -180,10 +188,13 @@ constexpr int kEpiStageBytes = kEpiChunk * 128;
 constexpr int kEpiStageTotal = kEpiWarps * 2 * kEpiStageBytes;
 // other kernels: per-quarter, per-frame tile argmax keys [4][kTcMaxN]
 constexpr int kTileKeysBytes = 4 * kTcMaxN * 8;
+// generator modes: running totals [2 halves x kTcMaxN / 2 columns][128 rows]
+constexpr int kTotSmemBytes = kTcMaxN * kTcM * 4;
 __host__ __device__ inline size_t tc_smem_bytes(int N, bool a_in_smem, bool pair, int stages,
-                                                bool epi_stage = false) {
+                                                bool epi_stage = false, bool tot_smem = false) {
   return 1024 /*align slack*/ + stages * tc_stage_bytes(N, a_in_smem, pair) +
-         (epi_stage ? kEpiStageTotal : kTileKeysBytes) + sizeof(TcSmem);
+         (tot_smem ? kTotSmemBytes : 0) + (epi_stage ? kEpiStageTotal : kTileKeysBytes) +
+         sizeof(TcSmem);
 }
 // TMEM columns: accumulators [0, 2N); K2's A stages (hi 32 + lo 32 columns
 // each) from column 2N: 2N + 64 * 3 <= 512 for N <= 160.
@@ -224,6 +235,21 @@ __device__ __forceinline__ void tc_drain(const TcParams& p, TcSmem* bar, bool re
       mbar_arrive_cluster(acc_empty_addr0 + 8u * b);
     else
       mbar_arrive(&bar->acc_empty[b]);
+  }
+}
+
+// Shared-memory form (generator modes): chunk C folded into this thread's
+// column slice of the running totals, layout [column][row] (lanes hit
+// consecutive banks).
+template <int C>
+__device__ __forceinline__ void tc_drain_chunk16_smem(uint32_t base, float* tot_s, int dbg) {
+  if constexpr (16 * C < kTcMaxN / 2) {
+    if (dbg & 16384) return;  // bound analysis only: no accumulator reads
+    uint32_t r[16];
+    tmem_ld16(base + 16 * C, r);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) tot_s[(16 * C + i) * kTcM] += __uint_as_float(r[i]);
   }
 }
 
@@ -591,11 +617,27 @@ struct PhaseGen {
 // rows of a warp share the column sequence, so pair changes are
 // warp-uniform); the next pair's split is prefetched into registers one
 // pair ahead, hiding its global-load latency.
+//
+// Cost: with d = E - t (E = i + column of lag 0, t the column), a run of 32
+// columns inside one pair needs, per weight, the exact integer-valued
+// denominator part (E - t0) - c, one rounding add of f, one MUFU reciprocal
+// and one multiply by the pair's signed amplitude 2^14 (-1)^E sin(pi f)/pi
+// (the (-1)^c alternation is compile-time) -- done two columns at a time with
+// the packed f32x2 adds/multiplies -- plus the fp16 hi/lo split: ~4 ALU
+// instructions and one MUFU per weight (the per-column pair tracking of a
+// generic column walk cost ~20).  Runs that cross a pair boundary (C4:
+// about one in nine) take one masked pass per pair.  Exact-node rows (f == 0,
+// and |f| < 1e-30, where the reference's sinc is 1 / 0 to fp64 rounding) use
+// amplitude 0 with a half-integer denominator and get their single 2^14
+// written afterwards.
 struct SincGen {
-  int p, next, base, total, P;  // current pair, its end column, column of lag 0
-  int si, nsi;                  // current / prefetched split
-  float sf, spi, nsf;
-  const int2* cols;             // shared: per pair (end column, column of lag 0)
+  int p, end, P;      // current pair, its end column (INT_MAX past the last pair)
+  int E;              // split integer part + column of lag 0: d = E - t
+  float f, amp;       // denominator fraction, signed 2^14 sin(pi f) / pi
+  bool node;          // exact-node row: weight 2^14 at d == 0, else 0
+  int nsi;            // prefetched split of pair p + 1
+  float nsf;
+  const int2* cols;   // shared: per pair (end column, column of lag 0)
 
   __device__ __forceinline__ void fetch(const TcParams& prm, int j, int q) {
     nsi = 0;
@@ -609,43 +651,104 @@ struct SincGen {
   __device__ __forceinline__ void start_tile(const TcParams& prm, int j, const int2* pair_cols) {
     P = prm.P;
     p = -1;
-    next = 0;
+    end = 0;
     cols = pair_cols;
-    total = pair_cols[P - 1].x;
     fetch(prm, j, 0);
   }
 
   __device__ __forceinline__ void advance(const TcParams& prm, int j) {
     ++p;
-    si = nsi;
-    sf = nsf;
-    spi = sinc_spi(sf);
-    const int2 c = cols[p];
-    next = c.x;
-    base = c.y;
-    fetch(prm, j, p + 1);
+    if (p < P) {
+      const int2 c = cols[p];
+      end = c.x;
+      E = nsi + c.y;
+      node = sinc_is_node(nsf);
+      f = node ? 0.5f : nsf;
+      const float a = node ? 0.0f : sinc_spi(nsf) * kF16PhaseScale;
+      amp = (E & 1) ? -a : a;
+      fetch(prm, j, p + 1);
+    } else {  // lattice padding columns: weight 0
+      end = 0x7fffffff;
+      E = 0;
+      node = false;
+      f = 0.5f;
+      amp = 0.0f;
+    }
+  }
+
+  static __device__ __forceinline__ void split2(float2 w, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(w.x, w.y);
+    const float2 hf = __half22float2(h);
+    const float2 r = __fadd2_rn(w, make_float2(-hf.x, -hf.y));  // exact residual
+    const __half2 l = __floats2half2_rn(r.x, r.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
   }
 
   __device__ __forceinline__ void block(const TcParams& prm, int j, int half, int kb,
                                         uint32_t a_hi_tmem, uint32_t a_lo_tmem) {
     uint32_t hi[16], lo[16];
     const int t0 = 64 * kb + 32 * half;
+    // a thread sees 32 of every 64 columns: pairs may end in the skipped half
+    while (t0 >= end) advance(prm, j);  // warp-uniform
+    if (prm.dbg & 2048) {  // bound analysis only: no weight arithmetic
 #pragma unroll
-    for (int c = 0; c < 32; c += 2) {
-      float w[2];
+      for (int i = 0; i < 16; ++i) hi[i] = lo[i] = __float_as_uint(f) + i;
+    } else if (t0 + 32 <= end) {
+      // the whole run lies in pair p
+      // integer-valued d of columns (c, c + 1), stepped by -2 (exact); then
+      // one rounding add of f: = float(d) + f.  (Per-column immediates would
+      // go through a recycled uniform register pair and serialise the loop.)
+      const float Df = static_cast<float>(E - t0);
+      float2 dd = make_float2(Df, Df - 1.0f);
+      const float2 m2 = make_float2(-2.0f, -2.0f);
+      const float2 a2 = make_float2(amp, -amp);
+      const float2 f2 = make_float2(f, f);
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int t = t0 + c + u;
-        // a thread sees 32 of every 64 columns: pairs may end in the skipped half
-        while (t >= next && t < total) advance(prm, j);
-        w[u] = t < total ? sinc_weight_fast(si, sf, spi, t - base) * kF16PhaseScale : 0.0f;
+      for (int c = 0; c < 32; c += 2) {
+        const float2 x = __fadd2_rn(dd, f2);
+        dd = __fadd2_rn(dd, m2);
+        const float2 r = (prm.dbg & 1024) ? x : make_float2(rcp_approx_ftz(x.x), rcp_approx_ftz(x.y));
+        split2(__fmul2_rn(r, a2), hi[c >> 1], lo[c >> 1]);
       }
-      const __half2 h = __floats2half2_rn(w[0], w[1]);
-      const float2 hf = __half22float2(h);
-      const __half2 l = __floats2half2_rn(w[0] - hf.x, w[1] - hf.y);
-      hi[c >> 1] = *reinterpret_cast<const uint32_t*>(&h);
-      lo[c >> 1] = *reinterpret_cast<const uint32_t*>(&l);
+      if (__any_sync(0xffffffffu, node)) {
+        // the node row's d == 0 column in this run as a column bit (selects
+        // per word: an `if (i == cs / 2) hi[i] = ..` becomes an indexed store
+        // and moves hi[] to local memory)
+        const int cs = E - t0;
+        const uint32_t hit = (node && cs >= 0 && cs < 32) ? (1u << cs) : 0u;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint32_t b2 = (hit >> (2 * i)) & 3u;
+          hi[i] = b2 == 0u ? hi[i] : (b2 == 1u ? 0x00007400u : 0x74000000u);
+        }
+      }
+    } else {
+      // the run meets several pairs: one masked 32-column pass per pair (all
+      // indices compile-time, so the weights stay in registers)
+      float w[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) w[c] = 0.0f;
+      int lo_c = 0;
+      for (;;) {  // warp-uniform
+        const int hi_c = min(end - t0, 32);
+        const int cs = E - t0;
+        const float Df = static_cast<float>(cs);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float x = (Df - static_cast<float>(c)) + f;
+          float v = rcp_approx_ftz(x) * ((c & 1) ? -amp : amp);
+          if (node) v = cs == c ? kF16PhaseScale : 0.0f;
+          w[c] = (c >= lo_c && c < hi_c) ? v : w[c];
+        }
+        if (hi_c == 32) break;
+        lo_c = hi_c;
+        advance(prm, j);
+      }
+#pragma unroll
+      for (int c = 0; c < 32; c += 2) split2(make_float2(w[c], w[c + 1]), hi[c >> 1], lo[c >> 1]);
     }
+    if (prm.dbg & 4096) return;  // bound analysis only: no TMEM stores
     tmem_st16(a_hi_tmem + 16 * half, hi);
     tmem_st16(a_lo_tmem + 16 * half, lo);
   }
@@ -660,7 +763,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   // K4: as many smem stages as the tile width leaves room for (narrow tiles,
   // e.g. batch 1, get more look-ahead on the W stream); generator modes:
   // their TMEM A ring
-  const int S = Cfg::kASmem ? p.stages : Cfg::kStages;
+  const int S = p.stages;
   constexpr bool kASmem = Cfg::kASmem;
   constexpr int KBE = Cfg::kKbElems;
   constexpr int kCta = kPair ? 2 : 1;
@@ -674,8 +777,10 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   // address space visible to the compiler: STS/LDS, not generic accesses)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const size_t stage_bytes = tc_stage_bytes(p.N, kASmem, kPair);
-  // [stages][epilogue staging (K4 pairs) | tile argmax keys][barriers]
-  uint8_t* epi_stage = smem + S * stage_bytes;  // 1024-aligned
+  // [stages][running totals (generator modes)][epilogue staging (K4 pairs) |
+  // tile argmax keys][barriers]
+  float* tot_smem = reinterpret_cast<float*>(smem + S * stage_bytes);
+  uint8_t* epi_stage = smem + S * stage_bytes + (Cfg::kTotSmem ? kTotSmemBytes : 0);
   unsigned long long* tile_keys = reinterpret_cast<unsigned long long*>(epi_stage);
   TcSmem* bar = reinterpret_cast<TcSmem*>(epi_stage +
                                           (Cfg::kEpiStage ? kEpiStageTotal : kTileKeysBytes));
@@ -716,8 +821,10 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       piece = q - (q / p.n_pieces) * p.n_pieces;
     }
     Item r;
-    r.m0 = ((b / p.n_tiles) * kCta + rank) * kTcM;
-    r.n0 = (b % p.n_tiles) * p.N;
+    const int mt = p.m_fast ? b % p.m_units : b / p.n_tiles;
+    const int nt = p.m_fast ? b / p.m_units : b % p.n_tiles;
+    r.m0 = (mt * kCta + rank) * kTcM;
+    r.n0 = nt * p.N;
     r.nc = p.N;
     if (piece >= 0) {
       r.n0 += piece * p.n_piece0;
@@ -877,12 +984,12 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
               if (!(p.dbg & 2)) tma_load_2d_pair(a_lo(s), &tmA_lo, fb, kb * KBE, m0);
             }
           } else {
-            mbar_expect_tx(&bar->full[s], tx);
-            for (int r = 0; r < rows; r += p.b_box) {
+            mbar_expect_tx(&bar->full[s], (p.dbg & 256) ? 0u : tx);
+            for (int r = 0; r < rows && !(p.dbg & 256); r += p.b_box) {
               tma_load_2d(b_hi(s) + r * 128, &tmB_hi, &bar->full[s], kb * KBE, nb + r);
               tma_load_2d(b_lo(s) + r * 128, &tmB_lo, &bar->full[s], kb * KBE, nb + r);
             }
-            if (kASmem) {
+            if (kASmem && !(p.dbg & 256)) {
               tma_load_2d(a_hi(s), &tmA_hi, &bar->full[s], kb * KBE, m0);
               tma_load_2d(a_lo(s), &tmA_lo, &bar->full[s], kb * KBE, m0);
             }
@@ -923,7 +1030,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
         const uint32_t idesc = kF16 ? idesc_f16(kTcM * kCta, nc) : idesc_tf32(kTcM * kCta, nc);
         for (int kb = 0; kb < p.num_kb; ++kb, ++kg, ms = ms + 1 == S ? 0 : ms + 1, mph ^= (ms == 0)) {
           const int s = ms;
-          const int gl = kb / p.kb_per_group;                 // group within the tile
+          const int gl = min(kb / p.kb_per_group, p.groups_per_tile - 1);  // group in the tile
           const int g = it * p.groups_per_tile + gl;          // global group
           const int in_group = kb - gl * p.kb_per_group;
           const uint32_t d = tmem + static_cast<uint32_t>((g & 1) * p.N);
@@ -995,7 +1102,8 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
                 }
               }
             }
-            const bool last_in_group = in_group == p.kb_per_group - 1 || kb == p.num_kb - 1;
+            const bool last_in_group =
+                (in_group == p.kb_per_group - 1 && gl < p.groups_per_tile - 1) || kb == p.num_kb - 1;
             if (kPair) {
               mma_commit_pair_mc(&bar->empty[s], 0x3);
               if (last_in_group) mma_commit_pair_mc(&bar->acc_full[g & 1], 0x3);
@@ -1027,7 +1135,11 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // incremental position of group `drained`: its tile, index in the tile,
     // and the global K block index of its last block (no divisions)
     int d_it = 0, d_gl = 0;
-    int d_last_kg = min(p.kb_per_group, p.num_kb) - 1;
+    // last K block of group gl of a tile (the last group takes the remainder)
+    auto group_last = [&](int gl) {
+      return gl == p.groups_per_tile - 1 ? p.num_kb - 1 : (gl + 1) * p.kb_per_group - 1;
+    };
+    int d_last_kg = group_last(0);
     TCP_DECL(c_gen_wait);
     TCP_DECL(c_gen);
     TCP_DECL(c_drain);
@@ -1039,23 +1151,42 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // kb_per_group blocks of slack)
     int d_chunk = -1;  // chunk of group `drained` next to fold (-1: not started)
     uint32_t d_base = 0;
+    // generator modes: this thread's slice of the shared running totals
+    float* tot_s = tot_smem + half * (kTcMaxN / 2) * kTcM + 32 * quarter + lane;
+    if constexpr (Cfg::kTotSmem) {
+#pragma unroll 8
+      for (int i = 0; i < kTcMaxN / 2; ++i) tot_s[i * kTcM] = 0.0f;
+    }
     auto finish_group = [&](const Item& t) {
       if (d_gl == p.groups_per_tile - 1) {
         TCP_T0();
+        if constexpr (Cfg::kTotSmem) {
+#pragma unroll
+          for (int i = 0; i < kTcMaxN / 2; ++i) {
+            tot[i] = tot_s[i * kTcM];
+            tot_s[i * kTcM] = 0.0f;
+          }
+        }
         tc_write_tile(p, tile_keys, t.m0, t.n0, t.nc, quarter, half, lane, tot);
         TCP_ACC(c_write);
         item_release(d_it);
         ++d_it;
         d_gl = 0;
-        d_last_kg = d_it * p.num_kb + min(p.kb_per_group, p.num_kb) - 1;
+        d_last_kg = d_it * p.num_kb + group_last(0);
       } else {
         ++d_gl;
-        d_last_kg = d_it * p.num_kb + min((d_gl + 1) * p.kb_per_group, p.num_kb) - 1;
+        d_last_kg = d_it * p.num_kb + group_last(d_gl);
       }
       ++drained;
     };
+    int f_it = -1;  // item cached by fold_step (item_of divides)
+    Item f_item{};
     auto fold_step = [&]() {
-      const Item t = item_of(item_id(d_it));
+      if (f_it != d_it) {
+        f_item = item_of(item_id(d_it));
+        f_it = d_it;
+      }
+      const Item t = f_item;
       TCP_T0();
       const int b = drained & 1;
       if (d_chunk < 0) {
@@ -1066,11 +1197,11 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
         d_chunk = 0;
       }
       switch (d_chunk) {
-        case 0: tc_drain_chunk16<0>(d_base, tot); break;
-        case 1: tc_drain_chunk16<1>(d_base, tot); break;
-        case 2: tc_drain_chunk16<2>(d_base, tot); break;
-        case 3: tc_drain_chunk16<3>(d_base, tot); break;
-        default: tc_drain_chunk16<4>(d_base, tot); break;
+        case 0: tc_drain_chunk16_smem<0>(d_base, tot_s, p.dbg); break;
+        case 1: tc_drain_chunk16_smem<1>(d_base, tot_s, p.dbg); break;
+        case 2: tc_drain_chunk16_smem<2>(d_base, tot_s, p.dbg); break;
+        case 3: tc_drain_chunk16_smem<3>(d_base, tot_s, p.dbg); break;
+        default: tc_drain_chunk16_smem<4>(d_base, tot_s, p.dbg); break;
       }
       if (++d_chunk == t.nc / 32) {  // group folded: release the buffer
         tc_fence_before();
@@ -1108,10 +1239,10 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
         item_release(d_it);
         ++d_it;
         d_gl = 0;
-        d_last_kg = d_it * p.num_kb + min(p.kb_per_group, p.num_kb) - 1;
+        d_last_kg = d_it * p.num_kb + group_last(0);
       } else {
         ++d_gl;
-        d_last_kg = d_it * p.num_kb + min((d_gl + 1) * p.kb_per_group, p.num_kb) - 1;
+        d_last_kg = d_it * p.num_kb + group_last(d_gl);
       }
       ++drained;
     };
@@ -1259,7 +1390,12 @@ cudaError_t make_map(CUtensorMap* m, const void* base, int rows, int cols, int b
 
 // Frames per tile: N-tiles of <= 160 frames, multiple of 32.
 int pick_n(int F) {
-  const int tiles = (F + kTcMaxN - 1) / kTcMaxN;
+  static int cap = -1;  // SRPB_TC_NMAX (experiments): narrower frame tiles
+  if (cap < 0) {
+    const char* e = getenv("SRPB_TC_NMAX");
+    cap = e ? max(32, min(kTcMaxN, atoi(e) / 32 * 32)) : kTcMaxN;
+  }
+  const int tiles = (F + cap - 1) / cap;
   const int per = (F + tiles - 1) / tiles;
   return (per + 31) / 32 * 32;
 }
@@ -1279,6 +1415,16 @@ bool use_pair(int m_tiles, bool default_on) {
   return env == 1 || default_on;
 }
 
+// on-the-fly K4: CTA pairs unless SRPB_OTF_PAIR=0
+bool use_pair_otf(int m_tiles) {
+  static int env = -2;
+  if (env == -2) {
+    const char* s = getenv("SRPB_OTF_PAIR");
+    env = s ? atoi(s) : -1;
+  }
+  return m_tiles >= 2 && env != 0;
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -1290,12 +1436,16 @@ int num_sms() {
   return n;
 }
 
-// Generator modes fold one 16-column accumulator chunk per generated K block;
-// a drain period shorter than a group's chunk count (N / 32) + 1 would leave
-// the MMA waiting for a buffer the blocked generator warps must release.
+// Generator modes fold one 16-column accumulator chunk per generated K block
+// (c = N / 32 chunks per group), starting S blocks after the group's last
+// block.  The MMA of group g + 2 needs group g folded, and the generator can
+// run at most S blocks ahead of the MMA, so every group after the first must
+// span at least c - 1 blocks or the generator stalls on a stage the MMA never
+// frees (measured: a 2-block tail group hung the kernel).  Groups are at
+// least c + 1 blocks and the tile's remainder joins its last group.
 void enforce_fold_window(TcParams& p) {
   p.kb_per_group = max(p.kb_per_group, p.N / 32 + 1);
-  p.groups_per_tile = (p.num_kb + p.kb_per_group - 1) / p.kb_per_group;
+  p.groups_per_tile = max(1, p.num_kb / p.kb_per_group);
 }
 
 void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16) {
@@ -1303,7 +1453,9 @@ void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16) {
   p.n_tiles = (p.F + p.N - 1) / p.N;
   const int m_tiles = (p.J + kTcM - 1) / kTcM;
   const int cta = pair ? 2 : 1;
-  p.num_items = p.n_tiles * ((m_tiles + cta - 1) / cta);
+  p.m_units = (m_tiles + cta - 1) / cta;
+  p.num_items = p.n_tiles * p.m_units;
+  p.m_fast = 0;
   // tail-wave split: items beyond the last full wave of `units` CTAs (pairs)
   // run as two frame pieces (widths multiples of 32: the epilogue drains
   // 16-column chunks per column half)
@@ -1317,7 +1469,7 @@ void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16) {
   p.kb_per_group = max(f16 ? 2 : 4, kb_per_group);
   p.b_box = getenv("SRPB_TC_BOX16") ? 16 : (pair ? p.N / 2 : p.N);
   p.dbg = getenv("SRPB_TC_DBG") ? atoi(getenv("SRPB_TC_DBG")) : 0;
-  p.groups_per_tile = (p.num_kb + p.kb_per_group - 1) / p.kb_per_group;
+  p.groups_per_tile = max(1, p.num_kb / p.kb_per_group);
 }
 
 template <int kAMode, bool kPair, bool kF16>
@@ -1327,13 +1479,16 @@ cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtens
   using Cfg = TcCfg<kAMode, kPair, kF16>;
   TcParams q = p;
   int S = Cfg::kStages;
-  if (Cfg::kASmem) {  // K4: fill the 227 KB (static 1 KB included)
+  if (!Cfg::kASmem) {  // generator modes: as many TMEM A stages as 2N + 64 S <= 512 allows
+    S = min(kTcMaxStages, (512 - 2 * p.N) / 64);
+    if (getenv("SRPB_TC_GSTAGES")) S = min(S, max(2, atoi(getenv("SRPB_TC_GSTAGES"))));
+  } else {  // K4: fill the 227 KB (static 1 KB included)
     S = kTcMaxStages;
     while (S > Cfg::kStages && tc_smem_bytes(p.N, true, kPair, S, Cfg::kEpiStage) + 1024 > 232448)
       --S;
   }
   q.stages = S;
-  const size_t smem = tc_smem_bytes(p.N, Cfg::kASmem, kPair, S, Cfg::kEpiStage) +
+  const size_t smem = tc_smem_bytes(p.N, Cfg::kASmem, kPair, S, Cfg::kEpiStage, Cfg::kTotSmem) +
                       (kAMode == kASinc ? sizeof(int2) * static_cast<size_t>(p.P) : 0);
   auto kern = srp_tc_kernel<kAMode, kPair, kF16>;
   cudaError_t e = allow_dynamic_smem(kern, static_cast<int>(smem));
@@ -1475,8 +1630,14 @@ cudaError_t launch_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, 
   p.F = F;
   p.J = J;
   p.num_kb = (T_pad + kTcKBlock16 - 1) / kTcKBlock16;
-  finish_params(p, kb_per_group, false, true);
+  // CTA pairs: each SM streams half of the tile's B rows (Xi is re-read from
+  // L2 by every candidate tile; the weights are generated, not loaded)
+  const bool pair = use_pair_otf((J + kTcM - 1) / kTcM);
+  finish_params(p, kb_per_group, pair, true);
   enforce_fold_window(p);
+  // candidate tiles fastest: the CTAs in flight share one frame tile's Xi
+  // rows in L2 instead of streaming every frame tile's
+  p.m_fast = getenv("SRPB_OTF_NFAST") ? 0 : 1;
   p.scale = 1.0f / (kF16PhaseScale * xi_scale);
   p.maps = maps;
   p.keys = keys;
@@ -1489,7 +1650,8 @@ cudaError_t launch_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, 
   cudaError_t e = make_map(&bh, xi_hi, F, T_pad, p.b_box, true);
   if (e == cudaSuccess) e = make_map(&bl, xi_lo, F, T_pad, p.b_box, true);
   if (e != cudaSuccess) return e;
-  return launch_tc<kASinc, false, true>(bh, bl, bh, bl, p, stream);
+  return pair ? launch_tc<kASinc, true, true>(bh, bl, bh, bl, p, stream)
+              : launch_tc<kASinc, false, true>(bh, bl, bh, bl, p, stream);
 }
 
 cudaError_t launch_conventional_tc(const float* psi_hi, const float* psi_lo, int F, int P, int Kb,

@@ -231,26 +231,45 @@ def make_c4(scene_index=0, num_frames=4096, grid_limit=None):
     return Scene("C4", mic, grid, Y.astype(np.complex64), n, n_aux=(2,), sources=srcs)
 
 
+def _c5_block(rng, batch, mic, box, n, omega):
+    """``batch`` independent seeded white-noise scenes (one frame each):
+    a random source in the box, 1/r gain, delay phase ramp, 10 dB white
+    sensor noise (vectorised over the batch)."""
+    srcs = rng.uniform(0.1, 0.9, size=(batch, 3)) * box
+    win = sqrt_hann(n)
+    S = np.fft.rfft(rng.standard_normal((batch, n)) * win[None, :], axis=1)[:, : n // 2]
+    r = np.linalg.norm(mic[None, :, :] - srcs[:, None, :], axis=2)  # (B, M)
+    Y = (S[:, None, :] * np.exp(-1j * r[:, :, None] / C_SOUND * omega[None, None, :])
+         / r[:, :, None])
+    return _add_noise(rng, Y, 10.0, n), srcs
+
+
 def make_c5(batch, scene_index=0, grid_limit=None):
     """C5 (configs[4]): UCA M=8 r=0.1 m, N=1024, 100x100x20 grid (200k)
     over 5x5x2 m, ``batch`` frames of independent seeded white-noise
-    scenes at 10 dB, N_aux=4."""
-    rng = _rng(5, scene_index, batch)
+    scenes at 10 dB, N_aux=4.  Batches above 4096 are rendered in blocks of
+    4096 scenes with their own seeds ``[5, scene_index, batch, block]``
+    (bounded host memory at 65536)."""
     box = np.array([5.0, 5.0, 2.0])
     mic = uca(8, 0.1, [2.5, 2.5, 1.0])
     n = 1024
     omega = _omega(n)
-    srcs = rng.uniform(0.1, 0.9, size=(batch, 3)) * box
-    win = sqrt_hann(n)
-    S = np.fft.rfft(rng.standard_normal((batch, n)) * win[None, :], axis=1)[:, : n // 2]
-    Y = np.zeros((batch, 8, n // 2), dtype=np.complex128)
-    for b in range(batch):
-        Y[b] = _render(rng, mic, [srcs[b]], [1.0], [S[b:b + 1]], omega, C_SOUND)[0]
-    Y = _add_noise(rng, Y, 10.0, n)
+    if batch <= 4096:
+        Y, srcs = _c5_block(_rng(5, scene_index, batch), batch, mic, box, n, omega)
+        Y = Y.astype(np.complex64)
+    else:
+        Y = np.empty((batch, 8, n // 2), dtype=np.complex64)
+        srcs = np.empty((batch, 3))
+        for b, lo in enumerate(range(0, batch, 4096)):
+            hi = min(batch, lo + 4096)
+            rng = np.random.default_rng(np.random.SeedSequence([5, scene_index, batch, b]))
+            yb, sb = _c5_block(rng, hi - lo, mic, box, n, omega)
+            Y[lo:hi] = yb
+            srcs[lo:hi] = sb
     grid = box_grid(100, 100, 20, box)
     if grid_limit is not None:
         grid = grid[:grid_limit]
-    return Scene("C5", mic, grid, Y.astype(np.complex64), n, n_aux=(4,), sources=srcs)
+    return Scene("C5", mic, grid, Y, n, n_aux=(4,), sources=srcs)
 
 
 def random_frames(rng, num_frames, num_mics, num_bins):

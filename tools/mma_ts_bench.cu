@@ -2,13 +2,15 @@
 // A from TMEM (TS, as K2 issues it) vs A from shared memory (SS), N = 160.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/mma_ts_bench tools/mma_ts_bench.cu
 #include <cstdio>
+#include <cstdlib>
 
 #include "../paper_2012_09499_b200/csrc/umma.cuh"
 
 using namespace srpb::umma;
 
 template <bool kTS>
-__global__ void __launch_bounds__(128, 1) bench(int N, int iters, unsigned long long* out) {
+__global__ void __launch_bounds__(128, 1) bench(int N, int iters, unsigned long long* out, int mode) {
+  __shared__ uint64_t sbar[4];
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar;
@@ -23,6 +25,7 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int iters, unsigned long 
   }
   if (warp == 0) tmem_alloc(&tbase, 512);
   if (threadIdx.x == 32) {
+    for (int i = 0; i < 4; ++i) mbar_init(&sbar[i], 1);
     mbar_init(&bar, 1);
     fence_mbar_init();
   }
@@ -42,12 +45,19 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int iters, unsigned long 
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           const uint32_t o = 2 * ks;
-          if (kTS)  // A: 8 TMEM columns (32 bytes of K) per MMA, columns 2N..
+          if (mode == 2) {  // the K4/K2 pattern: lo*hi + hi*lo + hi*hi, A from TMEM
+            const uint32_t ah = tmem + 2 * N + 64 * (s & 1) + 8 * ks, al = ah + 32;
+            const uint32_t d = tmem + ((it / 10) & 1) * N;
+            mma_f16_ts(d, al, db + o, idesc, (it % 10 > 0 || ks > 0) ? 1u : 0u);
+            mma_f16_ts(d, ah, db + o, idesc, 1u);
+            mma_f16_ts(d, ah, db + o, idesc, 1u);
+          } else if (kTS)  // A: 8 TMEM columns (32 bytes of K) per MMA, columns 2N..
             mma_f16_ts(tmem + (it & 1) * N, tmem + 2 * N + 32 * (it & 1) + 8 * ks, db + o, idesc,
                        (it > 1 || ks > 0) ? 1u : 0u);
           else
             mma_f16(tmem + (it & 1) * N, da + o, db + o, idesc, (it > 1 || ks > 0) ? 1u : 0u);
         }
+        if (mode >= 1) mma_commit(&sbar[s]);
       }
       __syncwarp();
     }
@@ -62,7 +72,7 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int iters, unsigned long 
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
-int main() {
+int main(int argc, char** argv) {
   unsigned long long* d;
   cudaMalloc(&d, 8);
   for (int N : {128, 160}) {
@@ -70,20 +80,22 @@ int main() {
     const size_t smem = 1024 + 4 * size_t(stage);
     cudaFuncSetAttribute(bench<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(bench<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int iters = 4000;
+    const int iters = argc > 1 ? atoi(argv[1]) : 4000;
+    for (int mode = (argc > 2 ? atoi(argv[2]) : 0); mode < (argc > 2 ? atoi(argv[2]) + 1 : 3); ++mode)
     for (int ts = 0; ts < 2; ++ts)
       for (int rep = 0; rep < 2; ++rep) {
         cudaMemset(d, 0, 8);
         if (ts)
-          bench<true><<<148, 128, smem>>>(N, iters, d);
+          bench<true><<<148, 128, smem>>>(N, iters, d, mode);
         else
-          bench<false><<<148, 128, smem>>>(N, iters, d);
+          bench<false><<<148, 128, smem>>>(N, iters, d, mode);
         cudaError_t e = cudaDeviceSynchronize();
         unsigned long long h = 0;
         cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
         if (rep == 1)
-          printf("%s N=%3d: %6.1f cycles/MMA (floor %.0f) %s\n", ts ? "TS" : "SS", N,
-                 double(h) / 148.0 / (4.0 * iters), 128.0 * N / 256.0, cudaGetErrorString(e));
+          printf("mode %d %s N=%3d: %6.1f cycles/MMA (floor %.0f) %s\n", mode, ts ? "TS" : "SS", N,
+                 double(h) / 148.0 / ((mode == 2 ? 12.0 : 4.0) * iters), 128.0 * N / 256.0,
+                 cudaGetErrorString(e));
       }
   }
   return 0;
