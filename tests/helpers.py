@@ -19,13 +19,17 @@ def top2_margin(values):
     return float((v[0] - v[1]) / scale) if v.size > 1 else np.inf
 
 
-def assert_maps_match(gpu, ref, argmax_gpu, tol=REL_L2_TOL, what=""):
-    """Per-frame rel-L2 <= tol and identical argmax (lowest index on ties).
+#: reference top-2 gaps below this (relative to the map scale) are ties at
+#: fp64 rounding (e.g. mirror-symmetric candidates); an fp32 map cannot order
+#: them, so only there may the argmax differ
+TIE_REL = 1e-9
 
-    An argmax difference is tolerated only when the reference's own top-2
-    margin is below the measured map error (a numerical tie), and is
-    reported in the assertion message otherwise.
-    """
+
+def assert_maps_match(gpu, ref, argmax_gpu, tol=REL_L2_TOL, what=""):
+    """Per-frame rel-L2 <= tol and identical argmax (lowest index on ties,
+    BASELINE north_star).  The only argmax difference accepted is between
+    candidates the reference itself scores equal to fp64 rounding
+    (gap <= TIE_REL of the map scale).  Returns the worst rel-L2."""
     gpu = np.atleast_2d(np.asarray(gpu, dtype=np.float64))
     ref = np.atleast_2d(np.asarray(ref, dtype=np.float64))
     assert gpu.shape == ref.shape, (gpu.shape, ref.shape)
@@ -38,9 +42,8 @@ def assert_maps_match(gpu, ref, argmax_gpu, tol=REL_L2_TOL, what=""):
         ga = int(argmax_gpu[f])
         if ga != ra:
             gap = (ref[f][ra] - ref[f][ga]) / max(np.max(np.abs(ref[f])), 1e-300)
-            err = np.max(np.abs(gpu[f] - ref[f])) / max(np.max(np.abs(ref[f])), 1e-300)
-            assert gap <= 2 * err, (
-                f"{what} frame {f}: argmax {ga} != reference {ra} (gap {gap:.3e}, "
-                f"max err {err:.3e})"
+            assert gap <= TIE_REL, (
+                f"{what} frame {f}: argmax {ga} != reference {ra} (reference gap {gap:.3e}, "
+                f"top-2 margin {top2_margin(ref[f]):.3e})"
             )
     return worst

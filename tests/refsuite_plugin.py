@@ -1,0 +1,115 @@
+"""pytest plugin: run the reference's own test files against the drop-ins.
+
+Loaded with ``-p refsuite_plugin`` by ``tests/test_reference_suite_gpu.py``
+on the reference's test modules shipped in ``baseline/_ref/srpfast_tests``
+(the unmodified reference package lives in ``baseline/_ref/srpfast``,
+installed with pip --target; both are git-ignored and travel to the GPU box).
+
+Before collection it rebinds, in ``srpfast.srp``, ``srpfast.spectral``,
+``srpfast.metrics``, ``srpfast.experiment`` and ``srpfast`` itself, every
+hot-path function and result type the reference exports that this package
+implements -- so ``from srpfast.srp import
+build_gcc_lattice`` inside a reference test binds the B200 drop-in, and the
+reference's harness (``run_experiment``, ``run_benchmark``) calls it too.
+Geometry, simulation, reporting and the private ``_phase_matrix`` stay the
+reference's.
+
+Tolerances: the reference asserts fp64 agreement (``rel=1e-12``).  The
+drop-ins compute in fp32 (3xFP16 tensor-core contractions; BASELINE
+north_star tolerance rel-L2 1e-5), so ``pytest.approx`` and
+``np.testing.assert_allclose`` are widened to ``FP32_REL`` relative plus
+``FP32_REL`` of the compared array's scale -- never tightened.  Structural
+checks (counts, shapes, argmax indices, raised errors and messages) are
+unchanged.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+REF = os.path.join(ROOT, "baseline", "_ref")
+
+#: fp32-path tolerance applied to the reference's fp64 comparisons
+FP32_REL = 2e-5
+
+#: reference names rebound to this package's drop-ins
+FUNCTIONS = {
+    "srpfast.spectral": ["cross_spectrum", "stft_analyze"],
+    "srpfast.srp": ["srp_conventional", "srp_conventional_frames", "build_gcc_lattice",
+                    "precompute_sinc_table", "srp_approx", "srp_oracle", "argmax_candidate",
+                    "gcc_at_lag", "lattice_half_counts", "complexity_report"],
+    "srpfast.metrics": ["approximation_error_db"],
+}
+TYPES = {
+    "srpfast.srp": ["SrpMap", "GccLattice", "SincTable", "MultCounter", "ComplexityReport"],
+}
+
+_orig_approx = pytest.approx
+_orig_allclose = np.testing.assert_allclose
+
+
+def _fp32_approx(expected, rel=None, abs=None, nan_ok=False):  # noqa: A002 - pytest's name
+    rel = max(rel if rel is not None else 1e-6, FP32_REL)
+    try:
+        scale = float(np.max(np.abs(np.asarray(expected, dtype=float))))
+    except (TypeError, ValueError):
+        scale = 0.0
+    abs_ = max(abs if abs is not None else 0.0, FP32_REL * scale)
+    return _orig_approx(expected, rel=rel, abs=abs_, nan_ok=nan_ok)
+
+
+def _fp32_allclose(actual, desired, rtol=1e-7, atol=0, equal_nan=True, err_msg="",
+                   verbose=True, **kw):
+    d = np.asarray(desired)
+    scale = float(np.max(np.abs(d))) if d.size and np.issubdtype(d.dtype, np.number) else 0.0
+    return _orig_allclose(actual, desired, rtol=max(rtol, FP32_REL),
+                          atol=max(atol, FP32_REL * scale), equal_nan=equal_nan,
+                          err_msg=err_msg, verbose=verbose, **kw)
+
+
+def rebind():
+    """Point the reference's hot-path names at the drop-ins; returns the
+    (module, name) list that was rebound."""
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    if ROOT not in sys.path:
+        sys.path.insert(0, ROOT)
+    import importlib
+
+    import paper_2012_09499_b200 as B
+
+    done = []
+    mods = {name: importlib.import_module(name) for name in
+            ("srpfast", "srpfast.spectral", "srpfast.srp", "srpfast.metrics",
+             "srpfast.experiment")}
+    table = {}
+    for src, names in list(FUNCTIONS.items()) + list(TYPES.items()):
+        for name in names:
+            table[name] = getattr(B, name)
+    for mod in mods.values():
+        for name, obj in table.items():
+            if hasattr(mod, name):
+                setattr(mod, name, obj)
+                done.append((mod.__name__, name))
+    return done
+
+
+def pytest_configure(config):
+    config.refsuite_rebound = rebind()
+    pytest.approx = _fp32_approx
+    np.testing.assert_allclose = _fp32_allclose
+
+
+def pytest_unconfigure(config):
+    pytest.approx = _orig_approx
+    np.testing.assert_allclose = _orig_allclose
+
+
+def pytest_report_header(config):
+    return (f"refsuite: {len(config.refsuite_rebound)} reference names rebound to "
+            f"paper_2012_09499_b200 drop-ins; fp64 tolerances widened to {FP32_REL}")
