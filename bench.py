@@ -638,7 +638,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2012_09499_b200 import _native
-    from paper_2012_09499_b200.distributed import frame_ranges, gather_frames
+    from paper_2012_09499_b200.distributed import frame_ranges, gather_results
     from paper_2012_09499_b200.pipeline import ChunkedRunner
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -678,8 +678,7 @@ def run_ours(args):
         def run():
             maps, am = graphs[path].replay()
             if world > 1:  # results of all ranks on every rank (NVLink all-gather)
-                gather_frames(am.to(torch.int64), F)
-                gather_frames(maps, F)
+                gather_results(maps, am, F)
         return run
 
     n0 = _native.launch_count()

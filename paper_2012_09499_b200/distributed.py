@@ -147,6 +147,14 @@ def run_frame_sharded(plan, Y_all, path="approx", maps=True, gather=True, group=
     m, am = plan.run(Y_all[lo:hi].contiguous(), path, maps=maps)
     if not gather or world == 1:
         return m, am
-    am_all = gather_frames(am.to(torch.int64), F, group).to(torch.int32)
-    m_all = gather_frames(m, F, group) if m is not None else None
+    return gather_results(m, am, F, group)
+
+
+def gather_results(maps_local, argmax_local, num_frames, group=None):
+    """All-gather one rank's frame-block results: per-frame maps
+    ``[F_r, J]`` (or None) and argmax ``[F_r]`` -> (maps [F, J] | None,
+    argmax [F] int32) on every rank, in frame order (NCCL over NVLink on the
+    GPU; the bench's multi-GPU step ends with this call)."""
+    am_all = gather_frames(argmax_local.to(torch.int64), num_frames, group).to(torch.int32)
+    m_all = gather_frames(maps_local, num_frames, group) if maps_local is not None else None
     return m_all, am_all

@@ -110,6 +110,7 @@ def pytest_unconfigure(config):
     np.testing.assert_allclose = _orig_allclose
 
 
-def pytest_report_header(config):
-    return (f"refsuite: {len(config.refsuite_rebound)} reference names rebound to "
-            f"paper_2012_09499_b200 drop-ins; fp64 tolerances widened to {FP32_REL}")
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    terminalreporter.write_line(
+        f"refsuite: {len(config.refsuite_rebound)} reference names rebound to "
+        f"paper_2012_09499_b200 drop-ins; fp64 tolerances widened to {FP32_REL}")
