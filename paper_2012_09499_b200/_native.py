@@ -15,6 +15,11 @@ import torch
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsrpb.so")
 _lib = None
 
+#: the C ABI revision these signatures describe (include/srpb.h); load()
+#: refuses a library of another revision instead of calling it with
+#: mismatched arguments
+ABI_VERSION = 12
+
 c_int, c_double, c_void_p = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
 
 # name -> argtypes (restype int unless listed in _RESTYPES)
@@ -106,6 +111,12 @@ def load(path: str | None = None):
             "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)"
         )
     lib = ctypes.CDLL(path)
+    lib.srpb_abi_version.argtypes = []
+    lib.srpb_abi_version.restype = c_int
+    got = int(lib.srpb_abi_version())
+    if got != ABI_VERSION:
+        raise ImportError(f"{path} implements C ABI v{got}, this package binds v{ABI_VERSION}; "
+                          "rebuild it (make)")
     for name, argtypes in _SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
@@ -178,6 +189,13 @@ def call(name, *args):
             raise ValueError(msg)
         raise NativeError(msg)
     return rc
+
+
+def on_device(device):
+    """Context in which launches go to ``device``: libsrpb launches on the
+    current CUDA device with the stream passed in, so a plan living on a
+    non-current GPU switches to it for its calls."""
+    return torch.cuda.device(device)
 
 
 def require_cuda(device=None) -> torch.device:

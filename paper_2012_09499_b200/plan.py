@@ -20,8 +20,10 @@ All per-frame work goes through ``libsrpb.so``; nothing here computes maps.
 
 from __future__ import annotations
 
+import functools
 import math
 import os
+import threading
 
 import numpy as np
 import torch
@@ -49,6 +51,20 @@ def split_rint(x: np.ndarray):
     """fp64 ``x`` -> (int64 rint(x), fp32 x - rint(x)), |fraction| <= 1/2."""
     i = np.rint(x)
     return i.astype(np.int64), (x - i).astype(np.float32)
+
+
+def _on_plan_device(fn):
+    """Run a plan method with the plan's GPU as the current device (the C
+    entry points launch on the current device; a plan built for a
+    non-current GPU would otherwise launch onto the wrong one)."""
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kw):
+        dev = getattr(self, "device", None)
+        if dev is None or dev.index is None or dev.index == torch.cuda.current_device():
+            return fn(self, *args, **kw)
+        with N.on_device(dev):
+            return fn(self, *args, **kw)
+    return wrapper
 
 
 def lattice_layout(tdoa_bounds, sample_period, n_aux):
@@ -84,11 +100,15 @@ class SrpPlan:
         3xTF32) or ``"tf32"`` (always 3xTF32)
     """
 
-    def __init__(self, tdoa_table, pair_m, pair_mp, tdoa_bounds, bin_frequencies,
-                 sample_period=None, n_aux=None, weights="auto", device=None,
+    def __init__(self, *args, device=None, **kw):
+        self.device = N.require_cuda(device)
+        with N.on_device(self.device):
+            self._init(*args, **kw)
+
+    def _init(self, tdoa_table, pair_m, pair_mp, tdoa_bounds, bin_frequencies,
+                 sample_period=None, n_aux=None, weights="auto",
                  max_weight_bytes=DEFAULT_MAX_WEIGHT_BYTES, conventional=True, backend="auto",
                  kb_per_group=4, interp_kb_per_group=10, precision="auto", _geometry=None):
-        self.device = N.require_cuda(device)
         if precision not in ("auto", "tf32"):
             raise ValueError(f"precision must be auto|tf32, got {precision!r}")
         self.precision = precision
@@ -248,29 +268,44 @@ class SrpPlan:
         self.weight_mode = "stored" if store else "onthefly"
 
     # ---------------------------------------------------------------- helpers
+    _owner_tls = threading.local()
+
+    def _state_owner(self):
+        """Key of the launch context that owns the persistent kernel state:
+        the CapturedStep being captured (its graph replays reuse the same
+        pointers), else the current stream.  Two launches that could run
+        concurrently never share a cursor / key buffer."""
+        owner = getattr(SrpPlan._owner_tls, "owner", None)
+        if owner is not None:
+            return ("graph", owner)
+        return ("stream", torch.cuda.current_stream(self.device).cuda_stream)
+
     def _argmax_state(self, F):
         """Persistent zeroed (keys [F], done counter + item cursor) for the
         tensor-core kernels' dynamic item scheduling and in-kernel argmax
         finish: the last CTA decodes the keys and resets all three, so no
-        reset / decode launches are needed per call."""
+        reset / decode launches are needed per call.  One set per (F, owner):
+        kernels in flight on different streams or graphs never share one."""
         st = getattr(self, "_am_state", None)
         if st is None:
             st = self._am_state = {}
-        if F not in st:
+        key = (F, self._state_owner())
+        if key not in st:
             # done counter [0] and the dynamic item cursor [1]
-            st[F] = (torch.zeros(F, dtype=torch.int64, device=self.device),
-                     torch.zeros(2, dtype=torch.int32, device=self.device))
-        return st[F]
+            st[key] = (torch.zeros(F, dtype=torch.int64, device=self.device),
+                       torch.zeros(2, dtype=torch.int32, device=self.device))
+        return st[key]
 
     def _frame_counters(self, F):
         """Persistent zeroed per-frame counters of the in-kernel floor fix-up
-        (the kernel leaves them zero)."""
+        (the kernel leaves them zero), one set per (F, owner)."""
         st = getattr(self, "_fc_state", None)
         if st is None:
             st = self._fc_state = {}
-        if F not in st:
-            st[F] = torch.zeros(F, dtype=torch.int32, device=self.device)
-        return st[F]
+        key = (F, self._state_owner())
+        if key not in st:
+            st[key] = torch.zeros(F, dtype=torch.int32, device=self.device)
+        return st[key]
 
     def _keys(self, F):
         keys = torch.empty(F, dtype=torch.int64, device=self.device)
@@ -307,6 +342,7 @@ class SrpPlan:
             abs_floor = float(phat_floor)
         return Y.shape[0], (0 if weighting == "phat" else 1), abs_floor
 
+    @_on_plan_device
     def cross_spectra(self, Y, weighting="phat", phat_floor=None, out=None):
         """K1: ``Y`` [F, M, Kb] complex64 -> (Psi [F, P, Kb] complex64,
         applied floors [F] float64)."""
@@ -319,6 +355,7 @@ class SrpPlan:
                N.ptr(floors), N.stream_handle(self.device))
         return psi, floors
 
+    @_on_plan_device
     def lattice_from_spectra(self, Y, weighting="phat", phat_floor=None, split=False):
         """K1a + fused K1b/K3: ``Y`` [F, M, Kb] -> Xi [F, T_pad] fp32, or its
         tensor-core operand split (Xi_hi, Xi_lo): ``split=True`` / ``"tf32"``
@@ -433,6 +470,7 @@ class SrpPlan:
             return self.harmonic and self.Kb % 32 == 0
         return True  # stored W, or weights generated in TMEM
 
+    @_on_plan_device
     def conventional(self, psi, maps=True, maps_out=None, _bounded=False):
         """K2 (+ fused K5): Psi [F, P, Kb] -> (maps [F, J] fp32 | None,
         argmax [F] int32)."""
@@ -475,6 +513,7 @@ class SrpPlan:
                    N.ptr(idx), N.ptr(done), N.stream_handle(self.device))
         return (out if maps else None), idx
 
+    @_on_plan_device
     def lattice(self, psi, out=None):
         """K3: Psi [F, P, Kb] -> Xi [F, T_pad] fp32 (pad columns zero)."""
         if self.sample_period is None:
@@ -488,6 +527,7 @@ class SrpPlan:
                N.stream_handle(self.device))
         return xi
 
+    @_on_plan_device
     def approx(self, xi, maps=True, maps_out=None):
         """K4 (+ fused K5): Xi [F, T_pad] -> (maps [F, J] | None, argmax [F])."""
         if self.sample_period is None:
@@ -542,6 +582,7 @@ class SrpPlan:
                    self.interp_kb_per_group, N.stream_handle(self.device))
         return out, self.keys_to_index(keys)
 
+    @_on_plan_device
     def argmax(self, maps):
         """K5 standalone over stored maps [F, J] fp32."""
         if maps.dim() != 2 or maps.dtype != torch.float32 or not maps.is_contiguous():
@@ -551,6 +592,7 @@ class SrpPlan:
         N.call("srpb_argmax", N.ptr(maps), F, J, N.ptr(keys), N.stream_handle(self.device))
         return self.keys_to_index(keys)
 
+    @_on_plan_device
     def run(self, Y, path="approx", maps=True, weighting="phat", phat_floor=None):
         """Y [F, M, Kb] complex64 -> (maps | None, argmax) along ``path``.
         The approximate path fuses K1's cross-spectra into K3; with PHAT
@@ -616,6 +658,7 @@ class SrpPlan:
                 "bounds": torch.as_tensor(bounds, device=dev)}
         return cls(None, pm, pmp, bounds, bin_frequencies, _geometry=geom, **kw)
 
+    @_on_plan_device
     def stft(self, x, frame_length, hop_length=None, window="sqrt_hann", out=None):
         """K0: audio ``x`` [M, L] float32 (CUDA) -> Y [F, M, frame_length/2]
         complex64 (``spectral.stft_analyze`` framing and window)."""
@@ -638,6 +681,7 @@ class SrpPlan:
                0 if window == "sqrt_hann" else 1, F, N.ptr(Y), N.stream_handle(self.device))
         return Y
 
+    @_on_plan_device
     def run_audio(self, x, frame_length, hop_length=None, window="sqrt_hann", path="approx",
                   maps=True, weighting="phat", phat_floor=None):
         """K0 + ``run``: audio [M, L] -> (maps | None, argmax) per frame."""
@@ -702,18 +746,25 @@ class CapturedStep:
                 plan.stft(self.x, n_, hop_, win_, out=self.Y)
             return plan.run(self.Y, path, maps, weighting, phat_floor)
 
+        tls = SrpPlan._owner_tls
+        prev_owner = getattr(tls, "owner", None)
         try:
-            # warm-up outside capture: lazily built operands (fp16 W split),
-            # kernel attributes, allocator pools
-            body()
-            torch.cuda.synchronize(dev)
-            self.graph = torch.cuda.CUDAGraph()
-            n0 = N.launch_count()
-            with torch.cuda.graph(self.graph):
-                self.maps, self.argmax = body()
-            #: kernels launched by one replay
-            self.launches = N.launch_count() - n0
+            # the graph owns its kernels' persistent state (keys, cursor):
+            # replays of different steps may overlap on different streams
+            tls.owner = id(self)
+            with N.on_device(dev):
+                # warm-up outside capture: lazily built operands (fp16 W
+                # split), kernel attributes, allocator pools
+                body()
+                torch.cuda.synchronize(dev)
+                self.graph = torch.cuda.CUDAGraph()
+                n0 = N.launch_count()
+                with torch.cuda.graph(self.graph):
+                    self.maps, self.argmax = body()
+                #: kernels launched by one replay
+                self.launches = N.launch_count() - n0
         finally:
+            tls.owner = prev_owner
             plan.kernel_timer = timer
 
     @property

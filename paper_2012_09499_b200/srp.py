@@ -478,7 +478,14 @@ def _full_pair_count(n_pairs):
 
 
 def srp_oracle_frames(frames, grid, weighting="phat", phat_floor=None) -> list:
-    """Batched :func:`srp_oracle`: one ``srpb_srp_quadform`` launch (fp64)."""
+    """Batched :func:`srp_oracle`: one ``srpb_srp_quadform`` launch (fp64).
+
+    Scope of the check: the quadratic form, steering vectors and sums run in
+    fp64 with direct exponentials, independently of K2's phase generator and
+    tensor-core contraction; given spectral frames, the weighted cross
+    matrix comes from K1 (complex64 psi), so this cross-check covers K2
+    onward, not K1 (K1 is pinned to the reference's golden vectors in
+    tests/test_parity_gpu.py)."""
     frames = list(frames)
     if not frames:
         return []
