@@ -555,6 +555,56 @@ class Timer:
         return ms, kms
 
 
+def dropin_line(dev, n_frames=64):
+    """The reference-API path a harness takes per frame (experiment.py:
+    460-484): SpectralFrame (host spectra) -> cross_spectrum ->
+    build_gcc_lattice -> srp_approx -> argmax_candidate, one frame at a time
+    on C2 (50k candidates, N_aux 4), plus the same through the batched
+    drop-ins (one call per stage for all frames).  Host-driven API: wall
+    clock, the argmax int read ends each frame."""
+    import torch
+
+    import paper_2012_09499_b200 as B
+    from paper_2012_09499_b200 import scenes
+
+    sc = scenes.make_c2(num_frames=n_frames)
+    arr = B.MicArray(sc.mic_pos, speed_of_sound=C_SOUND)
+    grid = B.build_tdoa_table(arr, B.CandidateGrid("near_field", sc.grid))
+    table = B.precompute_sinc_table(grid, arr.pairs, T, 4)
+    freqs = omega_of(sc.frame_length)
+    frames = [B.SpectralFrame(sc.Y[f], freqs, frame_index=f) for f in range(n_frames)]
+
+    def per_frame():
+        out = []
+        for fr in frames:
+            cross = B.cross_spectrum(fr, arr.pairs)
+            lat = B.build_gcc_lattice(cross, T, 4)
+            out.append(B.argmax_candidate(B.srp_approx(lat, table)))
+        return out
+
+    def batched():
+        crosses = B.cross_spectrum_frames(frames, arr.pairs)
+        lats = B.build_gcc_lattice_frames(crosses, T, 4)
+        return [B.argmax_candidate(m) for m in B.srp_approx_frames(lats, table, maps=False)]
+
+    res = {}
+    for name, fn in (("per_frame", per_frame), ("batched", batched)):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = 3
+        for _ in range(reps):
+            am = fn()
+        sec = (time.perf_counter() - t0) / reps
+        res[name] = {"value": n_frames * grid.tdoa_table.shape[0] / sec, "unit": UNIT,
+                     "ms_per_frame": 1e3 * sec / n_frames, "frames": n_frames}
+    res["argmax_agree"] = bool(per_frame() == am)
+    res["api"] = ("reference-named drop-ins from host numpy spectra (paper_2012_09499_b200 "
+                  "cross_spectrum / build_gcc_lattice / srp_approx / argmax_candidate), "
+                  "C2 N_aux 4, wall clock")
+    return res
+
+
 def sweep_lines(timer, dev, args):
     """Driver-visible lines for the other BASELINE configs (graph replay,
     inputs resident, 2 warm-ups + a few timed steps each)."""
@@ -625,6 +675,7 @@ def sweep_lines(timer, dev, args):
             torch.cuda.empty_cache()
         c5[str(B)] = row
         del Yb
+    out["C2_dropin_api"] = dropin_line(dev)
     out["C5"] = {"candidates": plan.J, "n_aux": 4, "unit": UNIT,
                  "note": "latency = ms per batch (CUDA-graph replay, inputs resident); batch "
                          "65536 argmax-only (maps not materialised)", "batches": c5}

@@ -528,8 +528,10 @@ class SrpPlan:
         return xi
 
     @_on_plan_device
-    def approx(self, xi, maps=True, maps_out=None):
-        """K4 (+ fused K5): Xi [F, T_pad] -> (maps [F, J] | None, argmax [F])."""
+    def approx(self, xi, maps=True, maps_out=None, bounded=False):
+        """K4 (+ fused K5): Xi [F, T_pad] -> (maps [F, J] | None, argmax [F]).
+        ``bounded``: the samples come from PHAT cross-spectra (|xi| <= 2 Kb),
+        so the 3xFP16 tensor-core kernel (argmax finished in-kernel) applies."""
         if self.sample_period is None:
             raise ValueError("plan was built without a lattice (sample_period)")
         self._check_frames(xi, (self.T_pad,), torch.float32, "xi")
@@ -538,6 +540,9 @@ class SrpPlan:
         if maps:
             out = maps_out if maps_out is not None else torch.empty(
                 (F, self.J), dtype=torch.float32, device=self.device)
+        if self._f16_ok("interp", bounded) and self._use_tc(F, "interp16"):
+            xh, xl = self.split_f16(xi, self.xi_scale16)
+            return self._approx_tc16(xh, xl, out)
         keys = self._keys(F)
         s = N.stream_handle(self.device)
         if self._use_tc(F, "interp"):

@@ -143,7 +143,7 @@ class CrossSpectra:
     """Weighted pairwise cross-spectra of one frame (``spectral.py:137-182``)."""
 
     def __init__(self, values, bin_frequencies, pairs, weighting, phat_floor=0.0,
-                 frame_index=0, _rows=None, _row=0):
+                 frame_index=0, _rows=None, _row=0, _floors=None):
         self.pairs = tuple(pairs)
         if _rows is not None:
             self._rows, self._row, self._host = _rows, _row, None
@@ -158,9 +158,19 @@ class CrossSpectra:
         if weighting not in WEIGHTINGS:
             raise ValueError(f"unknown weighting {weighting!r}")
         self.weighting = weighting
-        self.phat_floor = float(phat_floor)
+        # device-computed floors ([F] fp64 rows) are fetched when first read,
+        # so building cross-spectra never waits for the device
+        self._floors = _floors
+        self._phat_floor = None if _floors is not None else float(phat_floor)
         self.frame_index = frame_index
         self._shape = shape
+
+    @property
+    def phat_floor(self) -> float:
+        if self._phat_floor is None:
+            self._phat_floor = float(self._floors.host()[self._row]) \
+                if self.weighting == "phat" else 0.0
+        return self._phat_floor
 
     @property
     def values(self) -> np.ndarray:
@@ -278,11 +288,10 @@ def cross_spectrum_frames(frames, pairs, weighting="phat", phat_floor=None, devi
     Y = torch.stack([fr.device_spectra(dev) for fr in frames])
     psi, floors = gcc_phat_batch(Y, pm, pmp, weighting, phat_floor)
     rows = _DeviceRows(psi, np.complex128)
-    fl = floors.cpu().numpy()
+    frows = _DeviceRows(floors, np.float64)
     return [
-        CrossSpectra(None, fr.bin_frequencies, pairs, weighting,
-                     phat_floor=float(fl[i]) if weighting == "phat" else 0.0,
-                     frame_index=fr.frame_index, _rows=rows, _row=i)
+        CrossSpectra(None, fr.bin_frequencies, pairs, weighting, frame_index=fr.frame_index,
+                     _rows=rows, _row=i, _floors=frows)
         for i, fr in enumerate(frames)
     ]
 

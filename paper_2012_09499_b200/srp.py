@@ -80,6 +80,8 @@ class SrpMap:
     def __init__(self, values, method, frame_index=0, _rows=None, _row=0, _argmax=None):
         self.method = method
         self.frame_index = frame_index
+        # fused device argmax: an int, or (_DeviceRows of [F] indices, row)
+        # fetched on first use (building maps never waits for the device)
         self._argmax = _argmax
         if _rows is not None:
             self._rows, self._row, self._host = _rows, _row, None
@@ -112,6 +114,9 @@ def argmax_candidate(srp_map) -> int:
     run the K5 reduction (fp64) on the device.
     """
     am = getattr(srp_map, "_argmax", None)
+    if isinstance(am, tuple):
+        rows, i = am
+        return int(rows.host()[i])
     if am is not None:
         return int(am)
     dev_row = srp_map.device_values() if hasattr(srp_map, "device_values") else None
@@ -178,7 +183,10 @@ class GccLattice:
     """
 
     def __init__(self, sample_period, n_aux, half_counts, samples=None, frame_index=0,
-                 _rows=None, _row=0, _plan=None):
+                 _rows=None, _row=0, _plan=None, _bounded=False):
+        # _bounded: device samples of PHAT cross-spectra, |xi| <= 2 Kb (the
+        # 3xFP16 interpolation's operand bound)
+        self._bounded = bool(_bounded)
         self.sample_period = float(sample_period)
         self.n_aux = int(n_aux)
         self.half_counts = tuple(int(h) for h in half_counts)
@@ -236,6 +244,7 @@ class GccLattice:
         flat[0, :cat.size] = cat
         t = torch.as_tensor(flat, device=dev)
         self._rows, self._row = _DeviceRows(t, np.float64), 0
+        self._bounded = False
         return t[0]
 
 
@@ -278,9 +287,10 @@ def build_gcc_lattice_frames(crosses, sample_period, n_aux, counter=None, device
     if counter is not None:
         for _ in crosses:
             counter.add_complex(total * crosses[0].num_bins)
+    bounded = all(getattr(c, "weighting", None) == "phat" for c in crosses)
     return [
         GccLattice(sample_period, n_aux, halves, frame_index=c.frame_index, _rows=rows, _row=i,
-                   _plan=plan)
+                   _plan=plan, _bounded=bounded)
         for i, c in enumerate(crosses)
     ]
 
@@ -390,14 +400,15 @@ def srp_approx_frames(lattices, table, counter=None, maps=True):
             xi = xi[torch.as_tensor(idx, device=dev)].contiguous()
     else:
         xi = torch.stack([l.device_row(plan.T_pad, dev) for l in lattices]).contiguous()
-    out, am = plan.approx(xi, maps=maps)
-    am = am.cpu().numpy()
+    bounded = all(getattr(l, "_bounded", False) for l in lattices)
+    out, am = plan.approx(xi, maps=maps, bounded=bounded)
     if counter is not None:
         for _ in lattices:
             counter.add_real(plan.J * plan.total_samples)
     mrows = _DeviceRows(out, np.float64) if out is not None else None
+    arows = _DeviceRows(am, np.int64)
     return [SrpMap(None, "approximated", frame_index=l.frame_index, _rows=mrows, _row=i,
-                   _argmax=int(am[i])) for i, l in enumerate(lattices)]
+                   _argmax=(arows, i)) for i, l in enumerate(lattices)]
 
 
 def srp_approx(lattice, table, counter=None) -> SrpMap:
@@ -446,14 +457,15 @@ def srp_conventional_frames(frames, grid, counter=None, maps=True) -> list:
     dev = N.require_cuda()
     plan = _conventional_plan(grid, frames, dev)
     psi = _device_psi(frames, dev)
-    out, am = plan.conventional(psi, maps=maps)
-    am = am.cpu().numpy()
+    bounded = all(getattr(fr, "weighting", None) == "phat" for fr in frames)
+    out, am = plan.conventional(psi, maps=maps, _bounded=bounded)
     if counter is not None:
         for _ in range(n_pairs):
             counter.add_complex(table.shape[0] * omega.size * len(frames))
     mrows = _DeviceRows(out, np.float64) if out is not None else None
+    arows = _DeviceRows(am, np.int64)
     return [SrpMap(None, "conventional", frame_index=fr.frame_index, _rows=mrows, _row=i,
-                   _argmax=int(am[i])) for i, fr in enumerate(frames)]
+                   _argmax=(arows, i)) for i, fr in enumerate(frames)]
 
 
 def srp_conventional(cross, grid, counter=None) -> SrpMap:
