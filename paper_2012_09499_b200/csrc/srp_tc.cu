@@ -113,7 +113,11 @@ __device__ __forceinline__ void tc_trace(int it, int e) {
 #define TCP_T0() const long long _tcp0 = clock64()
 #define TCP_ACC(v) (v += clock64() - _tcp0)
 #define TCP_FLUSH(i, v) atomicAdd(&g_tc_prof[i], static_cast<unsigned long long>(v))
+#define TC_DBG(prm) ((prm).dbg)
 #else
+// bound-analysis switches (SRPB_TC_DBG) exist in the instrumentation build
+// only: the product kernels carry no per-block flag tests
+#define TC_DBG(prm) 0
 #define TCP_DECL(v)
 #define TCP_T0()
 #define TCP_ACC(v)
@@ -691,7 +695,7 @@ struct SincGen {
     const int t0 = 64 * kb + 32 * half;
     // a thread sees 32 of every 64 columns: pairs may end in the skipped half
     while (t0 >= end) advance(prm, j);  // warp-uniform
-    if (prm.dbg & 2048) {  // bound analysis only: no weight arithmetic
+    if (TC_DBG(prm) & 2048) {  // bound analysis only: no weight arithmetic
 #pragma unroll
       for (int i = 0; i < 16; ++i) hi[i] = lo[i] = __float_as_uint(f) + i;
     } else if (t0 + 32 <= end) {
@@ -708,7 +712,7 @@ struct SincGen {
       for (int c = 0; c < 32; c += 2) {
         const float2 x = __fadd2_rn(dd, f2);
         dd = __fadd2_rn(dd, m2);
-        const float2 r = (prm.dbg & 1024) ? x : make_float2(rcp_approx_ftz(x.x), rcp_approx_ftz(x.y));
+        const float2 r = (TC_DBG(prm) & 1024) ? x : make_float2(rcp_approx_ftz(x.x), rcp_approx_ftz(x.y));
         split2(__fmul2_rn(r, a2), hi[c >> 1], lo[c >> 1]);
       }
       if (__any_sync(0xffffffffu, node)) {
@@ -748,7 +752,7 @@ struct SincGen {
 #pragma unroll
       for (int c = 0; c < 32; c += 2) split2(make_float2(w[c], w[c + 1]), hi[c >> 1], lo[c >> 1]);
     }
-    if (prm.dbg & 4096) return;  // bound analysis only: no TMEM stores
+    if (TC_DBG(prm) & 4096) return;  // bound analysis only: no TMEM stores
     tmem_st16(a_hi_tmem + 16 * half, hi);
     tmem_st16(a_lo_tmem + 16 * half, lo);
   }
@@ -953,15 +957,15 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       if (!leader) item_release(it);
       if (leader) gid_next = item_fetch(it + 1);
       if (lane == 0) TCT(it, 0);
-      const int m0 = (p.dbg & 1) ? t.m0 % 2048 : t.m0;
+      const int m0 = (TC_DBG(p) & 1) ? t.m0 % 2048 : t.m0;
       const int rows = kPair ? t.nc / 2 : t.nc;    // this CTA's B rows (multiple of 16)
       const int nb = t.n0 + rank * rows;
       // one box per B buffer: b_box = the buffer's rows, so a narrower
       // (split) item loads unused tail rows -- never past the buffer
       const int nbox = (rows + p.b_box - 1) / p.b_box;
       const uint32_t tx = static_cast<uint32_t>(kCta) *
-                          (((p.dbg & 4) ? 1 : 2) * static_cast<uint32_t>(nbox * p.b_box) * 128 +
-                           (kASmem ? ((p.dbg & 2) ? 1 : 2) * kABytes : 0));
+                          (((TC_DBG(p) & 4) ? 1 : 2) * static_cast<uint32_t>(nbox * p.b_box) * 128 +
+                           (kASmem ? ((TC_DBG(p) & 2) ? 1 : 2) * kABytes : 0));
       for (int kb = 0; kb < p.num_kb; ++kb, ++kg, ps = ps + 1 == S ? 0 : ps + 1, pph ^= (ps == 0)) {
         const int s = ps;
         { TCP_T0();
@@ -972,24 +976,24 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
           if (kPair) {
             // leader arms the pair's byte count, the peer arrives remotely
             if (leader)
-              mbar_expect_tx(&bar->full[s], (p.dbg & 256) ? 0u : tx);
+              mbar_expect_tx(&bar->full[s], (TC_DBG(p) & 256) ? 0u : tx);
             else
               mbar_arrive_cluster_relaxed(fb);
-            for (int r = 0; r < rows && !(p.dbg & 256); r += p.b_box) {
+            for (int r = 0; r < rows && !(TC_DBG(p) & 256); r += p.b_box) {
               tma_load_2d_pair(b_hi(s) + r * 128, &tmB_hi, fb, kb * KBE, nb + r);
-              if (!(p.dbg & 4)) tma_load_2d_pair(b_lo(s) + r * 128, &tmB_lo, fb, kb * KBE, nb + r);
+              if (!(TC_DBG(p) & 4)) tma_load_2d_pair(b_lo(s) + r * 128, &tmB_lo, fb, kb * KBE, nb + r);
             }
-            if (kASmem && !(p.dbg & 256)) {
+            if (kASmem && !(TC_DBG(p) & 256)) {
               tma_load_2d_pair(a_hi(s), &tmA_hi, fb, kb * KBE, m0);
-              if (!(p.dbg & 2)) tma_load_2d_pair(a_lo(s), &tmA_lo, fb, kb * KBE, m0);
+              if (!(TC_DBG(p) & 2)) tma_load_2d_pair(a_lo(s), &tmA_lo, fb, kb * KBE, m0);
             }
           } else {
-            mbar_expect_tx(&bar->full[s], (p.dbg & 256) ? 0u : tx);
-            for (int r = 0; r < rows && !(p.dbg & 256); r += p.b_box) {
+            mbar_expect_tx(&bar->full[s], (TC_DBG(p) & 256) ? 0u : tx);
+            for (int r = 0; r < rows && !(TC_DBG(p) & 256); r += p.b_box) {
               tma_load_2d(b_hi(s) + r * 128, &tmB_hi, &bar->full[s], kb * KBE, nb + r);
               tma_load_2d(b_lo(s) + r * 128, &tmB_lo, &bar->full[s], kb * KBE, nb + r);
             }
-            if (kASmem && !(p.dbg & 256)) {
+            if (kASmem && !(TC_DBG(p) & 256)) {
               tma_load_2d(a_hi(s), &tmA_hi, &bar->full[s], kb * KBE, m0);
               tma_load_2d(a_lo(s), &tmA_lo, &bar->full[s], kb * KBE, m0);
             }
@@ -1057,11 +1061,11 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
                 const uint32_t o = 2 * ks;      // in 16-byte units
                 const uint32_t acc0 = (in_group > 0 || ks > 0) ? 1u : 0u;
                 if constexpr (kPair && kF16) {
-                  if (!(p.dbg & 8)) {
+                  if (!(TC_DBG(p) & 8)) {
                     mma_f16_pair(d, al + o, bh + o, idesc, acc0);
                     mma_f16_pair(d, ah + o, bl + o, idesc, 1u);
                   }
-                  mma_f16_pair(d, ah + o, bh + o, idesc, (p.dbg & 8) ? acc0 : 1u);
+                  mma_f16_pair(d, ah + o, bh + o, idesc, (TC_DBG(p) & 8) ? acc0 : 1u);
                 } else if constexpr (kPair) {
                   mma_tf32_pair(d, al + o, bh + o, idesc, acc0);
                   mma_tf32_pair(d, ah + o, bl + o, idesc, 1u);
@@ -1197,11 +1201,11 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
         d_chunk = 0;
       }
       switch (d_chunk) {
-        case 0: tc_drain_chunk16_smem<0>(d_base, tot_s, p.dbg); break;
-        case 1: tc_drain_chunk16_smem<1>(d_base, tot_s, p.dbg); break;
-        case 2: tc_drain_chunk16_smem<2>(d_base, tot_s, p.dbg); break;
-        case 3: tc_drain_chunk16_smem<3>(d_base, tot_s, p.dbg); break;
-        default: tc_drain_chunk16_smem<4>(d_base, tot_s, p.dbg); break;
+        case 0: tc_drain_chunk16_smem<0>(d_base, tot_s, TC_DBG(p)); break;
+        case 1: tc_drain_chunk16_smem<1>(d_base, tot_s, TC_DBG(p)); break;
+        case 2: tc_drain_chunk16_smem<2>(d_base, tot_s, TC_DBG(p)); break;
+        case 3: tc_drain_chunk16_smem<3>(d_base, tot_s, TC_DBG(p)); break;
+        default: tc_drain_chunk16_smem<4>(d_base, tot_s, TC_DBG(p)); break;
       }
       if (++d_chunk == t.nc / 32) {  // group folded: release the buffer
         tc_fence_before();
@@ -1415,14 +1419,16 @@ bool use_pair(int m_tiles, bool default_on) {
   return env == 1 || default_on;
 }
 
-// on-the-fly K4: CTA pairs unless SRPB_OTF_PAIR=0
+// on-the-fly K4: single-CTA tiles unless SRPB_OTF_PAIR=1 (measured at C4,
+// F=320: 148 ms single vs 151 ms paired -- the weights are generated, not
+// streamed, so halving each SM's B ingress buys nothing)
 bool use_pair_otf(int m_tiles) {
   static int env = -2;
   if (env == -2) {
     const char* s = getenv("SRPB_OTF_PAIR");
     env = s ? atoi(s) : -1;
   }
-  return m_tiles >= 2 && env != 0;
+  return m_tiles >= 2 && env == 1;
 }
 
 int num_sms() {
@@ -1598,7 +1604,7 @@ static cudaError_t interp_tc(const void* w_hi, const void* w_lo, const void* xi_
   CUtensorMap mm;
   p.maps_tma = 0;
   if (pair && maps && J % 4 == 0 && (reinterpret_cast<uintptr_t>(maps) & 15) == 0 &&
-      !(p.dbg & 512)) {
+      !(TC_DBG(p) & 512)) {
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(J), static_cast<cuuint64_t>(F)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(J) * 4};
     cuuint32_t box[2] = {32, static_cast<cuuint32_t>(kEpiChunk)};
