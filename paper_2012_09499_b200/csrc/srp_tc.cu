@@ -145,6 +145,13 @@ struct TcParams {
   int m_units;        // candidate tiles (of 128, or 256 per pair)
   int m_fast;         // item order: 1 = candidate tile fastest (all CTAs share a
                       // frame tile's B rows in L2), 0 = frame tile fastest
+  int lockstep;       // static items only: a CTA starts round r's item once
+                      // every CTA has issued its round r - 1 loads (done[1]
+                      // counts them), keeping the wave within L2 of each other
+  int dynamic;        // 1: items from the global cursor; 0: static round-robin
+                      // (many waves: the CTAs of a wave start together and run
+                      // identical items in lockstep, so they stream one B tile
+                      // through L2 once instead of each reading it from DRAM)
   float scale;
   float* maps;
   unsigned long long* keys;
@@ -836,7 +843,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     }
     return r;
   };
-  unsigned int* const cursor = p.done ? p.done + 1 : nullptr;
+  unsigned int* const cursor = (p.done && p.dynamic) ? p.done + 1 : nullptr;
   // item id of the it-th item of this CTA (pair): waits for the ring slot
   // (-1 = no more items)
   auto item_id = [&](int it) -> int {
@@ -956,6 +963,23 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       const Item t = item_of(gid);
       if (!leader) item_release(it);
       if (leader) gid_next = item_fetch(it + 1);
+      if (p.lockstep && leader && it > 0) {  // wave barrier (static schedule)
+        // bounded: CTAs that are not co-resident (another kernel holding
+        // SMs) must not deadlock the wave -- after 2 ms a CTA goes on alone
+        if (lane == 0) {
+          const unsigned need = static_cast<unsigned>(min(p.total_items, it * ncl));
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          unsigned got;
+          for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(got) : "l"(p.done + 1));
+            if (got >= need) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 2000000ull) break;
+          }
+        }
+        __syncwarp();
+      }
       if (lane == 0) TCT(it, 0);
       const int m0 = (TC_DBG(p) & 1) ? t.m0 % 2048 : t.m0;
       const int rows = kPair ? t.nc / 2 : t.nc;    // this CTA's B rows (multiple of 16)
@@ -1001,6 +1025,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
         }
         __syncwarp();
       }
+      if (p.lockstep && leader && lane == 0) atomicAdd(p.done + 1, 1u);
     }
     // tail: every stage's last release has landed before this CTA may exit
     for (int t = 0; t < S; ++t, ps = ps + 1 == S ? 0 : ps + 1, pph ^= (ps == 0))
@@ -1431,6 +1456,22 @@ bool use_pair_otf(int m_tiles) {
   return m_tiles >= 2 && env == 1;
 }
 
+int num_sms();
+// Generator modes stream only B (the A operand is generated): with many
+// waves, order items candidate tile fastest and schedule them statically so
+// a wave's CTAs share each B block in L2 (SRPB_TC_DYNAMIC=1 / 0 overrides;
+// measured at C4: K2 read 38.9 TB of DRAM per launch with the dynamic cursor).
+void lockstep_items(TcParams& p, bool pair) {
+  const int units = max(1, num_sms() / (pair ? 2 : 1));
+  const char* e = getenv("SRPB_TC_DYNAMIC");
+  const bool many = p.num_items >= 4 * units;
+  p.dynamic = e ? (atoi(e) != 0) : !many;
+  if (!p.dynamic) {
+    p.m_fast = 1;
+    p.lockstep = p.done != nullptr && getenv("SRPB_TC_NOLOCKSTEP") == nullptr;
+  }
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -1462,6 +1503,8 @@ void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16) {
   p.m_units = (m_tiles + cta - 1) / cta;
   p.num_items = p.n_tiles * p.m_units;
   p.m_fast = 0;
+  p.dynamic = 1;
+  p.lockstep = 0;
   // tail-wave split: items beyond the last full wave of `units` CTAs (pairs)
   // run as two frame pieces (widths multiples of 32: the epilogue drains
   // 16-column chunks per column half)
@@ -1544,6 +1587,7 @@ static cudaError_t conventional_tc(const void* psi_hi, const void* psi_lo, bool 
   p.keys = keys;
   p.argmax_out = argmax_out;
   p.done = done;
+  lockstep_items(p, pair);
   p.tau_i = tau_i;
   p.tau_f = tau_f;
   p.period = period;
@@ -1643,6 +1687,8 @@ cudaError_t launch_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, 
   enforce_fold_window(p);
   // candidate tiles fastest: the CTAs in flight share one frame tile's Xi
   // rows in L2 instead of streaming every frame tile's
+  // (dynamic items: the tile's Xi rows fit L2, 92 MB at C4; measured with
+  // the static lockstep schedule: 2.13 vs 2.06 s per C4 step)
   p.m_fast = getenv("SRPB_OTF_NFAST") ? 0 : 1;
   p.scale = 1.0f / (kF16PhaseScale * xi_scale);
   p.maps = maps;

@@ -77,7 +77,8 @@ class SrpMap:
     on the device keep the fused argmax and fetch values lazily.
     """
 
-    def __init__(self, values, method, frame_index=0, _rows=None, _row=0, _argmax=None):
+    def __init__(self, values, method, frame_index=0, _rows=None, _row=0, _argmax=None,
+                 _num=None):
         self.method = method
         self.frame_index = frame_index
         # fused device argmax: an int, or (_DeviceRows of [F] indices, row)
@@ -86,6 +87,8 @@ class SrpMap:
         if _rows is not None:
             self._rows, self._row, self._host = _rows, _row, None
             self._n = int(_rows.tensor.shape[1])
+        elif values is None and _argmax is not None:  # argmax-only (maps=False)
+            self._rows, self._row, self._host, self._n = None, _row, None, int(_num or 0)
         else:
             v = np.asarray(values, dtype=float)
             if v.ndim != 1 or v.size == 0:
@@ -95,6 +98,9 @@ class SrpMap:
     @property
     def values(self) -> np.ndarray:
         if self._host is None:
+            if self._rows is None:
+                raise ValueError("map values were not materialised (maps=False); "
+                                 "only argmax_candidate is available")
             self._host = self._rows.host()[self._row]
         return self._host
 
@@ -408,7 +414,7 @@ def srp_approx_frames(lattices, table, counter=None, maps=True):
     mrows = _DeviceRows(out, np.float64) if out is not None else None
     arows = _DeviceRows(am, np.int64)
     return [SrpMap(None, "approximated", frame_index=l.frame_index, _rows=mrows, _row=i,
-                   _argmax=(arows, i)) for i, l in enumerate(lattices)]
+                   _argmax=(arows, i), _num=plan.J) for i, l in enumerate(lattices)]
 
 
 def srp_approx(lattice, table, counter=None) -> SrpMap:
@@ -465,7 +471,7 @@ def srp_conventional_frames(frames, grid, counter=None, maps=True) -> list:
     mrows = _DeviceRows(out, np.float64) if out is not None else None
     arows = _DeviceRows(am, np.int64)
     return [SrpMap(None, "conventional", frame_index=fr.frame_index, _rows=mrows, _row=i,
-                   _argmax=(arows, i)) for i, fr in enumerate(frames)]
+                   _argmax=(arows, i), _num=plan.J) for i, fr in enumerate(frames)]
 
 
 def srp_conventional(cross, grid, counter=None) -> SrpMap:

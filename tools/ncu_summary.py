@@ -36,7 +36,7 @@ def main(path):
                 # normalise to base units before scaling
                 mult = {"ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9, "nsecond": 1, "usecond": 1e3,
                         "msecond": 1e6, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
-                        "Gbyte": 1e9}.get(u, 1)
+                        "Gbyte": 1e9, "Tbyte": 1e12}.get(u, 1)
                 x = x * mult * sc
                 cells.append(f"{lab}={x:.4g}")
             except ValueError:
