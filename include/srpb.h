@@ -42,6 +42,11 @@ int srpb_abi_version(void);
 /* Message of the last failing call on the calling thread ("" if none). */
 const char* srpb_last_error(void);
 
+/* Kernels launched by the calling thread's last srpb_gcc_phat /
+ * srpb_gcc_phat_split16 (1 for the frame-resident speculative pass with the
+ * relative PHAT floor, else 2).  Bookkeeping for launch counts (ABI v13). */
+int srpb_last_gcc_kernels(void);
+
 /*
  * Plan build on the device: candidate TDOAs (geometry.build_tdoa_table,
  * geometry.py:365-398; near field |q - p_m| - |q - p_m'| over c, far field

@@ -18,7 +18,7 @@ _lib = None
 #: the C ABI revision these signatures describe (include/srpb.h); load()
 #: refuses a library of another revision instead of calling it with
 #: mismatched arguments
-ABI_VERSION = 12
+ABI_VERSION = 13
 
 c_int, c_double, c_void_p = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
 
@@ -26,6 +26,7 @@ c_int, c_double, c_void_p = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
 _SIGNATURES = {
     "srpb_abi_version": [],
     "srpb_last_error": [],
+    "srpb_last_gcc_kernels": [],
     "srpb_tdoa_split": [c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
                         c_double, c_double, c_int, c_double, c_void_p, c_double, c_void_p,
                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
@@ -145,13 +146,15 @@ def stream_handle(device=None):
 
 
 _LAUNCHING = {n for n in _SIGNATURES if n not in ("srpb_abi_version", "srpb_last_error",
+                                                   "srpb_last_gcc_kernels",
                                                    "srpb_lattice_tc_cols",
                                                    "srpb_lattice_tc_supported",
                                                    "srpb_copy_rows_h2d")}
-# entry points that launch more than one kernel (floor/fill pass + psi pass;
-# speculative-floor lattice + its fix-up pass)
-_KERNELS_PER_CALL = {"srpb_gcc_phat": 2, "srpb_gcc_phat_split16": 2, "srpb_lattice_from_spectra": 2,
-                     "srpb_lattice_from_spectra_tc": 2, "srpb_map_error": 2}
+# entry points that launch more than one kernel (speculative-floor lattice +
+# its fix-up pass); the GCC-PHAT entries report theirs (srpb_last_gcc_kernels)
+_KERNELS_PER_CALL = {"srpb_lattice_from_spectra": 2, "srpb_lattice_from_spectra_tc": 2,
+                     "srpb_map_error": 2}
+_GCC = ("srpb_gcc_phat", "srpb_gcc_phat_split16")
 _launches = 0
 
 
@@ -181,7 +184,9 @@ def call(name, *args):
     global _launches
     lib = load()
     rc = getattr(lib, name)(*args)
-    if name in _LAUNCHING:
+    if name in _GCC:
+        _launches += int(lib.srpb_last_gcc_kernels()) if rc == 0 else 0
+    elif name in _LAUNCHING:
         _launches += _KERNELS_PER_CALL.get(name, 1)
     if rc != 0:
         msg = lib.srpb_last_error().decode(errors="replace")

@@ -14,6 +14,7 @@ cudaError_t launch_stft(const float*, int, int, int, int, int, int, float*, cuda
 cudaError_t launch_tdoa_split(const double*, const double*, int, const int32_t*, const int32_t*,
                               int, int, double, double, int, double, const double*, double,
                               int32_t*, float*, int32_t*, float*, double*, int*, cudaStream_t);
+int gcc_phat_last_kernels();
 cudaError_t launch_gcc_floor(const float*, int, int, int, const int32_t*, const int32_t*, int,
                              double, double*, int32_t*, cudaStream_t);
 cudaError_t launch_lattice_from_spectra(const float*, int, int, int, const int32_t*,
@@ -103,7 +104,11 @@ static bool pow2_scale(float s) {
   return s > 0.0f && std::isfinite(s) && std::frexp(s, &e) == 0.5f;
 }
 
-int srpb_abi_version(void) { return 12; }
+int srpb_abi_version(void) { return 13; }
+
+// kernels launched by this thread's last srpb_gcc_phat / srpb_gcc_phat_split16
+// call (1: the frame-resident single pass; 2: two-pass or row pass + fix-up)
+int srpb_last_gcc_kernels(void) { return srpb::gcc_phat_last_kernels(); }
 
 const char* srpb_last_error(void) { return g_err; }
 

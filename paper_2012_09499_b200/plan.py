@@ -451,7 +451,13 @@ class SrpPlan:
 
     @property
     def xi_scale16(self):
-        return 2.0 ** math.floor(math.log2(60000.0 / (2.0 * self.Kb)))
+        return self.f16_scale_for_bins(self.Kb)
+
+    @staticmethod
+    def f16_scale_for_bins(kb):
+        """Power-of-two prescale keeping PHAT lattice samples (|xi| <= 2 kb)
+        inside fp16's range."""
+        return 2.0 ** math.floor(math.log2(60000.0 / (2.0 * max(int(kb), 1))))
 
     def split_f16(self, x, scale):
         """(hi, lo) fp16 split of scale * x (float32/complex64 tensor)."""
@@ -530,8 +536,9 @@ class SrpPlan:
     @_on_plan_device
     def approx(self, xi, maps=True, maps_out=None, bounded=False):
         """K4 (+ fused K5): Xi [F, T_pad] -> (maps [F, J] | None, argmax [F]).
-        ``bounded``: the samples come from PHAT cross-spectra (|xi| <= 2 Kb),
-        so the 3xFP16 tensor-core kernel (argmax finished in-kernel) applies."""
+        ``bounded``: False, or the bin count Kb' of the PHAT cross-spectra the
+        samples come from (|xi| <= 2 Kb'): then the 3xFP16 tensor-core kernel
+        (argmax finished in-kernel) applies with a prescale for that bound."""
         if self.sample_period is None:
             raise ValueError("plan was built without a lattice (sample_period)")
         self._check_frames(xi, (self.T_pad,), torch.float32, "xi")
@@ -540,9 +547,10 @@ class SrpPlan:
         if maps:
             out = maps_out if maps_out is not None else torch.empty(
                 (F, self.J), dtype=torch.float32, device=self.device)
-        if self._f16_ok("interp", bounded) and self._use_tc(F, "interp16"):
-            xh, xl = self.split_f16(xi, self.xi_scale16)
-            return self._approx_tc16(xh, xl, out)
+        if bounded and self._f16_ok("interp", True) and self._use_tc(F, "interp16"):
+            scale = self.f16_scale_for_bins(int(bounded))
+            xh, xl = self.split_f16(xi, scale)
+            return self._approx_tc16(xh, xl, out, xi_scale=scale)
         keys = self._keys(F)
         s = N.stream_handle(self.device)
         if self._use_tc(F, "interp"):
@@ -556,23 +564,23 @@ class SrpPlan:
                    N.ptr(out), N.ptr(keys), s)
         return out, self.keys_to_index(keys)
 
-    def _approx_tc16(self, xh, xl, out):
+    def _approx_tc16(self, xh, xl, out, xi_scale=None):
         """K4 in 3xFP16 from the fp16 split of xi_scale16 * Xi (weights from
         the stored W split, or generated in tensor memory when W is not
         stored); argmax finished in-kernel."""
         F = xh.shape[0]
+        xs = self.xi_scale16 if xi_scale is None else xi_scale
         keys, done = self._argmax_state(F)
         idx = torch.empty(F, dtype=torch.int32, device=self.device)
         if self.W is None:
             self._main("srpb_interp_tc16_onthefly", N.ptr(self.sx_i), N.ptr(self.sx_f), self.P,
                        N.ptr(self.off), N.ptr(self.reach), N.ptr(xh), N.ptr(xl),
-                       self.xi_scale16, F, self.J, self.T_pad, N.ptr(out), N.ptr(keys),
+                       xs, F, self.J, self.T_pad, N.ptr(out), N.ptr(keys),
                        self.interp_kb_per_group16, N.ptr(idx), N.ptr(done),
                        N.stream_handle(self.device))
             return out, idx
         if self.W16 is None:
             self.W16 = self.split_f16(self.W, self.F16_UNIT_SCALE)
-        xs = self.xi_scale16
         self._main("srpb_interp_tc16", N.ptr(self.W16[0]), N.ptr(self.W16[1]),
                    self.F16_UNIT_SCALE, N.ptr(xh), N.ptr(xl), xs, F, self.J, self.T_pad,
                    N.ptr(out), N.ptr(keys), self.interp_kb_per_group16, N.ptr(idx), N.ptr(done),

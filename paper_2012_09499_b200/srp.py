@@ -190,9 +190,9 @@ class GccLattice:
 
     def __init__(self, sample_period, n_aux, half_counts, samples=None, frame_index=0,
                  _rows=None, _row=0, _plan=None, _bounded=False):
-        # _bounded: device samples of PHAT cross-spectra, |xi| <= 2 Kb (the
-        # 3xFP16 interpolation's operand bound)
-        self._bounded = bool(_bounded)
+        # _bounded: 0, or Kb of the PHAT cross-spectra the device samples come
+        # from (|xi| <= 2 Kb: the 3xFP16 interpolation's operand bound)
+        self._bounded = int(_bounded)
         self.sample_period = float(sample_period)
         self.n_aux = int(n_aux)
         self.half_counts = tuple(int(h) for h in half_counts)
@@ -250,7 +250,7 @@ class GccLattice:
         flat[0, :cat.size] = cat
         t = torch.as_tensor(flat, device=dev)
         self._rows, self._row = _DeviceRows(t, np.float64), 0
-        self._bounded = False
+        self._bounded = 0
         return t[0]
 
 
@@ -293,7 +293,9 @@ def build_gcc_lattice_frames(crosses, sample_period, n_aux, counter=None, device
     if counter is not None:
         for _ in crosses:
             counter.add_complex(total * crosses[0].num_bins)
-    bounded = all(getattr(c, "weighting", None) == "phat" for c in crosses)
+    # PHAT samples are bounded by 2 Kb (Kb of these cross-spectra)
+    bounded = crosses[0].num_bins if all(
+        getattr(c, "weighting", None) == "phat" for c in crosses) else 0
     return [
         GccLattice(sample_period, n_aux, halves, frame_index=c.frame_index, _rows=rows, _row=i,
                    _plan=plan, _bounded=bounded)
@@ -406,7 +408,8 @@ def srp_approx_frames(lattices, table, counter=None, maps=True):
             xi = xi[torch.as_tensor(idx, device=dev)].contiguous()
     else:
         xi = torch.stack([l.device_row(plan.T_pad, dev) for l in lattices]).contiguous()
-    bounded = all(getattr(l, "_bounded", False) for l in lattices)
+    kbs = {getattr(l, "_bounded", 0) for l in lattices}
+    bounded = kbs.pop() if len(kbs) == 1 else 0  # one bound for the batch
     out, am = plan.approx(xi, maps=maps, bounded=bounded)
     if counter is not None:
         for _ in lattices:

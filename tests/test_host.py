@@ -38,7 +38,7 @@ def test_library_exports_every_header_symbol():
 
 def test_abi_version_and_error_reporting_without_gpu():
     lib = _native.load()
-    assert lib.srpb_abi_version() == 12
+    assert lib.srpb_abi_version() == 13
     # invalid arguments are rejected on the host before any CUDA call
     with pytest.raises(ValueError, match="bad shape"):
         _native.call("srpb_gcc_phat", None, -1, 4, 64, None, None, 6, 0, 1e-12, -1.0, None, None,

@@ -420,7 +420,7 @@ def test_captured_step_and_chunked_runner_match_eager():
         ref_maps, ref_am = plan.run(dev(Y), path)
         cap = plan.capture(Y.shape[0], Y.shape[1], path)
         m, a = cap.replay(dev(Y))
-        assert cap.launches >= 3
+        assert cap.launches >= 2
         assert torch.equal(m, ref_maps) and torch.equal(a, ref_am)
         m2, a2 = cap.replay()  # replays are repeatable
         assert torch.equal(m2, ref_maps) and torch.equal(a2, ref_am)
@@ -694,4 +694,5 @@ def test_conventional_fused_split_equals_two_step():
     m2, a2 = plan.conventional(psi, _bounded=True)  # PHAT psi: the 3xFP16 K2 as well
     two = NN.launch_count() - n0
     assert torch.equal(m1, m2) and torch.equal(a1, a2)
-    assert fused == 3 and two == 2  # floor + psi16 + K2 vs split + K2 (after K1's 2)
+    # K1's frame-resident single pass (floor, psi16) + K2 vs split + K2 (after K1)
+    assert fused == 2 and two == 2

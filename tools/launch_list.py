@@ -14,7 +14,7 @@ def main(path, skip=0):
     rows = list(csv.reader(lines))
     h = rows[0]
     kn, mv, mu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}
+    scale = {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}
     agg = collections.OrderedDict()
     for r in rows[1 + skip:]:
         name = r[kn].split("(")[0].strip()
