@@ -417,7 +417,7 @@ __device__ __forceinline__ void lattice_run(const LatticeArgs& a, const LatticeW
     s_min[warp * 32 + lane] = st.min;
     s_bad[warp * 32 + lane] = st.bad;
     __syncthreads();
-    if (blockIdx.z == 0 && threadIdx.x < 32 && threadIdx.x < fv) {
+    if (blockIdx.x == 0 && threadIdx.x < 32 && threadIdx.x < fv) {  // half-lag group 0
       float sum = 0.0f, mn = 3.0e38f;
       int bad = 0;
 #pragma unroll
@@ -452,13 +452,16 @@ template <bool kFromY, bool kTma>
 __global__ void __launch_bounds__(kLatThreads, 2)
 lattice_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant__ CUtensorMap tm_tw,
                const LatticeArgs a) {
-  const int p = blockIdx.x;
-  const int f0 = blockIdx.y * kLatF;
+  // grid (half-lag group, pair, frame tile): the half-lag groups of one
+  // (pair, frame tile) are adjacent in launch order and share its spectra in
+  // L2 (C4: 19 groups -- pair-fastest order re-read Y from DRAM per group)
+  const int p = blockIdx.y;
+  const int f0 = blockIdx.z * kLatF;
   const int tid = threadIdx.x;
   if (p == a.P) {  // pad-column zero fill for this frame tile
     const int t0 = __ldg(a.off + a.P);
     const int w = a.T_pad - t0;
-    if (blockIdx.z != 0 || w <= 0) return;
+    if (blockIdx.x != 0 || w <= 0) return;
     for (int e = tid; e < kLatF * w; e += blockDim.x) {
       const int fl = e / w, t = t0 + e - fl * w;
       if (f0 + fl < a.F) lattice_store(a, static_cast<size_t>(f0 + fl) * a.T_pad + t, 0.0f);
@@ -466,7 +469,7 @@ lattice_kernel(const __grid_constant__ CUtensorMap tm_src, const __grid_constant
     return;
   }
   const int R = __ldg(a.reach + p);
-  const int hl0 = blockIdx.z * kLatHl;
+  const int hl0 = blockIdx.x * kLatHl;
   if (hl0 > R) return;
 
   extern __shared__ __align__(1024) uint8_t s_lat_raw[];
@@ -689,7 +692,7 @@ static cudaError_t launch_lattice_kernel(const CUtensorMap& tm_src, const CUtens
 static cudaError_t launch_lattice_args(const LatticeArgs& a, bool from_y, int max_Tp,
                                       cudaStream_t stream) {
   const int max_reach = (max_Tp - 1) / 2;
-  dim3 grid(a.P + 1, (a.F + kLatF - 1) / kLatF, max_reach / kLatHl + 1);
+  dim3 grid(max_reach / kLatHl + 1, a.P + 1, (a.F + kLatF - 1) / kLatF);
   // TMA staging: 3-D map over the source rows [F][rows][Kb] of 8-byte
   // complex elements (box 4 bins x 1 row x 32 frames, 32-byte swizzle) and a
   // 2-D map over the twiddles [Kb][Hs] (box 16 half-lags x 4 bins); needs
