@@ -99,6 +99,22 @@ def canonical(mic_pos):
             np.array([p.tdoa_bound for p in pairs]))
 
 
+N_AUX = 4  # C2's benchmarked N_aux (round-1 tools)
+
+
+def workload(rank=0):
+    """C2 (configs[1]) host inputs used by the tools/ scripts: scene, pair
+    rows, bounds, TDOA table (the package's geometry), bin frequencies."""
+    from paper_2012_09499_b200 import scenes
+    from paper_2012_09499_b200.geometry import CandidateGrid, MicArray, build_tdoa_table
+
+    scene = scenes.make_c2(scene_index=rank)
+    pm, pmp, bounds = canonical(scene.mic_pos)
+    grid = build_tdoa_table(MicArray(scene.mic_pos, C_SOUND),
+                            CandidateGrid("near_field", scene.grid))
+    return scene, pm, pmp, bounds, grid.tdoa_table, omega_of(scene.frame_length)
+
+
 def build_plan(scene, n_aux, dev, weights="auto", conventional=True):
     """Product plan from the scene geometry (device TDOAs and splits)."""
     from paper_2012_09499_b200.plan import SrpPlan

@@ -182,7 +182,7 @@ gcc_psi_spec_kernel(const float4* __restrict__ Y, int M, int Kb2, const int32_t*
 // frame's statistics in registers, reduces them in a fixed order, writes the
 // floor, and redoes the frame exactly from the staged spectra if needed:
 // one kernel, Y read once, psi written once (twice for a flagged frame).
-constexpr int kFrameThreads = 512;
+constexpr int kFrameThreads = 1024;
 template <bool kSplit>
 __global__ void __launch_bounds__(kFrameThreads)
 gcc_psi_frame_kernel(const float4* __restrict__ Y, int M, int Kb2, const int32_t* __restrict__ pm,
@@ -229,16 +229,40 @@ gcc_psi_frame_kernel(const float4* __restrict__ Y, int M, int Kb2, const int32_t
     if (pa != 0.0f && pb != 0.0f) mn = fminf(mn, pa * pb);
     bad |= !(phat_power_clean(pa) && phat_power_clean(pb));
   };
+  if (kSplit && !Psi && (Kb2 & 1) == 0) {
+    // split only: 4 bins per thread per step, 16-byte stores of hi and lo
+#pragma unroll 2
+    for (int e = 2 * threadIdx.x; e < n; e += 2 * kFrameThreads) {
+      const int p = pow2 ? e >> sh : e / Kb2;
+      const int k2 = e - p * Kb2;
+      const int2 ab = s_pair[p];
+      const float4 a0 = y_s[ab.x * Kb2 + k2], b0 = y_s[ab.y * Kb2 + k2];
+      const float4 a1 = y_s[ab.x * Kb2 + k2 + 1], b1 = y_s[ab.y * Kb2 + k2 + 1];
+      float2 ov[4];
+      one(make_float2(a0.x, a0.y), make_float2(b0.x, b0.y), ov[0]);
+      one(make_float2(a0.z, a0.w), make_float2(b0.z, b0.w), ov[1]);
+      one(make_float2(a1.x, a1.y), make_float2(b1.x, b1.y), ov[2]);
+      one(make_float2(a1.z, a1.w), make_float2(b1.z, b1.w), ov[3]);
+      uint4 h, l;
+      psi_split16(ov[0], scale, h.x, l.x);
+      psi_split16(ov[1], scale, h.y, l.y);
+      psi_split16(ov[2], scale, h.z, l.z);
+      psi_split16(ov[3], scale, h.w, l.w);
+      __stcs(reinterpret_cast<uint4*>(Psi_hi + o + e), h);
+      __stcs(reinterpret_cast<uint4*>(Psi_lo + o + e), l);
+    }
+  } else {
 #pragma unroll 4
-  for (int e = threadIdx.x; e < n; e += kFrameThreads) {
-    const int p = pow2 ? e >> sh : e / Kb2;
-    const int k2 = e - p * Kb2;
-    const int2 ab = s_pair[p];
-    const float4 a = y_s[ab.x * Kb2 + k2], b = y_s[ab.y * Kb2 + k2];
-    float2 o0, o1;
-    one(make_float2(a.x, a.y), make_float2(b.x, b.y), o0);
-    one(make_float2(a.z, a.w), make_float2(b.z, b.w), o1);
-    store(e, o0, o1);
+    for (int e = threadIdx.x; e < n; e += kFrameThreads) {
+      const int p = pow2 ? e >> sh : e / Kb2;
+      const int k2 = e - p * Kb2;
+      const int2 ab = s_pair[p];
+      const float4 a = y_s[ab.x * Kb2 + k2], b = y_s[ab.y * Kb2 + k2];
+      float2 o0, o1;
+      one(make_float2(a.x, a.y), make_float2(b.x, b.y), o0);
+      one(make_float2(a.z, a.w), make_float2(b.z, b.w), o1);
+      store(e, o0, o1);
+    }
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {

@@ -16,7 +16,6 @@ lib = _native.load(os.path.join(ROOT, "paper_2012_09499_b200", "libsrpb_prof.so"
 lib.srpb_lt_profile_read.argtypes = [ctypes.c_void_p]
 
 import bench  # noqa: E402
-from paper_2012_09499_b200.plan import SrpPlan  # noqa: E402
 
 NAMES = {0: "setup", 2: "mma_done(epi view)", 3: "generator loop (per gen warp)",
          4: "gen wait Y (per gen warp)", 5: "epi wait acc (per epi warp)",
@@ -24,8 +23,10 @@ NAMES = {0: "setup", 2: "mma_done(epi view)", 3: "generator loop (per gen warp)"
 
 
 def main():
-    scene, pm, pmp, bounds, tdoa, omega = bench.workload(0)
-    plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=bench.T, n_aux=bench.N_AUX)
+    from paper_2012_09499_b200 import scenes
+
+    scene = scenes.make_c2()
+    plan = bench.build_plan(scene, 4, torch.device("cuda", 0), weights="stored")
     Y = torch.from_numpy(scene.Y).cuda()
     for _ in range(2):
         plan.lattice_from_spectra(Y, split="f16")
