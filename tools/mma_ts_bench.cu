@@ -9,11 +9,12 @@
 using namespace srpb::umma;
 
 template <bool kTS>
-__global__ void __launch_bounds__(128, 1) bench(int N, int iters, unsigned long long* out, int mode) {
+__global__ void __launch_bounds__(384, 1) bench(int N, int iters, unsigned long long* out, int mode) {
   __shared__ uint64_t sbar[4];
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar;
+  __shared__ uint64_t spin_done;
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x >> 5;
   const int a_bytes = 128 * 128, b_bytes = N * 128;
@@ -27,6 +28,7 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int iters, unsigned long 
   if (threadIdx.x == 32) {
     for (int i = 0; i < 4; ++i) mbar_init(&sbar[i], 1);
     mbar_init(&bar, 1);
+    mbar_init(&spin_done, 1);
     fence_mbar_init();
   }
   fence_proxy_async_smem();
@@ -45,7 +47,7 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int iters, unsigned long 
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           const uint32_t o = 2 * ks;
-          if (mode == 2) {  // the K4/K2 pattern: lo*hi + hi*lo + hi*hi, A from TMEM
+          if (mode >= 2) {  // the K4/K2 pattern: lo*hi + hi*lo + hi*hi, A from TMEM
             const uint32_t ah = tmem + 2 * N + 64 * (s & 1) + 8 * ks, al = ah + 32;
             const uint32_t d = tmem + ((it / 10) & 1) * N;
             mma_f16_ts(d, al, db + o, idesc, (it % 10 > 0 || ks > 0) ? 1u : 0u);
@@ -65,9 +67,11 @@ __global__ void __launch_bounds__(128, 1) bench(int N, int iters, unsigned long 
     __syncwarp();
     mbar_wait(&bar, 0);
     const long long t1 = clock64();
+    if (threadIdx.x == 32) mbar_arrive(&spin_done);
     if (threadIdx.x == 32) atomicAdd(out, static_cast<unsigned long long>(t1 - t0));
   }
   tc_fence_before();
+  if (warp >= 4) mbar_wait(&spin_done, 0);  // mode 3: 8 warps poll a barrier throughout
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
@@ -86,15 +90,15 @@ int main(int argc, char** argv) {
       for (int rep = 0; rep < 2; ++rep) {
         cudaMemset(d, 0, 8);
         if (ts)
-          bench<true><<<148, 128, smem>>>(N, iters, d, mode);
+          bench<true><<<148, mode == 3 ? 384 : 128, smem>>>(N, iters, d, mode);
         else
-          bench<false><<<148, 128, smem>>>(N, iters, d, mode);
+          bench<false><<<148, mode == 3 ? 384 : 128, smem>>>(N, iters, d, mode);
         cudaError_t e = cudaDeviceSynchronize();
         unsigned long long h = 0;
         cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
         if (rep == 1)
           printf("mode %d %s N=%3d: %6.1f cycles/MMA (floor %.0f) %s\n", mode, ts ? "TS" : "SS", N,
-                 double(h) / 148.0 / ((mode == 2 ? 12.0 : 4.0) * iters), 128.0 * N / 256.0,
+                 double(h) / 148.0 / ((mode >= 2 ? 12.0 : 4.0) * iters), 128.0 * N / 256.0,
                  cudaGetErrorString(e));
       }
   }
