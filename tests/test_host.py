@@ -225,6 +225,40 @@ def test_chunk_bounds():
     assert chunk_bounds(100, 3) == [(0, 34), (34, 67), (67, 100)]
     b = chunk_bounds(1000, 7)
     assert b[0][0] == 0 and b[-1][1] == 1000 and all(x[1] == y[0] for x, y in zip(b, b[1:]))
+    # explicit chunk sizes (the C4 bench: tile multiples + a short last chunk)
+    assert chunk_bounds(4096, sizes=[1280, 1280, 1280, 256]) == [
+        (0, 1280), (1280, 2560), (2560, 3840), (3840, 4096)]
+    assert chunk_bounds(1000, sizes=[300, 300]) == [(0, 300), (300, 1000)]  # remainder joins
+    assert chunk_bounds(500, sizes=[300, 300, 300]) == [(0, 300), (300, 500)]  # clipped
+
+
+def test_srpmap_argmax_only_and_lazy_argmax():
+    """SrpMap without materialised values (maps=False drop-ins) reports its
+    argmax and refuses .values; the fused argmax is fetched lazily from the
+    shared device rows (no per-call host sync)."""
+    import numpy as np
+    import pytest
+
+    from paper_2012_09499_b200.spectral import _DeviceRows
+    from paper_2012_09499_b200.srp import SrpMap, argmax_candidate
+
+    class FakeTensor:  # the host copy is all _DeviceRows touches here
+        def __init__(self, a):
+            self.a = a
+
+        def cpu(self):
+            return self
+
+        def numpy(self):
+            return self.a
+
+    rows = _DeviceRows(FakeTensor(np.array([5, 1, 7])), np.int64)
+    m = SrpMap(None, "approximated", frame_index=2, _argmax=(rows, 2), _num=50)
+    assert argmax_candidate(m) == 7 and m.num_candidates == 50
+    with pytest.raises(ValueError, match="maps=False"):
+        _ = m.values
+    with pytest.raises(ValueError):
+        SrpMap(None, "x")  # neither values nor argmax
 
 
 def test_harness_install_rebinds_and_restores():

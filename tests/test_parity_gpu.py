@@ -696,3 +696,56 @@ def test_conventional_fused_split_equals_two_step():
     assert torch.equal(m1, m2) and torch.equal(a1, a2)
     # K1's frame-resident single pass (floor, psi16) + K2 vs split + K2 (after K1)
     assert fused == 2 and two == 2
+
+
+def test_concurrent_steps_of_one_plan_own_their_kernel_state():
+    """Two captured steps of the same plan and frame count, replayed
+    concurrently on two streams, and eager calls on a third: each owns its
+    argmax keys and item cursor (ADVICE: shared per-F state let concurrent
+    grids advance one cursor), so every result equals the serial one."""
+    g = load_golden("c2_subset")
+    Y = dev(np.concatenate([g["Y"]] * 12).astype(np.complex64))  # 36 frames
+    plan = plan_from_golden(g, 4, weights="stored", backend="tc")
+    for path in ("approx", "conventional"):
+        ref_m, ref_a = plan.run(Y, path)
+        c1 = plan.capture(Y.shape[0], Y.shape[1], path)
+        c2 = plan.capture(Y.shape[0], Y.shape[1], path)
+        c1.Y.copy_(Y)
+        c2.Y.copy_(Y)
+        torch.cuda.synchronize()
+        s1, s2, s3 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        eager = []
+        for _ in range(4):
+            with torch.cuda.stream(s1):
+                c1.replay()
+            with torch.cuda.stream(s2):
+                c2.replay()
+            with torch.cuda.stream(s3):
+                eager.append(plan.run(Y, path))
+        torch.cuda.synchronize()
+        for m, a in [(c1.maps, c1.argmax), (c2.maps, c2.argmax)] + eager:
+            assert torch.equal(m, ref_m) and torch.equal(a, ref_a), path
+
+
+def test_dropin_argmax_only_and_small_bin_tables():
+    """srp_approx_frames(..., maps=False) returns argmax-only maps equal to the
+    full maps' argmax; a sinc table built without bin frequencies takes the
+    fp16 prescale from the lattice's own bins (no overflow for Kb < 512)."""
+    g = load_golden("random_small")
+    arr = B.MicArray(g["mic_pos"], speed_of_sound=float(g["speed_of_sound"]))
+    grid = B.build_tdoa_table(arr, B.CandidateGrid("near_field", g["grid"]))
+    freqs = g["omega"]
+    frames = [B.SpectralFrame(g["Y"][f].astype(complex), freqs, frame_index=f)
+              for f in range(g["Y"].shape[0])]
+    crosses = B.cross_spectrum_frames(frames, arr.pairs)
+    lats = B.build_gcc_lattice_frames(crosses, T, 1)
+    table = B.precompute_sinc_table(grid, arr.pairs, T, 1)  # Kb-agnostic table plan
+    full = B.srp_approx_frames(lats, table)
+    am = B.srp_approx_frames(lats, table, maps=False)
+    got = np.stack([m.values for m in full])
+    assert_maps_match(got, g["approx_1"], [B.argmax_candidate(m) for m in full],
+                      what="drop-in approx (64 bins)")
+    for mf, ma in zip(full, am):
+        assert B.argmax_candidate(ma) == B.argmax_candidate(mf) == int(np.argmax(mf.values))
+        with pytest.raises(ValueError, match="maps=False"):
+            _ = ma.values
