@@ -70,6 +70,39 @@ __global__ void __launch_bounds__(384, 1) bench(int N, int iters, unsigned long 
     if (threadIdx.x == 32) mbar_arrive(&spin_done);
     if (threadIdx.x == 32) atomicAdd(out, static_cast<unsigned long long>(t1 - t0));
   }
+  if (warp >= 4 && mode == 4) {  // 8 warps issue ALU work (FFMA chains + MUFU) throughout
+    float x0 = threadIdx.x, x1 = x0 + 1.f, x2 = x0 + 2.f, x3 = x0 + 3.f;
+    while (!mbar_try_wait(smem_u32(&spin_done), 0)) {
+#pragma unroll 16
+      for (int i = 0; i < 64; ++i) {
+        x0 = fmaf(x0, 0.999f, 0.5f);
+        x1 = fmaf(x1, 0.999f, 0.5f);
+        x2 = __frcp_rn(x2 + 1.f);
+        x3 = fmaf(x3, 0.999f, x0);
+      }
+    }
+    if (x0 + x1 + x2 + x3 == 1234.5f) out[1] = 1;
+  } else if (warp >= 4 && (mode == 5 || mode == 6)) {
+    // 8 warps stream tcgen05.st (5) / tcgen05.ld (6) to the A columns of the
+    // stage the MMAs are not reading (columns 2N + 128.. : a third A slot)
+    const uint32_t q = static_cast<uint32_t>(warp & 3) << 21;  // lane quarter (<<16 * 32)
+    const uint32_t col = tmem + 2 * N + 128 + 16 * ((warp >> 2) & 1);
+    uint32_t r[16];
+    for (int i = 0; i < 16; ++i) r[i] = threadIdx.x * 16 + i;
+    while (!mbar_try_wait(smem_u32(&spin_done), 0)) {
+      for (int i = 0; i < 8; ++i) {
+        if (mode == 5) {
+          tmem_st16(col + q, r);
+          tmem_wait_st();
+        } else {
+          tmem_ld16(col + q, r);
+          tmem_wait_ld();
+          r[0] += r[15];
+        }
+      }
+    }
+    if (r[0] == 12345u) out[1] = 1;
+  }
   tc_fence_before();
   if (warp >= 4) mbar_wait(&spin_done, 0);  // mode 3: 8 warps poll a barrier throughout
   __syncthreads();
@@ -78,21 +111,21 @@ __global__ void __launch_bounds__(384, 1) bench(int N, int iters, unsigned long 
 
 int main(int argc, char** argv) {
   unsigned long long* d;
-  cudaMalloc(&d, 8);
+  cudaMalloc(&d, 16);
   for (int N : {128, 160}) {
     const int stage = 128 * 128 + N * 128;
     const size_t smem = 1024 + 4 * size_t(stage);
     cudaFuncSetAttribute(bench<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(bench<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int iters = argc > 1 ? atoi(argv[1]) : 4000;
-    for (int mode = (argc > 2 ? atoi(argv[2]) : 0); mode < (argc > 2 ? atoi(argv[2]) + 1 : 3); ++mode)
+    for (int mode = (argc > 2 ? atoi(argv[2]) : 0); mode < (argc > 2 ? atoi(argv[2]) + 1 : 7); ++mode)
     for (int ts = 0; ts < 2; ++ts)
       for (int rep = 0; rep < 2; ++rep) {
         cudaMemset(d, 0, 8);
         if (ts)
-          bench<true><<<148, mode == 3 ? 384 : 128, smem>>>(N, iters, d, mode);
+          bench<true><<<148, mode >= 3 ? 384 : 128, smem>>>(N, iters, d, mode);
         else
-          bench<false><<<148, mode == 3 ? 384 : 128, smem>>>(N, iters, d, mode);
+          bench<false><<<148, mode >= 3 ? 384 : 128, smem>>>(N, iters, d, mode);
         cudaError_t e = cudaDeviceSynchronize();
         unsigned long long h = 0;
         cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
