@@ -91,6 +91,19 @@ struct TcCfg {
   // generator modes keep the folded running totals in shared memory
   // (registers go to the A generator)
   static constexpr bool kTotSmem = kAMode != kAFromTma;
+  // Generator teams (on-the-fly K4, single-CTA tiles): two teams of 8
+  // generator warps take alternate K blocks, so two blocks' weights are in
+  // production at once (one team per block: the MMA waited on a single team
+  // ~20% of the time, tools/tc_probe_c4.py); each team folds and writes its
+  // own 16-column accumulator chunks straight from the shared totals.  Warp
+  // roles: generators 0..15 (TMEM lane quarter = warp % 4), TMA producer 16,
+  // MMA issuer 17.  Otherwise: producer 0, MMA 1, epilogue warps 4..11.
+  static constexpr int kTeams = kAMode == kASinc ? 2 : 1;
+  static constexpr int kGenW0 = kTeams == 2 ? 0 : kEpiWarp0;  // first epilogue / generator warp
+  static constexpr int kGenWarps = kEpiWarps * kTeams;
+  static constexpr int kProdWarp = kTeams == 2 ? kGenWarps : 0;
+  static constexpr int kMmaWarp = kTeams == 2 ? kGenWarps + 1 : 1;
+  static constexpr int kThreads = kTeams == 2 ? 32 * (kGenWarps + 2) : kTcThreads;
 };
 
 // Instrumentation build only (make prof -> libsrpb_prof.so, tools/tc_probe.py):
@@ -396,6 +409,84 @@ __device__ __forceinline__ void tc_write_tile(const TcParams& p, unsigned long l
   if (threadIdx.x == kEpiWarp0 * 32) {
     TCP_FLUSH(12, w_loop);
     TCP_FLUSH(13, w_flush);
+  }
+}
+
+// Team epilogue (generator teams): the warp of column half `half`, lane
+// quarter `quarter` writes the 16-column chunks it owns (c0, c0 + 2, ...)
+// straight from the shared running totals (zeroing them for the next tile):
+// scale, streaming stores, and the fused argmax -- per chunk the warp's 32
+// rows reduce to one key per column (a 16-column butterfly transpose-reduce),
+// the four quarters combine in shared memory (the team's named barrier) and
+// one global atomicMax per frame publishes it.
+__device__ __forceinline__ void tc_write_chunks(const TcParams& p, unsigned long long* tk,
+                                                float* tot_s, int m0, int n0, int nc, int quarter,
+                                                int half, int lane, int team, int c0, int cstep,
+                                                int et) {
+  const int J = p.J;
+  const uint32_t jbase = static_cast<uint32_t>(m0 + 32 * quarter);
+  const int j = static_cast<int>(jbase) + lane;
+  const int ncols = nc / 2;
+  const int cbase = half * ncols;
+  const int nv = max(0, min(ncols, p.F - (n0 + cbase)));  // columns with f < F
+  const int lim = j < J ? nv : 0;
+  const unsigned long long low = static_cast<unsigned long long>(0xFFFFFFFFu - (jbase + lane));
+  for (int c = c0; 16 * c < ncols; c += cstep) {
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v[i] = tot_s[(16 * c + i) * kTcM] * p.scale;
+      tot_s[(16 * c + i) * kTcM] = 0.0f;
+    }
+    if (p.maps) {
+      float* ptr = p.maps + (static_cast<size_t>(n0 + cbase + 16 * c) * J + j);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        st_cs_pred(ptr, v[i], 16 * c + i < lim);
+        ptr += J;
+      }
+    }
+    if (p.keys) {
+      unsigned long long k[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        k[i] = 16 * c + i < lim ? (static_cast<unsigned long long>(orderable_bits(v[i])) << 32) | low
+                                : 0ull;
+      // lane halves first (no transpose), then a 16-column transpose-reduce:
+      // lane l < 16 ends holding column l
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const unsigned long long r = __shfl_xor_sync(0xffffffffu, k[i], 16);
+        k[i] = k[i] > r ? k[i] : r;
+      }
+#pragma unroll
+      for (int o = 8, n = 8; o >= 1; o >>= 1, n >>= 1) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const unsigned long long keep = up ? k[i + n] : k[i];
+          const unsigned long long send = up ? k[i] : k[i + n];
+          const unsigned long long recv = __shfl_xor_sync(0xffffffffu, send, o);
+          k[i] = keep > recv ? keep : recv;
+        }
+      }
+      if (lane < 16 && 16 * c + lane < ncols) tk[quarter * kTcMaxN + cbase + 16 * c + lane] = k[0];
+    }
+  }
+  if (p.keys) {
+    // the team's four quarters of each owned column -> one atomic per frame
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "n"(kEpiWarps * 32) : "memory");
+    for (int col = et; col < nc; col += kEpiWarps * 32) {
+      const int h = col >= ncols ? 1 : 0;
+      const int c = (col - h * ncols) >> 4;
+      if (((c + h) & 1) != team && cstep == 2) continue;  // the other team's chunk
+      unsigned long long k = tk[col];
+#pragma unroll
+      for (int q = 1; q < 4; ++q) k = key_max(k, tk[q * kTcMaxN + col]);
+      const int f = n0 + col;
+      if (k != 0ull && f < p.F) atomicMax(p.keys + f, k);
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "n"(kEpiWarps * 32) : "memory");  // tk reusable
   }
 }
 
@@ -766,7 +857,7 @@ struct SincGen {
 };
 
 template <int kAMode, bool kPair, bool kF16>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__((TcCfg<kAMode, kPair, kF16>::kThreads), 1)
 srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
               const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
               const __grid_constant__ CUtensorMap tmMaps, const TcParams p) {
@@ -776,6 +867,11 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   // their TMEM A ring
   const int S = p.stages;
   constexpr bool kASmem = Cfg::kASmem;
+  constexpr int kTeams = Cfg::kTeams;
+  constexpr int kGenW0 = Cfg::kGenW0;
+  constexpr int kGenWarps = Cfg::kGenWarps;
+  constexpr int kProdWarp = Cfg::kProdWarp;
+  constexpr int kMmaWarp = Cfg::kMmaWarp;
   constexpr int KBE = Cfg::kKbElems;
   constexpr int kCta = kPair ? 2 : 1;
 #ifdef SRPB_TC_PROFILE
@@ -889,7 +985,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   auto b_hi = [&](int s) { return smem + s * stage_bytes + a_bytes; };
   auto b_lo = [&](int s) { return smem + s * stage_bytes + a_bytes + b_bytes; };
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kProdWarp && lane == 0) {
     tma_prefetch(&tmB_hi);
     tma_prefetch(&tmB_lo);
     if (kASmem) {
@@ -897,16 +993,17 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       tma_prefetch(&tmA_lo);
     }
   }
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     if (kPair)
       tmem_alloc_pair(&bar->tmem_base, 512);
     else
       tmem_alloc(&bar->tmem_base, 512);
   }
-  if (warp == 2 && lane == 0) {
-    // full: producers (x kCta) + K2 A-generator warps (x kCta) arrive on the
-    // leader's barrier; empty / acc_full: one commit from the leader's MMA;
-    // acc_empty: the epilogue warps of both CTAs arrive on the leader's.
+  if (warp == kProdWarp && lane == 1) {
+    // full: producers (x kCta) + one team of A-generator warps (x kCta)
+    // arrive on the leader's barrier; empty / acc_full: one commit from the
+    // leader's MMA; acc_empty: the epilogue warps of both CTAs arrive on the
+    // leader's.
     const int full_count = kCta * (1 + (kAMode != kAFromTma ? kEpiWarps : 0));
     for (int s = 0; s < S; ++s) {
       mbar_init(&bar->full[s], full_count);
@@ -914,13 +1011,13 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bar->acc_full[b], 1);
-      mbar_init(&bar->acc_empty[b], kCta * kEpiWarps);
+      mbar_init(&bar->acc_empty[b], kCta * kGenWarps);
     }
     // item ring: the leader producer fills every CTA's slot; consumers are the
     // MMA issuer, all epilogue warps and the peer's producer
     for (int r = 0; r < kItemRing; ++r) {
       mbar_init(&bar->item_full[r], 1);
-      mbar_init(&bar->item_empty[r], 1 + kCta * kEpiWarps + (kCta - 1));
+      mbar_init(&bar->item_empty[r], 1 + kCta * kGenWarps + (kCta - 1));
     }
     if (!Cfg::kEpiStage)
       for (int c = 0; c < 4 * kTcMaxN; ++c) tile_keys[c] = 0ull;
@@ -944,7 +1041,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   const uint32_t acc_empty_addr0 =
       kPair ? mapa(&bar->acc_empty[0], 0) : smem_u32(&bar->acc_empty[0]);
 
-  if (warp == 0) {
+  if (warp == kProdWarp) {
     // ------------------------------------------------------------ TMA producer
     // warp-wide loop, one elected lane issues (uniform operands, no per-issue
     // register broadcasts)
@@ -1014,8 +1111,10 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
           } else {
             mbar_expect_tx(&bar->full[s], (TC_DBG(p) & 256) ? 0u : tx);
             for (int r = 0; r < rows && !(TC_DBG(p) & 256); r += p.b_box) {
-              tma_load_2d(b_hi(s) + r * 128, &tmB_hi, &bar->full[s], kb * KBE, nb + r);
-              tma_load_2d(b_lo(s) + r * 128, &tmB_lo, &bar->full[s], kb * KBE, nb + r);
+              // (bound analysis: 32 = every block loads K block 0's B)
+              const int kx = (TC_DBG(p) & 32) ? 0 : kb * KBE;
+              tma_load_2d(b_hi(s) + r * 128, &tmB_hi, &bar->full[s], kx, nb + r);
+              tma_load_2d(b_lo(s) + r * 128, &tmB_lo, &bar->full[s], kx, nb + r);
             }
             if (kASmem && !(TC_DBG(p) & 256)) {
               tma_load_2d(a_hi(s), &tmA_hi, &bar->full[s], kb * KBE, m0);
@@ -1035,7 +1134,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       TCP_FLUSH(3, w_empty);
       TCP_FLUSH(4, t_all);
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------- MMA issuer
     // warp-wide loop (leader CTA only for pairs); descriptors are base +
     // byte-offset>>4 arithmetic on uniform values; one elected lane issues
@@ -1152,11 +1251,16 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
         TCP_FLUSH(11, 1);
       }
     }
-  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
-    // ------------------------------------- epilogue (+ A generation for K2)
-    const int e = warp - kEpiWarp0;  // 0..7
-    const int quarter = warp & 3;    // TMEM lane quarter this warp may access
-    const int half = e >> 2;         // column half of the tile
+  } else if (warp >= kGenW0 && warp < kGenW0 + kGenWarps) {
+    // ---------------------- epilogue (+ A generation for the generator modes)
+    const int e = warp - kGenW0;       // 0..8 kTeams - 1
+    const int team = e >> 3;           // generator team: K blocks kg = team (mod kTeams)
+    const int quarter = warp & 3;      // TMEM lane quarter this warp may access
+    const int half = (e >> 2) & 1;     // column half of the tile
+    // accumulator chunks (16 columns of this half) folded and written by this
+    // warp: all of them, or with two teams every other one (alternating
+    // between the halves so each team owns half of the tile's columns)
+    const int c0 = kTeams == 2 ? ((team + half) & 1) : 0;
     float tot[kTcMaxN / 2];
 #pragma unroll
     for (int i = 0; i < kTcMaxN / 2; ++i) tot[i] = 0.0f;
@@ -1183,20 +1287,26 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // generator modes: this thread's slice of the shared running totals
     float* tot_s = tot_smem + half * (kTcMaxN / 2) * kTcM + 32 * quarter + lane;
     if constexpr (Cfg::kTotSmem) {
-#pragma unroll 8
-      for (int i = 0; i < kTcMaxN / 2; ++i) tot_s[i * kTcM] = 0.0f;
+      for (int c = c0; c < kTcMaxN / 32; c += kTeams)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) tot_s[(16 * c + i) * kTcM] = 0.0f;
     }
     auto finish_group = [&](const Item& t) {
       if (d_gl == p.groups_per_tile - 1) {
         TCP_T0();
-        if constexpr (Cfg::kTotSmem) {
+        if constexpr (kTeams == 2) {
+          tc_write_chunks(p, tile_keys, tot_s, t.m0, t.n0, t.nc, quarter, half, lane, team, c0,
+                          kTeams, (e & 7) * 32 + lane);
+        } else {
+          if constexpr (Cfg::kTotSmem) {
 #pragma unroll
-          for (int i = 0; i < kTcMaxN / 2; ++i) {
-            tot[i] = tot_s[i * kTcM];
-            tot_s[i * kTcM] = 0.0f;
+            for (int i = 0; i < kTcMaxN / 2; ++i) {
+              tot[i] = tot_s[i * kTcM];
+              tot_s[i * kTcM] = 0.0f;
+            }
           }
+          tc_write_tile(p, tile_keys, t.m0, t.n0, t.nc, quarter, half, lane, tot);
         }
-        tc_write_tile(p, tile_keys, t.m0, t.n0, t.nc, quarter, half, lane, tot);
         TCP_ACC(c_write);
         item_release(d_it);
         ++d_it;
@@ -1223,11 +1333,14 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
         tc_fence_after();
         d_base = tmem + (static_cast<uint32_t>(32 * quarter) << 16) +
                  static_cast<uint32_t>(b * p.N + half * (t.nc / 2));
-        d_chunk = 0;
+        d_chunk = c0;
       }
       // (shared-memory totals: the chunk is a runtime offset, one code copy)
-      tc_drain_chunk16_smem(d_base, tot_s, d_chunk, TC_DBG(p));
-      if (++d_chunk == t.nc / 32) {  // group folded: release the buffer
+      if (d_chunk < t.nc / 32) {
+        tc_drain_chunk16_smem(d_base, tot_s, d_chunk, TC_DBG(p));
+        d_chunk += kTeams;
+      }
+      if (d_chunk >= t.nc / 32) {  // this warp's chunks folded: release its share
         tc_fence_before();
         __syncwarp();
         if ((threadIdx.x & 31) == 0) {
@@ -1250,7 +1363,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       { TCP_T0();
       tc_drain(p, bar, !leader, acc_empty_addr0, tmem, drained, t.nc, quarter, half, tot);
       TCP_ACC(c_drain); }
-      if (warp == kEpiWarp0 && lane == 0) TCT(d_it, 3);
+      if (warp == kGenW0 && lane == 0) TCT(d_it, 3);
       if (d_gl == p.groups_per_tile - 1) {
         TCP_T0();
         if constexpr (Cfg::kEpiStage)
@@ -1259,7 +1372,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
         else
           tc_write_tile(p, tile_keys, t.m0, t.n0, t.nc, quarter, half, lane, tot);
         TCP_ACC(c_write);
-        if (warp == kEpiWarp0 && lane == 0) TCT(d_it, 4);
+        if (warp == kGenW0 && lane == 0) TCT(d_it, 4);
         item_release(d_it);
         ++d_it;
         d_gl = 0;
@@ -1278,7 +1391,9 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
       using Gen = typename std::conditional<kAMode == kASinc, SincGen, PhaseGen<kF16>>::type;
       Gen gen;
-      int kg = 0, s = 0, ph = 0;  // stage ring position
+      // global K block kg (across items) and its stage ring position; a team
+      // takes every kTeams-th block (S >= 2 >= kTeams)
+      int kg = team, s = team, ph = 0;
       int n_items = 0;            // items seen so far (the fold trails them)
       for (int it = 0;; ++it) {
         const int gid = item_id(it);
@@ -1289,7 +1404,9 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
           gen.start_tile(p, j, pair_cols);
         else
           gen.start_tile(p);
-        for (int kb = 0; kb < p.num_kb; ++kb, ++kg) {
+        const int kg_base = it * p.num_kb;
+        for (; kg < kg_base + p.num_kb; kg += kTeams) {
+          const int kb = kg - kg_base;
           { TCP_T0();
           mbar_wait(&bar->empty[s], ph ^ 1);
           TCP_ACC(c_gen_wait); }
@@ -1297,7 +1414,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
           tc_fence_after();  // MMAs that read this stage have completed
           const uint32_t a_col = lane_base + static_cast<uint32_t>(tc_a_tmem_col(p.N, s));
           if constexpr (kAMode == kASinc)
-            gen.block(p, j, half, kb, a_col, a_col + 32);
+            gen.block(p, j, half, (TC_DBG(p) & 64) ? 0 : kb, a_col, a_col + 32);  // 64: A of block 0
           else
             gen.block(p, j, half, a_col, a_col + 32);
           tmem_wait_st();
@@ -1310,8 +1427,9 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
             else  // pair peer: its TMEM A tile is complete (wait::st + fence above)
               mbar_arrive_cluster_relaxed(full_addr0 + 8u * s);
           }
-          if (++s == S) {
-            s = 0;
+          s += kTeams;
+          if (s >= S) {
+            s -= S;
             ph ^= 1;
           }
           // fold one chunk of the oldest group whose last K block is at
@@ -1329,7 +1447,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       if (Cfg::kEpiStage && lane == 0) bulk_wait_all();  // maps written, staging free
     }
     TCP_ACC(c_all); }
-    if (warp == kEpiWarp0 && lane == 0) {
+    if (warp == kGenW0 && lane == 0) {
       TCP_FLUSH(5, c_gen_wait);
       TCP_FLUSH(6, c_gen);
       TCP_FLUSH(7, c_drain);
@@ -1386,7 +1504,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     atomicMax(&g_tc_prof[23], g_entry);   // latest entry
   }
 #endif
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     if (kPair)
       tmem_dealloc_pair(tmem, 512);
@@ -1439,16 +1557,19 @@ bool use_pair(int m_tiles, bool default_on) {
   return env == 1 || default_on;
 }
 
-// on-the-fly K4: single-CTA tiles unless SRPB_OTF_PAIR=1 (measured at C4,
-// F=320: 148 ms single vs 151 ms paired -- the weights are generated, not
-// streamed, so halving each SM's B ingress buys nothing)
+// on-the-fly K4: CTA pairs unless SRPB_OTF_PAIR=0.  With two generator
+// teams the kernel is power-bound (sw_power_cap; tensor pipe busy), and the
+// Xi stream from L2 is the largest non-MMA energy item (measured at C4,
+// F = 320: without B loads the same cycle count ran at 1.61 instead of
+// 1.37 GHz); a pair halves each SM's B rows: 143 -> 137 ms (single-team
+// round: 148 single vs 151 ms paired).
 bool use_pair_otf(int m_tiles) {
   static int env = -2;
   if (env == -2) {
     const char* s = getenv("SRPB_OTF_PAIR");
     env = s ? atoi(s) : -1;
   }
-  return m_tiles >= 2 && env == 1;
+  return m_tiles >= 2 && env != 0;
 }
 
 int num_sms();
@@ -1485,8 +1606,11 @@ int num_sms() {
 // span at least c - 1 blocks or the generator stalls on a stage the MMA never
 // frees (measured: a 2-block tail group hung the kernel).  Groups are at
 // least c + 1 blocks and the tile's remainder joins its last group.
-void enforce_fold_window(TcParams& p) {
-  p.kb_per_group = max(p.kb_per_group, p.N / 32 + 1);
+// With two generator teams a warp folds every other chunk, one per block of
+// its own team (every second block): groups of >= 2 ceil(c / 2) + 1 blocks.
+void enforce_fold_window(TcParams& p, int teams = 1) {
+  const int c = p.N / 32;
+  p.kb_per_group = max(p.kb_per_group, teams == 2 ? 2 * ((c + 1) / 2) + 1 : c + 1);
   p.groups_per_tile = max(1, p.num_kb / p.kb_per_group);
 }
 
@@ -1541,7 +1665,7 @@ cudaError_t launch_tc(const CUtensorMap& ah, const CUtensorMap& al, const CUtens
   const int units = min(p.total_items, num_sms() / cta);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * cta);
-  cfg.blockDim = dim3(kTcThreads);
+  cfg.blockDim = dim3(Cfg::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -1679,7 +1803,7 @@ cudaError_t launch_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, 
   // L2 by every candidate tile; the weights are generated, not loaded)
   const bool pair = use_pair_otf((J + kTcM - 1) / kTcM);
   finish_params(p, kb_per_group, pair, true);
-  enforce_fold_window(p);
+  enforce_fold_window(p, pair ? TcCfg<kASinc, true, true>::kTeams : TcCfg<kASinc, false, true>::kTeams);
   // candidate tiles fastest: the CTAs in flight share one frame tile's Xi
   // rows in L2 instead of streaming every frame tile's
   // (dynamic items: the tile's Xi rows fit L2, 92 MB at C4; measured with

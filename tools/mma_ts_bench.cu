@@ -11,6 +11,7 @@ using namespace srpb::umma;
 template <bool kTS>
 __global__ void __launch_bounds__(384, 1) bench(int N, int iters, unsigned long long* out, int mode) {
   __shared__ uint64_t sbar[4];
+  __shared__ uint64_t sfull[3], sempty[3];
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t bar;
@@ -29,6 +30,10 @@ __global__ void __launch_bounds__(384, 1) bench(int N, int iters, unsigned long 
     for (int i = 0; i < 4; ++i) mbar_init(&sbar[i], 1);
     mbar_init(&bar, 1);
     mbar_init(&spin_done, 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&sfull[i], 1 + 8);
+      mbar_init(&sempty[i], 1);
+    }
     fence_mbar_init();
   }
   fence_proxy_async_smem();
@@ -41,13 +46,47 @@ __global__ void __launch_bounds__(384, 1) bench(int N, int iters, unsigned long 
     const uint32_t idesc = idesc_f16(128, N);
     for (int it = 0; it < iters; ++it) {
       const int s = it & 3;
+      if (mode == 11) {  // the kernel's ring: wait for the stage's producers
+        mbar_wait(&sfull[it % 3], (it / 3) & 1);
+        tc_fence_after();
+      }
       const uint64_t da = sw128_kmajor_desc(smem_u32(smem + s * stage));
       const uint64_t db = sw128_kmajor_desc(smem_u32(smem + s * stage + a_bytes));
       if (elect_one()) {
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
           const uint32_t o = 2 * ks;
-          if (mode >= 2) {  // the K4/K2 pattern: lo*hi + hi*lo + hi*hi, A from TMEM
+          if (mode >= 7) {
+            // the kernel's operands: distinct B_hi / B_lo (B_lo = the next
+            // stage's B region), 3 TMEM A stages; 7: (lo,hi) (hi,lo) (hi,hi)
+            // as K2/K4 issue them; 8: (lo,hi) (hi,hi) (hi,lo) -- consecutive
+            // MMAs on the same B; 9: (hi,hi) (lo,hi) (hi,lo); 10: as 7, A
+            // from smem (SS)
+            const int s3 = it % 3;
+            const uint64_t bh = db + o;
+            const uint64_t bl = sw128_kmajor_desc(smem_u32(smem + ((s + 1) & 3) * stage + a_bytes)) + o;
+            const uint32_t ah = tmem + 2 * N + 64 * s3 + 8 * ks, al = ah + 32;
+            const uint32_t d = tmem + ((it / 10) & 1) * N;
+            const uint32_t a0 = (it % 10 > 0 || ks > 0) ? 1u : 0u;
+            if (mode == 7 || mode == 11) {
+              mma_f16_ts(d, al, bh, idesc, a0);
+              mma_f16_ts(d, ah, bl, idesc, 1u);
+              mma_f16_ts(d, ah, bh, idesc, 1u);
+            } else if (mode == 8) {
+              mma_f16_ts(d, al, bh, idesc, a0);
+              mma_f16_ts(d, ah, bh, idesc, 1u);
+              mma_f16_ts(d, ah, bl, idesc, 1u);
+            } else if (mode == 9) {
+              mma_f16_ts(d, ah, bh, idesc, a0);
+              mma_f16_ts(d, al, bh, idesc, 1u);
+              mma_f16_ts(d, ah, bl, idesc, 1u);
+            } else {
+              const uint64_t sah = da + o, sal = sw128_kmajor_desc(smem_u32(smem + ((s + 1) & 3) * stage)) + o;
+              mma_f16(d, sal, bh, idesc, a0);
+              mma_f16(d, sah, bl, idesc, 1u);
+              mma_f16(d, sah, bh, idesc, 1u);
+            }
+          } else if (mode >= 2) {  // the K4/K2 pattern: lo*hi + hi*lo + hi*hi, A from TMEM
             const uint32_t ah = tmem + 2 * N + 64 * (s & 1) + 8 * ks, al = ah + 32;
             const uint32_t d = tmem + ((it / 10) & 1) * N;
             mma_f16_ts(d, al, db + o, idesc, (it % 10 > 0 || ks > 0) ? 1u : 0u);
@@ -59,7 +98,10 @@ __global__ void __launch_bounds__(384, 1) bench(int N, int iters, unsigned long 
           else
             mma_f16(tmem + (it & 1) * N, da + o, db + o, idesc, (it > 1 || ks > 0) ? 1u : 0u);
         }
-        if (mode >= 1) mma_commit(&sbar[s]);
+        if (mode == 11)
+          mma_commit(&sempty[it % 3]);
+        else if (mode >= 1)
+          mma_commit(&sbar[s]);
       }
       __syncwarp();
     }
@@ -69,6 +111,15 @@ __global__ void __launch_bounds__(384, 1) bench(int N, int iters, unsigned long 
     const long long t1 = clock64();
     if (threadIdx.x == 32) mbar_arrive(&spin_done);
     if (threadIdx.x == 32) atomicAdd(out, static_cast<unsigned long long>(t1 - t0));
+  }
+  if (mode == 11 && (warp == 0 || warp >= 4)) {
+    // producer + 8 generator warps: wait for the stage to drain, arrive
+    for (int it = 0; it < iters; ++it) {
+      if (it >= 3) mbar_wait(&sempty[it % 3], ((it / 3) - 1) & 1);
+      tc_fence_after();
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&sfull[it % 3]);
+    }
   }
   if (warp >= 4 && mode == 4) {  // 8 warps issue ALU work (FFMA chains + MUFU) throughout
     float x0 = threadIdx.x, x1 = x0 + 1.f, x2 = x0 + 2.f, x3 = x0 + 3.f;
@@ -104,7 +155,7 @@ __global__ void __launch_bounds__(384, 1) bench(int N, int iters, unsigned long 
     if (r[0] == 12345u) out[1] = 1;
   }
   tc_fence_before();
-  if (warp >= 4) mbar_wait(&spin_done, 0);  // mode 3: 8 warps poll a barrier throughout
+  if (warp >= 4 && mode != 11) mbar_wait(&spin_done, 0);  // mode 3: 8 warps poll a barrier throughout
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
@@ -118,7 +169,7 @@ int main(int argc, char** argv) {
     cudaFuncSetAttribute(bench<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(bench<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int iters = argc > 1 ? atoi(argv[1]) : 4000;
-    for (int mode = (argc > 2 ? atoi(argv[2]) : 0); mode < (argc > 2 ? atoi(argv[2]) + 1 : 7); ++mode)
+    for (int mode = (argc > 2 ? atoi(argv[2]) : 0); mode < (argc > 2 ? atoi(argv[2]) + 1 : 12); ++mode)
     for (int ts = 0; ts < 2; ++ts)
       for (int rep = 0; rep < 2; ++rep) {
         cudaMemset(d, 0, 8);
