@@ -98,7 +98,7 @@ struct TcCfg {
   // own 16-column accumulator chunks straight from the shared totals.  Warp
   // roles: generators 0..15 (TMEM lane quarter = warp % 4), TMA producer 16,
   // MMA issuer 17.  Otherwise: producer 0, MMA 1, epilogue warps 4..11.
-  static constexpr int kTeams = kAMode == kASinc ? 2 : 1;
+  static constexpr int kTeams = kAMode != kAFromTma ? 2 : 1;
   static constexpr int kGenW0 = kTeams == 2 ? 0 : kEpiWarp0;  // first epilogue / generator warp
   static constexpr int kGenWarps = kEpiWarps * kTeams;
   static constexpr int kProdWarp = kTeams == 2 ? kGenWarps : 0;
@@ -631,45 +631,59 @@ __device__ __forceinline__ uint32_t tf32_rna_bits(float x) {
 }
 
 // Steering-phase generator of one A row (candidate j) and one half of every
-// K block (kBins bins: 8 per 32-column tf32 block, 16 per 64-element fp16
-// block).  Per pair: the one-bin and one-block rotations e^{j2pi x/N},
-// e^{j2pi 2 kBins x/N} from exact turn arithmetic; per block: the anchor
-// phase, exact (integer-reduced turns + sincospif) every 64 bins and
-// otherwise the previous anchor rotated by one block; then kBins - 1 one-bin
-// rotations.  Longest rotation chain ~ 3 block + 15 one-bin rotations, ~1e-6
-// relative phase error.
-template <bool kF16>
+// K block it is given (kBins bins: 8 per 32-column tf32 block, 16 per
+// 64-element fp16 block).  The blocks of a tile come in increasing order,
+// kStride apart (generator teams take every other block).  Per pair: the
+// one-bin and kStride-block rotations e^{j2pi x/N}, e^{j2pi 2 kBins kStride
+// x/N} from exact turn arithmetic; per block: the anchor phase, exact
+// (integer-reduced turns + sincospif) every kAnchorBlocks of this thread's
+// blocks and otherwise the previous anchor rotated by kStride blocks; then
+// kBins - 1 one-bin rotations.  Longest rotation chain ~ 1 block + 15 one-bin
+// rotations, ~1e-6 relative phase error.
+template <bool kF16, int kStride = 1>
 struct PhaseGen {
   static constexpr int kBins = kF16 ? 16 : 8;                 // bins per half block
-  static constexpr int kAnchorBlocks = 64 / (2 * kBins);     // exact anchor every 64 bins
-  int kbp, left;  // K blocks per pair, blocks left in the current pair
+  static constexpr int kAnchorBlocks = 64 / (2 * kBins);     // exact anchor every 64 bins (per thread)
+  int kbp, bip;   // K blocks per pair, block index in the current pair
   int pair, ti;
   float tf, sc, ss, sbc, sbs, ac, as;
   int since_exact;
 
   __device__ __forceinline__ void start_tile(const TcParams& p) {
     kbp = p.kb_per_pair;
-    left = 0;
     pair = -1;
   }
 
-  __device__ __forceinline__ void block(const TcParams& p, int j, int half, uint32_t a_hi_tmem,
-                                        uint32_t a_lo_tmem) {
-    if (left == 0) {  // next pair
-      ++pair;
-      left = kbp;
-      ti = 0;
-      tf = 0.0f;
-      if (j < p.J) {
-        ti = p.tau_i[static_cast<size_t>(pair) * p.J + j];
-        tf = p.tau_f[static_cast<size_t>(pair) * p.J + j];
-      }
-      sincospif(2.0f * (static_cast<float>(ti) + tf) * p.inv_period, &ss, &sc);
-      const float tb = harmonic_turns(2 * kBins, ti, tf, p.period, p.mask, p.inv_period);
-      sincospif(2.0f * tb, &sbs, &sbc);
-      since_exact = kAnchorBlocks;
+  __device__ __forceinline__ void load_pair(const TcParams& p, int j) {
+    ti = 0;
+    tf = 0.0f;
+    if (j < p.J) {
+      ti = p.tau_i[static_cast<size_t>(pair) * p.J + j];
+      tf = p.tau_f[static_cast<size_t>(pair) * p.J + j];
     }
-    const int k = (kbp - left) * (2 * kBins) + kBins * half;
+    sincospif(2.0f * (static_cast<float>(ti) + tf) * p.inv_period, &ss, &sc);
+    const float tb = harmonic_turns(2 * kBins * kStride, ti, tf, p.period, p.mask, p.inv_period);
+    sincospif(2.0f * tb, &sbs, &sbc);
+    since_exact = kAnchorBlocks;
+  }
+
+  __device__ __forceinline__ void block(const TcParams& p, int j, int half, int kb,
+                                        uint32_t a_hi_tmem, uint32_t a_lo_tmem) {
+    if (pair < 0) {  // first block of the tile
+      pair = kb / kbp;
+      bip = kb - pair * kbp;
+      load_pair(p, j);
+    } else {
+      bip += kStride;
+      if (bip >= kbp) {  // a later pair
+        do {
+          bip -= kbp;
+          ++pair;
+        } while (bip >= kbp);
+        load_pair(p, j);
+      }
+    }
+    const int k = bip * (2 * kBins) + kBins * half;
     if (since_exact >= kAnchorBlocks) {
       harmonic_phase(k, ti, tf, p.period, p.mask, p.inv_period, &ac, &as);
       since_exact = 0;
@@ -679,7 +693,6 @@ struct PhaseGen {
       ac = cn;
     }
     ++since_exact;
-    --left;
     float c = ac, s = as;
     uint32_t hi[16], lo[16];
 #pragma unroll
@@ -1389,7 +1402,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       // [16*half, +16) of each 32-column A block
       const int r = 32 * quarter + lane;
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
-      using Gen = typename std::conditional<kAMode == kASinc, SincGen, PhaseGen<kF16>>::type;
+      using Gen = typename std::conditional<kAMode == kASinc, SincGen, PhaseGen<kF16, kTeams>>::type;
       Gen gen;
       // global K block kg (across items) and its stage ring position; a team
       // takes every kTeams-th block (S >= 2 >= kTeams)
@@ -1416,7 +1429,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
           if constexpr (kAMode == kASinc)
             gen.block(p, j, half, (TC_DBG(p) & 64) ? 0 : kb, a_col, a_col + 32);  // 64: A of block 0
           else
-            gen.block(p, j, half, a_col, a_col + 32);
+            gen.block(p, j, half, kb, a_col, a_col + 32);
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
@@ -1544,9 +1557,10 @@ int pick_n(int F) {
 
 // CTA pairs by default when there are >= 2 candidate tiles; SRPB_TC_PAIR=0
 // forces single-CTA tiles (tuning / A-B comparison).
-// Measured on B200 (C2): K4 108.5 us paired vs 116 us single; K2 4.36 ms
-// paired vs 3.60 ms single (its 3-stage TMEM A ring cannot absorb the
-// cross-SM signalling latency), so pairs are the default for K4 only.
+// Measured on B200 (C2): K4 108.5 us paired vs 116 us single; K2 with one
+// generator team 4.36 ms paired vs 3.60 ms single (its 3-stage TMEM A ring
+// could not absorb the cross-SM signalling latency) -- with two teams pairs
+// win for K2 as well (see conventional_tc).
 bool use_pair(int m_tiles, bool default_on) {
   static int env = -2;
   if (env == -2) {
@@ -1698,9 +1712,12 @@ static cudaError_t conventional_tc(const void* psi_hi, const void* psi_lo, bool 
   p.J = J;
   p.kb_per_pair = Kb / (f16 ? 32 : 16);  // K blocks per pair: 2 Kb elements
   p.num_kb = P * p.kb_per_pair;
-  const bool pair = use_pair((J + kTcM - 1) / kTcM, false);
+  // CTA pairs by default: with two generator teams the pair's cross-SM
+  // signalling is absorbed (measured C4 shapes, F = 320, J = 148k: 125.5 ms
+  // single-team single-CTA, 124.5 two teams, 117 two teams + pairs)
+  const bool pair = use_pair((J + kTcM - 1) / kTcM, true);
   finish_params(p, kb_per_group, pair, f16);
-  enforce_fold_window(p);
+  enforce_fold_window(p, TcCfg<kAPhase, false, true>::kTeams);
   p.scale = f16 ? 2.0f / (kF16PhaseScale * psi_scale) : 2.0f;
   p.maps = maps;
   p.keys = keys;
