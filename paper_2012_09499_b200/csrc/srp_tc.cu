@@ -188,7 +188,12 @@ struct TcParams {
   int P;
 };
 
-constexpr int kItemRing = 8;  // work-item ids in flight between the roles
+// Work-item ids in flight between the roles.  A generator warp releases an
+// item only when it has folded the item's last group, which may trail its
+// generation by S + 2 groups, and the two teams and the MMA stay within S
+// blocks of each other: with one-block tiles the producer can be 2 S + 2
+// items ahead of the slowest release (S <= 8), so the ring holds 32.
+constexpr int kItemRing = 32;
 
 struct TcSmem {
   uint64_t full[kTcMaxStages];
@@ -799,73 +804,81 @@ struct SincGen {
     lo = *reinterpret_cast<const uint32_t*>(&l);
   }
 
+  // One 32-column run in two 16-column slabs (8 hi + 8 lo words each, one
+  // tcgen05.st.x8 per half of the split): half the live weight registers of
+  // a whole-run pass (the 18-warp kernel has 96 registers per thread).
   __device__ __forceinline__ void block(const TcParams& prm, int j, int half, int kb,
                                         uint32_t a_hi_tmem, uint32_t a_lo_tmem) {
-    uint32_t hi[16], lo[16];
     const int t0 = 64 * kb + 32 * half;
     // a thread sees 32 of every 64 columns: pairs may end in the skipped half
     while (t0 >= end) advance(prm, j);  // warp-uniform
-    if (TC_DBG(prm) & 2048) {  // bound analysis only: no weight arithmetic
 #pragma unroll
-      for (int i = 0; i < 16; ++i) hi[i] = lo[i] = __float_as_uint(f) + i;
-    } else if (t0 + 32 <= end) {
-      // the whole run lies in pair p
-      // integer-valued d of columns (c, c + 1), stepped by -2 (exact); then
-      // one rounding add of f: = float(d) + f.  (Per-column immediates would
-      // go through a recycled uniform register pair and serialise the loop.)
-      const float Df = static_cast<float>(E - t0);
-      float2 dd = make_float2(Df, Df - 1.0f);
-      const float2 m2 = make_float2(-2.0f, -2.0f);
-      const float2 a2 = make_float2(amp, -amp);
-      const float2 f2 = make_float2(f, f);
+    for (int q = 0; q < 2; ++q) {
+      constexpr int kW = 16;  // columns per slab
+      const int cb = kW * q;  // first column of the slab in the run
+      uint32_t hi[8], lo[8];
+      if (TC_DBG(prm) & 2048) {  // bound analysis only: no weight arithmetic
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) {
-        const float2 x = __fadd2_rn(dd, f2);
-        dd = __fadd2_rn(dd, m2);
-        const float2 r = (TC_DBG(prm) & 1024) ? x : make_float2(rcp_approx_ftz(x.x), rcp_approx_ftz(x.y));
-        split2(__fmul2_rn(r, a2), hi[c >> 1], lo[c >> 1]);
-      }
-      if (__any_sync(0xffffffffu, node)) {
-        // the node row's d == 0 column in this run as a column bit (selects
-        // per word: an `if (i == cs / 2) hi[i] = ..` becomes an indexed store
-        // and moves hi[] to local memory)
-        const int cs = E - t0;
-        const uint32_t hit = (node && cs >= 0 && cs < 32) ? (1u << cs) : 0u;
+        for (int i = 0; i < 8; ++i) hi[i] = lo[i] = __float_as_uint(f) + i;
+      } else if (t0 + cb + kW <= end) {
+        // the slab lies in pair p: integer-valued d of columns (c, c + 1),
+        // stepped by -2 (exact), then one rounding add of f = float(d) + f.
+        // (Per-column immediates would go through a recycled uniform
+        // register pair and serialise the loop.)
+        const float Df = static_cast<float>(E - t0 - cb);
+        float2 dd = make_float2(Df, Df - 1.0f);
+        const float2 m2 = make_float2(-2.0f, -2.0f);
+        const float2 a2 = make_float2(amp, -amp);
+        const float2 f2 = make_float2(f, f);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const uint32_t b2 = (hit >> (2 * i)) & 3u;
-          hi[i] = b2 == 0u ? hi[i] : (b2 == 1u ? 0x00007400u : 0x74000000u);
+        for (int c = 0; c < kW; c += 2) {
+          const float2 x = __fadd2_rn(dd, f2);
+          dd = __fadd2_rn(dd, m2);
+          const float2 r = (TC_DBG(prm) & 1024) ? x : make_float2(rcp_approx_ftz(x.x), rcp_approx_ftz(x.y));
+          split2(__fmul2_rn(r, a2), hi[c >> 1], lo[c >> 1]);
         }
-      }
-    } else {
-      // the run meets several pairs: one masked 32-column pass per pair (all
-      // indices compile-time, so the weights stay in registers; a rolled
-      // column walk through local memory measured 11% slower at C4)
-      float w[32];
+        if (__any_sync(0xffffffffu, node)) {
+          // the node row's d == 0 column in this slab as a column bit
+          // (selects per word: an `if (i == cs / 2) hi[i] = ..` becomes an
+          // indexed store and moves hi[] to local memory)
+          const int cs = E - t0 - cb;
+          const uint32_t hit = (node && cs >= 0 && cs < kW) ? (1u << cs) : 0u;
 #pragma unroll
-      for (int c = 0; c < 32; ++c) w[c] = 0.0f;
-      int lo_c = 0;
-      for (;;) {  // warp-uniform
-        const int hi_c = min(end - t0, 32);
-        const int cs = E - t0;
-        const float Df = static_cast<float>(cs);
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const float x = (Df - static_cast<float>(c)) + f;
-          float v = rcp_approx_ftz(x) * ((c & 1) ? -amp : amp);
-          if (node) v = cs == c ? kF16PhaseScale : 0.0f;
-          w[c] = (c >= lo_c && c < hi_c) ? v : w[c];
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t b2 = (hit >> (2 * i)) & 3u;
+            hi[i] = b2 == 0u ? hi[i] : (b2 == 1u ? 0x00007400u : 0x74000000u);
+          }
         }
-        if (hi_c == 32) break;
-        lo_c = hi_c;
-        advance(prm, j);
-      }
+      } else {
+        // the slab meets several pairs: one masked pass per pair (all
+        // indices compile-time, so the weights stay in registers; a rolled
+        // column walk through local memory measured 11% slower at C4)
+        float w[kW];
 #pragma unroll
-      for (int c = 0; c < 32; c += 2) split2(make_float2(w[c], w[c + 1]), hi[c >> 1], lo[c >> 1]);
+        for (int c = 0; c < kW; ++c) w[c] = 0.0f;
+        int lo_c = 0;
+        for (;;) {  // warp-uniform
+          const int hi_c = min(end - t0 - cb, kW);
+          const int cs = E - t0 - cb;
+          const float Df = static_cast<float>(cs);
+#pragma unroll
+          for (int c = 0; c < kW; ++c) {
+            const float x = (Df - static_cast<float>(c)) + f;
+            float v = rcp_approx_ftz(x) * ((c & 1) ? -amp : amp);
+            if (node) v = cs == c ? kF16PhaseScale : 0.0f;
+            w[c] = (c >= lo_c && c < hi_c) ? v : w[c];
+          }
+          if (hi_c == kW) break;
+          lo_c = hi_c;
+          advance(prm, j);
+        }
+#pragma unroll
+        for (int c = 0; c < kW; c += 2) split2(make_float2(w[c], w[c + 1]), hi[c >> 1], lo[c >> 1]);
+      }
+      if (TC_DBG(prm) & 4096) continue;  // bound analysis only: no TMEM stores
+      tmem_st8(a_hi_tmem + 16 * half + 8 * q, hi);
+      tmem_st8(a_lo_tmem + 16 * half + 8 * q, lo);
     }
-    if (TC_DBG(prm) & 4096) return;  // bound analysis only: no TMEM stores
-    tmem_st16(a_hi_tmem + 16 * half, hi);
-    tmem_st16(a_lo_tmem + 16 * half, lo);
   }
 };
 
@@ -1286,6 +1299,8 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       return gl == p.groups_per_tile - 1 ? p.num_kb - 1 : (gl + 1) * p.kb_per_group - 1;
     };
     int d_last_kg = group_last(0);
+    // generator modes: tiles shorter than the fold window
+    const bool fold_all = p.num_kb < p.kb_per_group;
     TCP_DECL(c_gen_wait);
     TCP_DECL(c_gen);
     TCP_DECL(c_drain);
@@ -1446,8 +1461,18 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
             ph ^= 1;
           }
           // fold one chunk of the oldest group whose last K block is at
-          // least S behind
-          if (d_chunk >= 0 || (d_it < n_items && d_last_kg <= kg - S)) fold_step();
+          // least S behind; with tiles shorter than the fold window (one
+          // group of fewer blocks, groups arriving faster than a team's
+          // blocks) every such group is folded at once, or the MMA of group
+          // g + 2 would wait on a fold that waits for blocks it holds up
+          auto fold_due = [&]() {
+            return d_chunk >= 0 || (d_it < n_items && d_last_kg <= kg - S);
+          };
+          if (fold_due()) {
+            do {
+              fold_step();
+            } while (fold_all && fold_due());
+          }
         }
       }
       while (d_it < n_items) fold_step();

@@ -1,0 +1,95 @@
+"""Edge shapes of the two-team tcgen05 generator kernels (K2 steering
+phases, on-the-fly K4 sinc weights): teams take alternate K blocks, so the
+cases that matter are tiles with very few K blocks (fewer than the fold
+window, a single block), odd K-block counts per pair (the phase generator
+strides across pair boundaries) and many work items per CTA pair (the
+accumulator ping-pong wraps across items).  Checked against the pinned
+oracle (and, for K4, bit for bit against the stored-weight kernel)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import srp_oracle as O
+from paper_2012_09499_b200.plan import SrpPlan
+from helpers import REL_L2_TOL, assert_maps_match, rel_l2
+
+pytestmark = pytest.mark.gpu
+T = 1.0 / 16000.0
+C = 343.0
+
+
+def _geometry(mic_pos, points):
+    pairs = O.canonical_pairs(mic_pos.shape[0])
+    pm = np.array([m for m, _ in pairs], np.int32)
+    pmp = np.array([mp for _, mp in pairs], np.int32)
+    bounds = np.array([np.linalg.norm(mic_pos[m] - mic_pos[mp]) / C for m, mp in pairs])
+    tdoa = O.tdoa_table_nearfield(mic_pos, points, pairs, C)
+    return pairs, pm, pmp, bounds, tdoa
+
+
+def _spectra(rng, F, M, Kb):
+    return (rng.standard_normal((F, M, Kb)) + 1j * rng.standard_normal((F, M, Kb))).astype(
+        np.complex64)
+
+
+@pytest.mark.parametrize("n_aux", [0, 1])
+def test_onthefly_short_lattice_many_items(n_aux):
+    """3 microphones 2 cm apart: every pair's lattice has 3 (+2 N_aux)
+    samples, so a tile is a single 64-column K block -- far below the fold
+    window -- while 150k candidates give each CTA pair ~8 work items."""
+    rng = np.random.default_rng(7 + n_aux)
+    mic = np.array([[0.0, 0.0, 1.5], [0.02, 0.0, 1.5], [0.0, 0.02, 1.5]])
+    pts = rng.uniform([-2.0, -2.0, 0.0], [2.0, 2.0, 2.5], size=(150_000, 3))
+    pairs, pm, pmp, bounds, tdoa = _geometry(mic, pts)
+    omega = O.bin_frequencies(16000.0, 1024)
+    Y = _spectra(rng, 40, 3, omega.size)
+    st = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=n_aux, weights="stored",
+                 backend="tc")
+    ot = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=n_aux,
+                 weights="onthefly", backend="tc")
+    assert ot.W is None and ot.T_pad <= 64  # one K block per tile
+    Yd = torch.from_numpy(Y).cuda()
+    m1, a1 = st.run(Yd, "approx")
+    m2, a2 = ot.run(Yd, "approx")
+    torch.cuda.synchronize()
+    assert torch.equal(m1, m2) and torch.equal(a1, a2)
+    # oracle on every frame, a seeded candidate subset (+ each frame's argmax)
+    sel = np.unique(np.concatenate([rng.choice(pts.shape[0], 3000, replace=False),
+                                    a2.cpu().numpy()]))
+    _, w = O.sinc_table(tdoa[sel], bounds, T, n_aux)
+    ref = np.stack([O.approx_map(w, O.gcc_lattice(
+        O.cross_spectrum(Y[f].astype(np.complex128), pm, pmp)[0], omega, bounds, T, n_aux)[1])
+        for f in range(Y.shape[0])])
+    got = m2.cpu().numpy()[:, sel].astype(np.float64)
+    for f in range(ref.shape[0]):
+        assert rel_l2(got[f], ref[f]) <= REL_L2_TOL, f
+        # a 2 cm array barely separates candidates: many are equal to fp32
+        # rounding, so the argmax is checked up to such near-ties
+        ga = int(np.searchsorted(sel, int(a2[f])))
+        assert ref[f].max() - ref[f][ga] <= 1e-6 * np.abs(ref[f]).max(), f
+
+
+@pytest.mark.parametrize("kb", [32, 96, 160])
+def test_conventional_teams_odd_blocks_per_pair(kb):
+    """K2 with 1, 3 and 5 K blocks per pair (Kb = 32, 96, 160 harmonic
+    bins): the two generator teams' blocks straddle pair boundaries in both
+    parities; 12 work items per CTA pair."""
+    rng = np.random.default_rng(kb)
+    M = 6
+    mic = rng.uniform(0.0, 1.0, size=(M, 3)) * np.array([4.0, 3.0, 2.5])
+    pts = rng.uniform(0.0, 1.0, size=(60_000, 3)) * np.array([4.0, 3.0, 2.5])
+    pairs, pm, pmp, bounds, tdoa = _geometry(mic, pts)
+    omega = O.bin_frequencies(16000.0, 1024)[:kb]
+    Y = _spectra(rng, 24, M, kb)
+    plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=2, backend="tc")
+    maps, am = plan.run(torch.from_numpy(Y).cuda(), "conventional")
+    torch.cuda.synchronize()
+    psi = np.stack([O.cross_spectrum(Y[f].astype(np.complex128), pm, pmp)[0]
+                    for f in range(Y.shape[0])])
+    sel = np.unique(np.concatenate([rng.choice(pts.shape[0], 4000, replace=False),
+                                    am.cpu().numpy()]))
+    ref = O.conventional_frames(psi, omega, tdoa[sel])
+    got = maps.cpu().numpy()[:, sel]
+    assert_maps_match(got, ref, np.searchsorted(sel, am.cpu().numpy()),
+                      what=f"conventional Kb={kb}")
