@@ -203,6 +203,7 @@ struct TcSmem {
   uint64_t item_full[kItemRing];   // ring slot holds the next item id (each CTA)
   uint64_t item_empty[kItemRing];  // every consumer is done with the slot (leader)
   int item_ring[kItemRing];
+  int4 item_cache[16];  // generator modes: per warp, the item its fold is on
   uint32_t tmem_base;
 };
 
@@ -750,7 +751,7 @@ struct PhaseGen {
 // amplitude 0 with a half-integer denominator and get their single 2^14
 // written afterwards.
 struct SincGen {
-  int p, end, P;      // current pair, its end column (INT_MAX past the last pair)
+  int p, end;         // current pair, its end column (INT_MAX past the last pair)
   int E;              // split integer part + column of lag 0: d = E - t
   float f, amp;       // denominator fraction, signed 2^14 sin(pi f) / pi
   bool node;          // exact-node row: weight 2^14 at d == 0, else 0
@@ -761,14 +762,13 @@ struct SincGen {
   __device__ __forceinline__ void fetch(const TcParams& prm, int j, int q) {
     nsi = 0;
     nsf = 0.0f;
-    if (q < P && j < prm.J) {
+    if (q < prm.P && j < prm.J) {
       nsi = __ldg(prm.sx_i + static_cast<size_t>(q) * prm.J + j);
       nsf = __ldg(prm.sx_f + static_cast<size_t>(q) * prm.J + j);
     }
   }
 
   __device__ __forceinline__ void start_tile(const TcParams& prm, int j, const int2* pair_cols) {
-    P = prm.P;
     p = -1;
     end = 0;
     cols = pair_cols;
@@ -777,7 +777,7 @@ struct SincGen {
 
   __device__ __forceinline__ void advance(const TcParams& prm, int j) {
     ++p;
-    if (p < P) {
+    if (p < prm.P) {
       const int2 c = cols[p];
       end = c.x;
       E = nsi + c.y;
@@ -1311,7 +1311,6 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // is released when the group is complete (the ping-pong leaves the MMA
     // kb_per_group blocks of slack)
     int d_chunk = -1;  // chunk of group `drained` next to fold (-1: not started)
-    uint32_t d_base = 0;
     // generator modes: this thread's slice of the shared running totals
     float* tot_s = tot_smem + half * (kTcMaxN / 2) * kTcM + 32 * quarter + lane;
     if constexpr (Cfg::kTotSmem) {
@@ -1346,25 +1345,30 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       }
       ++drained;
     };
-    int f_it = -1;  // item cached by fold_step (item_of divides)
-    Item f_item{};
+    // item of the group being folded, cached per warp in shared memory
+    // (item_of divides; registers are scarce in the 18-warp kernels)
+    int f_it = -1;
+    int4* const f_cache = &bar->item_cache[(warp - kGenW0) & 15];
     auto fold_step = [&]() {
       if (f_it != d_it) {
-        f_item = item_of(item_id(d_it));
+        const Item ti = item_of(item_id(d_it));
+        if (lane == 0) *f_cache = make_int4(ti.m0, ti.n0, ti.nc, 0);
+        __syncwarp();
         f_it = d_it;
       }
-      const Item t = f_item;
+      const volatile int* fcv = reinterpret_cast<volatile int*>(f_cache);
+      const Item t{fcv[0], fcv[1], fcv[2]};
       TCP_T0();
       const int b = drained & 1;
       if (d_chunk < 0) {
         mbar_wait(&bar->acc_full[b], (drained >> 1) & 1);
         tc_fence_after();
-        d_base = tmem + (static_cast<uint32_t>(32 * quarter) << 16) +
-                 static_cast<uint32_t>(b * p.N + half * (t.nc / 2));
         d_chunk = c0;
       }
       // (shared-memory totals: the chunk is a runtime offset, one code copy)
       if (d_chunk < t.nc / 32) {
+        const uint32_t d_base = tmem + (static_cast<uint32_t>(32 * quarter) << 16) +
+                                static_cast<uint32_t>(b * p.N + half * (t.nc / 2));
         tc_drain_chunk16_smem(d_base, tot_s, d_chunk, TC_DBG(p));
         d_chunk += kTeams;
       }
