@@ -104,6 +104,7 @@ struct TcCfg {
   static constexpr int kProdWarp = kTeams == 2 ? kGenWarps : 0;
   static constexpr int kMmaWarp = kTeams == 2 ? kGenWarps + 1 : 1;
   static constexpr int kThreads = kTeams == 2 ? 32 * (kGenWarps + 2) : kTcThreads;
+  static constexpr int kItemRing = kTotSmem ? 32 : 8;  // see TcSmemT
 };
 
 // Instrumentation build only (make prof -> libsrpb_prof.so, tools/tc_probe.py):
@@ -192,20 +193,22 @@ struct TcParams {
 // item only when it has folded the item's last group, which may trail its
 // generation by S + 2 groups, and the two teams and the MMA stay within S
 // blocks of each other: with one-block tiles the producer can be 2 S + 2
-// items ahead of the slowest release (S <= 8), so the ring holds 32.
-constexpr int kItemRing = 32;
-
-struct TcSmem {
+// items ahead of the slowest release (S <= 8), so generator modes ring 32
+// ids.  The stored-weight K4 (epilogue warps release after their drain) keeps
+// 8: its 4 x 52 KB stages + staging leave no room.
+template <int kRing>
+struct TcSmemT {
   uint64_t full[kTcMaxStages];
   uint64_t empty[kTcMaxStages];
   uint64_t acc_full[2];
   uint64_t acc_empty[2];
-  uint64_t item_full[kItemRing];   // ring slot holds the next item id (each CTA)
-  uint64_t item_empty[kItemRing];  // every consumer is done with the slot (leader)
-  int item_ring[kItemRing];
-  int4 item_cache[16];  // generator modes: per warp, the item its fold is on
+  uint64_t item_full[kRing];   // ring slot holds the next item id (each CTA)
+  uint64_t item_empty[kRing];  // every consumer is done with the slot (leader)
+  int item_ring[kRing];
+  int4 item_cache[kRing > 8 ? 16 : 1];  // generator modes: per warp, the item its fold is on
   uint32_t tmem_base;
 };
+
 
 // Per-CTA smem stage: A hi/lo (K4) + this CTA's B rows (all N, or N/2 per pair).
 __host__ __device__ inline size_t tc_stage_bytes(int N, bool a_in_smem, bool pair) {
@@ -224,7 +227,7 @@ __host__ __device__ inline size_t tc_smem_bytes(int N, bool a_in_smem, bool pair
                                                 bool epi_stage = false, bool tot_smem = false) {
   return 1024 /*align slack*/ + stages * tc_stage_bytes(N, a_in_smem, pair) +
          (tot_smem ? kTotSmemBytes : 0) + (epi_stage ? kEpiStageTotal : kTileKeysBytes) +
-         sizeof(TcSmem);
+         (tot_smem ? sizeof(TcSmemT<32>) : sizeof(TcSmemT<8>));
 }
 // TMEM columns: accumulators [0, 2N); K2's A stages (hi 32 + lo 32 columns
 // each) from column 2N: 2N + 64 * 3 <= 512 for N <= 160.
@@ -233,7 +236,8 @@ __host__ __device__ constexpr int tc_a_tmem_col(int N, int s) { return 2 * N + 6
 // Fold TMEM accumulator buffer of global group `g` into this thread's totals:
 // row = 32*(warp%4) + lane, columns [half*N/2, half*N/2 + N/2); release the
 // buffer on `acc_empty_addr` (the leader's barrier for pairs).
-__device__ __forceinline__ void tc_drain(const TcParams& p, TcSmem* bar, bool remote,
+template <class Bar>
+__device__ __forceinline__ void tc_drain(const TcParams& p, Bar* bar, bool remote,
                                          uint32_t acc_empty_addr0, uint32_t tmem, int g, int nc,
                                          int quarter, int half, float (&tot)[kTcMaxN / 2]) {
   const int b = g & 1;
@@ -915,6 +919,8 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   float* tot_smem = reinterpret_cast<float*>(smem + S * stage_bytes);
   uint8_t* epi_stage = smem + S * stage_bytes + (Cfg::kTotSmem ? kTotSmemBytes : 0);
   unsigned long long* tile_keys = reinterpret_cast<unsigned long long*>(epi_stage);
+  using TcSmem = TcSmemT<Cfg::kItemRing>;
+  constexpr int kItemRing = Cfg::kItemRing;
   TcSmem* bar = reinterpret_cast<TcSmem*>(epi_stage +
                                           (Cfg::kEpiStage ? kEpiStageTotal : kTileKeysBytes));
   // kASinc: per pair (end column, column of lag 0), after the barriers
@@ -1348,7 +1354,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // item of the group being folded, cached per warp in shared memory
     // (item_of divides; registers are scarce in the 18-warp kernels)
     int f_it = -1;
-    int4* const f_cache = &bar->item_cache[(warp - kGenW0) & 15];
+    int4* const f_cache = &bar->item_cache[Cfg::kItemRing > 8 ? (warp - kGenW0) & 15 : 0];
     auto fold_step = [&]() {
       if (f_it != d_it) {
         const Item ti = item_of(item_id(d_it));
