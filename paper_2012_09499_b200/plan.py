@@ -108,7 +108,7 @@ class SrpPlan:
     def _init(self, tdoa_table, pair_m, pair_mp, tdoa_bounds, bin_frequencies,
                  sample_period=None, n_aux=None, weights="auto",
                  max_weight_bytes=DEFAULT_MAX_WEIGHT_BYTES, conventional=True, backend="auto",
-                 kb_per_group=4, interp_kb_per_group=10, precision="auto", _geometry=None):
+                 kb_per_group=4, interp_kb_per_group=None, precision="auto", _geometry=None):
         if precision not in ("auto", "tf32"):
             raise ValueError(f"precision must be auto|tf32, got {precision!r}")
         self.precision = precision
@@ -120,14 +120,21 @@ class SrpPlan:
         # K2's long K (2 P Kb) folds every 4 blocks (48 MMA steps, ~6e-7);
         # K4's short K (C2: 19 blocks) folds every 10 (120 steps, ~1.5e-6).
         self.kb_per_group = int(kb_per_group)
-        self.interp_kb_per_group = int(interp_kb_per_group)
+        self.interp_kb_per_group = 10 if interp_kb_per_group is None else int(interp_kb_per_group)
         # 3xFP16 blocks hold 64 elements but the same 12 MMA accumulations as
         # a tf32 block, and the drift grows with accumulations.  Measured K2
         # rel-L2 vs the oracle at full C2 J / C4's K (tools/conv_kbg_accuracy.py):
         # period 4: 1.5e-6, 8: 3.4e-6, 16: 7.1e-6, 32: 1.1e-5 -> 8 keeps a 3x
         # margin under the 1e-5 tolerance and is ~6% faster than 4
         self.kb_per_group16 = 2 * self.kb_per_group
-        self.interp_kb_per_group16 = self.interp_kb_per_group
+        # 3xFP16 K4 (stored and on-the-fly weights share it: their maps are
+        # bitwise equal): the error is almost all a scale bias growing with
+        # the period -- measured at C4 (P = 496, 2246 K blocks, 8 frames x 2048
+        # candidates, tools/otf_kbg_accuracy.py): period 10: 2.1e-6, 16:
+        # 3.1e-6, 24: 4.6e-6, 32: 6.1e-6; 16 keeps the 3x margin (on-the-fly
+        # K4 at C4 shapes 1.5% faster than 10, fewer folds)
+        self.interp_kb_per_group16 = (16 if interp_kb_per_group is None
+                                      else self.interp_kb_per_group)
         self.W_hi = self.W_lo = None
         self.W16 = None
         omega = np.asarray(bin_frequencies, dtype=np.float64)

@@ -37,7 +37,7 @@ def main():
     ap.add_argument("--cands", type=int, default=600000)
     ap.add_argument("--conv-cands", type=int, default=40000)
     ap.add_argument("--reps", type=int, default=2)
-    ap.add_argument("--kbg", type=int, default=10, help="K blocks per accumulator group (K4)")
+    ap.add_argument("--kbg", type=int, default=None, help="K blocks per accumulator group (K4; default: the plan's)")
     args = ap.parse_args()
     rng = np.random.default_rng(np.random.SeedSequence([4, 0, 0]))
     box = np.array([6.0, 5.0, 3.0])
