@@ -190,6 +190,14 @@ __device__ __forceinline__ float rcp_approx_ftz(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Reciprocals of an (even, odd) column pair's denominators from one MUFU:
+// P = 1 / (xe xo), 1 / xe = xo P, 1 / xo = xe P (<= ~2.5 ulp; |x| >= 0.5 or
+// a normal |f| > 1e-30, so xe xo neither over- nor underflows).  odd selects
+// the column.  The tensor-core generator evaluates the same expressions.
+__device__ __forceinline__ float sinc_pair_rcp(float xe, float xo, int odd) {
+  const float P = rcp_approx_ftz(xe * xo);
+  return (odd ? xe : xo) * P;
+}
 __device__ __forceinline__ float sinc_spi(float f) {
   return sinpif(f) * 0.318309886183790671538f;  // sin(pi f) / pi
 }

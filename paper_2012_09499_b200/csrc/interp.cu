@@ -41,8 +41,25 @@ __global__ void sinc_table_kernel(const int32_t* __restrict__ sx_i, const float*
     const int i = sx_i[static_cast<size_t>(p) * J + j];
     const float fr = sx_f[static_cast<size_t>(p) * J + j];
     const float spi = sinc_spi(fr);
-    for (int ni = threadIdx.x; ni < 2 * R + 1; ni += blockDim.x)
-      row[base + ni] = sinc_weight_fast(i, fr, spi, ni - R);
+    const int end = off[p + 1];
+    for (int ni = threadIdx.x; ni < 2 * R + 1; ni += blockDim.x) {
+      // the on-the-fly tensor-core generator takes the two reciprocals of an
+      // (even, odd) column pair from one (sinc_pair_rcp) wherever the pair's
+      // 16-column slab lies inside this pair's columns; the table follows
+      // it so both kernels see the same weights bit for bit
+      const int t = base + ni;
+      const int s0 = t & ~15;
+      if (!sinc_is_node(fr) && s0 >= base && s0 + 16 <= end) {
+        const int te = t & ~1;
+        const float xe = static_cast<float>(i - (te - base - R)) + fr;
+        const float xo = static_cast<float>(i - (te + 1 - base - R)) + fr;
+        const float r = sinc_pair_rcp(xe, xo, t & 1);
+        const int d = i - (ni - R);
+        row[t] = __uint_as_float(__float_as_uint(spi * r) ^ (static_cast<uint32_t>(d & 1) << 31));
+      } else {
+        row[t] = sinc_weight_fast(i, fr, spi, ni - R);
+      }
+    }
   }
   for (int t = off[P] + threadIdx.x; t < T_pad; t += blockDim.x) row[t] = 0.0f;
 }
