@@ -1870,6 +1870,11 @@ cudaError_t launch_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, 
   // (dynamic items: the tile's Xi rows fit L2, 92 MB at C4; measured with
   // the static lockstep schedule: 2.13 vs 2.06 s per C4 step)
   p.m_fast = getenv("SRPB_OTF_NFAST") ? 0 : 1;
+  // SRPB_OTF_LOCKSTEP=1 (experiments): static items with the wave barrier, as K2
+  if (getenv("SRPB_OTF_LOCKSTEP") && done) {
+    p.dynamic = 0;
+    p.lockstep = 1;
+  }
   p.scale = 1.0f / (kF16PhaseScale * xi_scale);
   p.maps = maps;
   p.keys = keys;
