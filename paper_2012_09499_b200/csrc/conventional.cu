@@ -112,11 +112,112 @@ conventional_simt_kernel(const float* __restrict__ Psi, int F, int P, int Kb, in
   simt_epilogue(tot, 2.0, j0, f0, J, F, tj, tf, maps, keys);
 }
 
+// Few-frame batches (C5 batch 1, real-time localisation): the GEMM form
+// wastes the tile's frame columns and every steering phase is generated for
+// a single frame, so each thread takes one candidate and walks the bins of
+// every pair with the phase recurrence -- exact anchor (integer-reduced
+// turns + sincospif) every 16 bins, one-bin rotations in between (chain <=
+// 15 rotations, as the tensor-core generator) -- accumulating
+// 2 Re(e^{j w_k tau} psi_k) for its kF frames straight from the block's
+// shared copy of the pair's cross-spectra (broadcast reads).  fp32 per pair,
+// folded into fp64 (the reference's per-pair acc += order, srp.py:420-422).
+constexpr int kFewThreads = 256;
+constexpr int kFewMaxFrames = 4;
+
+template <int kF>
+__global__ void __launch_bounds__(kFewThreads)
+conventional_few_kernel(const float2* __restrict__ Psi, int F, int P, int Kb, int period, int mask,
+                        const int32_t* __restrict__ tau_i, const float* __restrict__ tau_f, int J,
+                        float* __restrict__ maps, unsigned long long* __restrict__ keys) {
+  extern __shared__ float2 s_psi[];  // [Kb][kF] of the current pair
+  __shared__ unsigned long long s_key[kFewThreads / 32][kF];
+  const int j = blockIdx.x * kFewThreads + threadIdx.x;
+  const float inv_period = 1.0f / static_cast<float>(period);
+  double tot[kF];
+#pragma unroll
+  for (int f = 0; f < kF; ++f) tot[f] = 0.0;
+  for (int p = 0; p < P; ++p) {
+    __syncthreads();  // the previous pair's spectra are consumed
+    for (int e = threadIdx.x; e < Kb * kF; e += kFewThreads) {
+      const int k = e / kF, f = e - (e / kF) * kF;
+      s_psi[e] = f < F ? Psi[(static_cast<size_t>(f) * P + p) * Kb + k] : make_float2(0.0f, 0.0f);
+    }
+    __syncthreads();
+    int ti = 0;
+    float tf = 0.0f;
+    if (j < J) {
+      ti = __ldg(tau_i + static_cast<size_t>(p) * J + j);
+      tf = __ldg(tau_f + static_cast<size_t>(p) * J + j);
+    }
+    float c1, s1;  // one-bin rotation
+    harmonic_phase(1, ti, tf, period, mask, inv_period, &c1, &s1);
+    float acc[kF];
+#pragma unroll
+    for (int f = 0; f < kF; ++f) acc[f] = 0.0f;
+    for (int k0 = 0; k0 < Kb; k0 += 16) {
+      float c, sn;
+      harmonic_phase(k0, ti, tf, period, mask, inv_period, &c, &sn);
+      const int nk = min(16, Kb - k0);
+#pragma unroll 4
+      for (int kk = 0; kk < nk; ++kk) {
+        const float2* v = s_psi + (k0 + kk) * kF;
+#pragma unroll
+        for (int f = 0; f < kF; ++f) {
+          acc[f] = fmaf(c, v[f].x, acc[f]);
+          acc[f] = fmaf(-sn, v[f].y, acc[f]);
+        }
+        const float cn = c * c1 - sn * s1;
+        sn = fmaf(c, s1, sn * c1);
+        c = cn;
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < kF; ++f) tot[f] += static_cast<double>(acc[f]);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int f = 0; f < kF; ++f) {
+    const float v = static_cast<float>(2.0 * tot[f]);
+    unsigned long long k = 0ull;
+    if (j < J && f < F) {
+      if (maps) __stcs(maps + static_cast<size_t>(f) * J + j, v);
+      k = make_key(v, static_cast<uint32_t>(j));
+    }
+    k = warp_key_max(k);
+    if (lane == 0) s_key[w][f] = k;
+  }
+  __syncthreads();
+  if (keys && threadIdx.x < kF && threadIdx.x < F) {
+    unsigned long long k = 0ull;
+#pragma unroll
+    for (int q = 0; q < kFewThreads / 32; ++q) k = key_max(k, s_key[q][threadIdx.x]);
+    if (k != 0ull) atomicMax(keys + threadIdx.x, k);
+  }
+}
+
+template <int kF>
+cudaError_t launch_few(const float* Psi, int F, int P, int Kb, int period, int mask,
+                       const int32_t* tau_i, const float* tau_f, int J, float* maps,
+                       unsigned long long* keys, cudaStream_t stream) {
+  const size_t smem = sizeof(float2) * static_cast<size_t>(Kb) * kF;
+  auto kern = conventional_few_kernel<kF>;
+  cudaError_t e = allow_dynamic_smem(kern, smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(J + kFewThreads - 1) / kFewThreads, kFewThreads, smem, stream>>>(
+      reinterpret_cast<const float2*>(Psi), F, P, Kb, period, mask, tau_i, tau_f, J, maps, keys);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_conventional(const float* Psi, int F, int P, int Kb, int period,
                                 const int32_t* tau_i, const float* tau_f, int J, float* maps,
                                 unsigned long long* keys, cudaStream_t stream) {
   if (F == 0 || J == 0) return cudaSuccess;
   const int mask = (period & (period - 1)) == 0 ? period - 1 : 0;
+  if (F <= kFewMaxFrames && static_cast<size_t>(Kb) * kFewMaxFrames * sizeof(float2) <= 200 * 1024) {
+    if (F == 1) return launch_few<1>(Psi, F, P, Kb, period, mask, tau_i, tau_f, J, maps, keys, stream);
+    if (F == 2) return launch_few<2>(Psi, F, P, Kb, period, mask, tau_i, tau_f, J, maps, keys, stream);
+    return launch_few<4>(Psi, F, P, Kb, period, mask, tau_i, tau_f, J, maps, keys, stream);
+  }
   dim3 grid((J + kTileJ - 1) / kTileJ, (F + kTileF - 1) / kTileF);
   conventional_simt_kernel<true><<<grid, kGemmThreads, 0, stream>>>(
       Psi, F, P, Kb, period, mask, tau_i, tau_f, nullptr, nullptr, J, maps, keys);

@@ -34,6 +34,9 @@ from .geometry import TDOA_BOUND_SLACK
 DEFAULT_PHAT_FLOOR_REL = 1e-12  # spectral.py:31-32
 #: store W when it needs at most this many bytes (else generate on the fly)
 DEFAULT_MAX_WEIGHT_BYTES = 48 << 30
+#: conventional batches up to this many frames take the few-frame SIMT kernel
+#: (conventional.cu conventional_few_kernel; kFewMaxFrames)
+FEW_FRAMES = 4
 
 
 def is_harmonic(omega: np.ndarray) -> bool:
@@ -418,10 +421,15 @@ class SrpPlan:
         at C5 (J = 200k): even at F = 1 the tcgen05 kernels win (the steering
         phases / weights dominate and are shared by the frames of a tile), so
         the SIMT kernels serve only shapes the tensor-core path cannot take
-        (Kb % 16 != 0, non-harmonic bins, tf32 without a stored W)."""
+        (Kb % 16 != 0, non-harmonic bins, tf32 without a stored W) -- and
+        conventional batches of <= FEW_FRAMES frames with harmonic bins, which
+        the per-candidate phase-recurrence kernel serves (C5 batch 1: 2.83 ms
+        on the tensor cores, whose frame tile is 31/32 idle there)."""
         if self.backend == "simt":
             return False
         if kind == "conv":
+            if self.backend != "tc" and self.harmonic and F <= FEW_FRAMES:
+                return False
             ok = self.harmonic and self.Kb % 16 == 0
         elif kind == "interp16":  # 3xFP16 K4: stored W or weights generated in TMEM
             ok = True

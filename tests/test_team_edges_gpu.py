@@ -93,3 +93,30 @@ def test_conventional_teams_odd_blocks_per_pair(kb):
     got = maps.cpu().numpy()[:, sel]
     assert_maps_match(got, ref, np.searchsorted(sel, am.cpu().numpy()),
                       what=f"conventional Kb={kb}")
+
+
+@pytest.mark.parametrize("F", [1, 2, 3, 4])
+def test_conventional_few_frames_vs_oracle(F):
+    """Few-frame conventional batches (C5 batch 1 ..) take the per-candidate
+    phase-recurrence kernel (conventional.cu conventional_few_kernel): maps
+    and argmax vs the oracle, and vs the tensor-core K2 on the same psi."""
+    rng = np.random.default_rng(100 + F)
+    ang = 2 * np.pi * np.arange(8) / 8
+    mic = np.stack([0.1 * np.cos(ang), 0.1 * np.sin(ang), np.full(8, 1.2)], axis=1)
+    pts = rng.uniform([-2.5, -2.5, 0.0], [2.5, 2.5, 2.5], size=(40_000, 3))
+    pairs, pm, pmp, bounds, tdoa = _geometry(mic, pts)
+    omega = O.bin_frequencies(16000.0, 1024)
+    Y = _spectra(rng, F, 8, omega.size)
+    plan = SrpPlan(tdoa, pm, pmp, bounds, omega)
+    maps, am = plan.run(torch.from_numpy(Y).cuda(), "conventional")
+    torch.cuda.synchronize()
+    psi = np.stack([O.cross_spectrum(Y[f].astype(np.complex128), pm, pmp)[0] for f in range(F)])
+    sel = np.unique(np.concatenate([rng.choice(pts.shape[0], 4000, replace=False),
+                                    am.cpu().numpy()]))
+    ref = O.conventional_frames(psi, omega, tdoa[sel])
+    assert_maps_match(maps.cpu().numpy()[:, sel], ref, np.searchsorted(sel, am.cpu().numpy()),
+                      what=f"few-frame conventional F={F}")
+    tc = SrpPlan(tdoa, pm, pmp, bounds, omega, backend="tc")
+    m2, a2 = tc.run(torch.from_numpy(Y).cuda(), "conventional")
+    assert rel_l2(maps.cpu().numpy(), m2.cpu().numpy()) <= 1e-5
+    assert torch.equal(am.cpu(), a2.cpu())
