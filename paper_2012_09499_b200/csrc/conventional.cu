@@ -121,8 +121,10 @@ conventional_simt_kernel(const float* __restrict__ Psi, int F, int P, int Kb, in
 // 2 Re(e^{j w_k tau} psi_k) for its kF frames straight from the block's
 // shared copy of the pair's cross-spectra (broadcast reads).  fp32 per pair,
 // folded into fp64 (the reference's per-pair acc += order, srp.py:420-422).
-constexpr int kFewThreads = 256;
+constexpr int kFewThreads = 128;
 constexpr int kFewMaxFrames = 4;
+
+constexpr int kFewCands = 4;  // candidates per thread (share the spectra reads)
 
 template <int kF>
 __global__ void __launch_bounds__(kFewThreads)
@@ -131,11 +133,14 @@ conventional_few_kernel(const float2* __restrict__ Psi, int F, int P, int Kb, in
                         float* __restrict__ maps, unsigned long long* __restrict__ keys) {
   extern __shared__ float2 s_psi[];  // [Kb][kF] of the current pair
   __shared__ unsigned long long s_key[kFewThreads / 32][kF];
-  const int j = blockIdx.x * kFewThreads + threadIdx.x;
+  // candidates j0 + kFewThreads * c of this thread (coalesced per c)
+  const int j0 = blockIdx.x * (kFewThreads * kFewCands) + threadIdx.x;
   const float inv_period = 1.0f / static_cast<float>(period);
-  double tot[kF];
+  double tot[kFewCands][kF];
 #pragma unroll
-  for (int f = 0; f < kF; ++f) tot[f] = 0.0;
+  for (int c = 0; c < kFewCands; ++c)
+#pragma unroll
+    for (int f = 0; f < kF; ++f) tot[c][f] = 0.0;
   for (int p = 0; p < P; ++p) {
     __syncthreads();  // the previous pair's spectra are consumed
     for (int e = threadIdx.x; e < Kb * kF; e += kFewThreads) {
@@ -143,45 +148,65 @@ conventional_few_kernel(const float2* __restrict__ Psi, int F, int P, int Kb, in
       s_psi[e] = f < F ? Psi[(static_cast<size_t>(f) * P + p) * Kb + k] : make_float2(0.0f, 0.0f);
     }
     __syncthreads();
-    int ti = 0;
-    float tf = 0.0f;
-    if (j < J) {
-      ti = __ldg(tau_i + static_cast<size_t>(p) * J + j);
-      tf = __ldg(tau_f + static_cast<size_t>(p) * J + j);
-    }
-    float c1, s1;  // one-bin rotation
-    harmonic_phase(1, ti, tf, period, mask, inv_period, &c1, &s1);
-    float acc[kF];
+    int ti[kFewCands];
+    float tf[kFewCands], c1[kFewCands], s1[kFewCands];
 #pragma unroll
-    for (int f = 0; f < kF; ++f) acc[f] = 0.0f;
+    for (int c = 0; c < kFewCands; ++c) {
+      const int j = j0 + kFewThreads * c;
+      ti[c] = 0;
+      tf[c] = 0.0f;
+      if (j < J) {
+        ti[c] = __ldg(tau_i + static_cast<size_t>(p) * J + j);
+        tf[c] = __ldg(tau_f + static_cast<size_t>(p) * J + j);
+      }
+      harmonic_phase(1, ti[c], tf[c], period, mask, inv_period, &c1[c], &s1[c]);  // one bin
+    }
+    float acc[kFewCands][kF];
+#pragma unroll
+    for (int c = 0; c < kFewCands; ++c)
+#pragma unroll
+      for (int f = 0; f < kF; ++f) acc[c][f] = 0.0f;
     for (int k0 = 0; k0 < Kb; k0 += 16) {
-      float c, sn;
-      harmonic_phase(k0, ti, tf, period, mask, inv_period, &c, &sn);
+      float cs[kFewCands], sn[kFewCands];
+#pragma unroll
+      for (int c = 0; c < kFewCands; ++c)
+        harmonic_phase(k0, ti[c], tf[c], period, mask, inv_period, &cs[c], &sn[c]);
       const int nk = min(16, Kb - k0);
 #pragma unroll 4
       for (int kk = 0; kk < nk; ++kk) {
-        const float2* v = s_psi + (k0 + kk) * kF;
+        float2 v[kF];
 #pragma unroll
-        for (int f = 0; f < kF; ++f) {
-          acc[f] = fmaf(c, v[f].x, acc[f]);
-          acc[f] = fmaf(-sn, v[f].y, acc[f]);
+        for (int f = 0; f < kF; ++f) v[f] = s_psi[(k0 + kk) * kF + f];
+#pragma unroll
+        for (int c = 0; c < kFewCands; ++c) {
+#pragma unroll
+          for (int f = 0; f < kF; ++f) {
+            acc[c][f] = fmaf(cs[c], v[f].x, acc[c][f]);
+            acc[c][f] = fmaf(-sn[c], v[f].y, acc[c][f]);
+          }
+          const float cn = cs[c] * c1[c] - sn[c] * s1[c];
+          sn[c] = fmaf(cs[c], s1[c], sn[c] * c1[c]);
+          cs[c] = cn;
         }
-        const float cn = c * c1 - sn * s1;
-        sn = fmaf(c, s1, sn * c1);
-        c = cn;
       }
     }
 #pragma unroll
-    for (int f = 0; f < kF; ++f) tot[f] += static_cast<double>(acc[f]);
+    for (int c = 0; c < kFewCands; ++c)
+#pragma unroll
+      for (int f = 0; f < kF; ++f) tot[c][f] += static_cast<double>(acc[c][f]);
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int f = 0; f < kF; ++f) {
-    const float v = static_cast<float>(2.0 * tot[f]);
     unsigned long long k = 0ull;
-    if (j < J && f < F) {
-      if (maps) __stcs(maps + static_cast<size_t>(f) * J + j, v);
-      k = make_key(v, static_cast<uint32_t>(j));
+#pragma unroll
+    for (int c = 0; c < kFewCands; ++c) {
+      const int j = j0 + kFewThreads * c;
+      const float v = static_cast<float>(2.0 * tot[c][f]);
+      if (j < J && f < F) {
+        if (maps) __stcs(maps + static_cast<size_t>(f) * J + j, v);
+        k = key_max(k, make_key(v, static_cast<uint32_t>(j)));
+      }
     }
     k = warp_key_max(k);
     if (lane == 0) s_key[w][f] = k;
@@ -203,7 +228,8 @@ cudaError_t launch_few(const float* Psi, int F, int P, int Kb, int period, int m
   auto kern = conventional_few_kernel<kF>;
   cudaError_t e = allow_dynamic_smem(kern, smem);
   if (e != cudaSuccess) return e;
-  kern<<<(J + kFewThreads - 1) / kFewThreads, kFewThreads, smem, stream>>>(
+  const int per_block = kFewThreads * kFewCands;
+  kern<<<(J + per_block - 1) / per_block, kFewThreads, smem, stream>>>(
       reinterpret_cast<const float2*>(Psi), F, P, Kb, period, mask, tau_i, tau_f, J, maps, keys);
   return cudaGetLastError();
 }
