@@ -64,6 +64,9 @@ constexpr int kTcThreads = 384;
 constexpr int kTcMaxStages = 8;
 constexpr int kTcM = 128;            // candidate rows per CTA
 constexpr int kTcMaxN = 160;
+// generator modes (shared-memory totals, no register tiles): up to 192 frames
+// per tile (TMEM 2 x 192 accumulators + 2 A stages)
+constexpr int kTcMaxNGen = 192;
 constexpr int kTcKBlock = 32;        // tf32 elements per K block = one 128-B swizzle row
 constexpr int kTcKBlock16 = 64;      // fp16 elements per K block
 constexpr float kF16PhaseScale = 16384.0f;  // 2^14: steering phases / sinc weights
@@ -220,9 +223,9 @@ constexpr int kEpiChunk = 8;  // frames per staged chunk (one 1 KB swizzle atom)
 constexpr int kEpiStageBytes = kEpiChunk * 128;
 constexpr int kEpiStageTotal = kEpiWarps * 2 * kEpiStageBytes;
 // other kernels: per-quarter, per-frame tile argmax keys [4][kTcMaxN]
-constexpr int kTileKeysBytes = 4 * kTcMaxN * 8;
+constexpr int kTileKeysBytes = 4 * kTcMaxNGen * 8;
 // generator modes: running totals [2 halves x kTcMaxN / 2 columns][128 rows]
-constexpr int kTotSmemBytes = kTcMaxN * kTcM * 4;
+constexpr int kTotSmemBytes = kTcMaxNGen * kTcM * 4;
 __host__ __device__ inline size_t tc_smem_bytes(int N, bool a_in_smem, bool pair, int stages,
                                                 bool epi_stage = false, bool tot_smem = false) {
   return 1024 /*align slack*/ + stages * tc_stage_bytes(N, a_in_smem, pair) +
@@ -480,7 +483,7 @@ __device__ __forceinline__ void tc_write_chunks(const TcParams& p, unsigned long
           k[i] = keep > recv ? keep : recv;
         }
       }
-      if (lane < 16 && 16 * c + lane < ncols) tk[quarter * kTcMaxN + cbase + 16 * c + lane] = k[0];
+      if (lane < 16 && 16 * c + lane < ncols) tk[quarter * kTcMaxNGen + cbase + 16 * c + lane] = k[0];
     }
   }
   if (p.keys) {
@@ -492,7 +495,7 @@ __device__ __forceinline__ void tc_write_chunks(const TcParams& p, unsigned long
       if (((c + h) & 1) != team && cstep == 2) continue;  // the other team's chunk
       unsigned long long k = tk[col];
 #pragma unroll
-      for (int q = 1; q < 4; ++q) k = key_max(k, tk[q * kTcMaxN + col]);
+      for (int q = 1; q < 4; ++q) k = key_max(k, tk[q * kTcMaxNGen + col]);
       const int f = n0 + col;
       if (k != 0ull && f < p.F) atomicMax(p.keys + f, k);
     }
@@ -1061,7 +1064,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       mbar_init(&bar->item_empty[r], 1 + kCta * kGenWarps + (kCta - 1));
     }
     if (!Cfg::kEpiStage)
-      for (int c = 0; c < 4 * kTcMaxN; ++c) tile_keys[c] = 0ull;
+      for (int c = 0; c < 4 * kTcMaxNGen; ++c) tile_keys[c] = 0ull;
     fence_mbar_init();
   }
   tc_fence_before();
@@ -1327,9 +1330,9 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // kb_per_group blocks of slack)
     int d_chunk = -1;  // chunk of group `drained` next to fold (-1: not started)
     // generator modes: this thread's slice of the shared running totals
-    float* tot_s = tot_smem + half * (kTcMaxN / 2) * kTcM + 32 * quarter + lane;
+    float* tot_s = tot_smem + half * (kTcMaxNGen / 2) * kTcM + 32 * quarter + lane;
     if constexpr (Cfg::kTotSmem) {
-      for (int c = c0; c < kTcMaxN / 32; c += kTeams)
+      for (int c = c0; c < kTcMaxNGen / 32; c += kTeams)
 #pragma unroll
         for (int i = 0; i < 16; ++i) tot_s[(16 * c + i) * kTcM] = 0.0f;
     }
@@ -1588,12 +1591,13 @@ cudaError_t make_map(CUtensorMap* m, const void* base, int rows, int cols, int b
 }
 
 // Frames per tile: N-tiles of <= 160 frames, multiple of 32.
-int pick_n(int F) {
-  static int cap = -1;  // SRPB_TC_NMAX (experiments): narrower frame tiles
-  if (cap < 0) {
+int pick_n(int F, int hard_cap = kTcMaxN) {
+  static int env = -1;  // SRPB_TC_NMAX (experiments): narrower frame tiles
+  if (env < 0) {
     const char* e = getenv("SRPB_TC_NMAX");
-    cap = e ? max(32, min(kTcMaxN, atoi(e) / 32 * 32)) : kTcMaxN;
+    env = e ? max(32, atoi(e) / 32 * 32) : 0;
   }
+  const int cap = env ? min(env, hard_cap) : hard_cap;
   const int tiles = (F + cap - 1) / cap;
   const int per = (F + tiles - 1) / tiles;
   return (per + 31) / 32 * 32;
@@ -1672,8 +1676,18 @@ void enforce_fold_window(TcParams& p, int teams = 1) {
   p.groups_per_tile = max(1, p.num_kb / p.kb_per_group);
 }
 
-void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16) {
-  p.N = pick_n(p.F);
+// frame-tile cap of the generator kernels (SRPB_TC_GEN_NMAX: 160 or 192)
+int gen_nmax() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SRPB_TC_GEN_NMAX");
+    v = e ? max(32, min(kTcMaxNGen, atoi(e) / 32 * 32)) : kTcMaxN;
+  }
+  return v;
+}
+
+void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16, int nmax = kTcMaxN) {
+  p.N = pick_n(p.F, nmax);
   p.n_tiles = (p.F + p.N - 1) / p.N;
   const int m_tiles = (p.J + kTcM - 1) / kTcM;
   const int cta = pair ? 2 : 1;
@@ -1760,7 +1774,7 @@ static cudaError_t conventional_tc(const void* psi_hi, const void* psi_lo, bool 
   // signalling is absorbed (measured C4 shapes, F = 320, J = 148k: 125.5 ms
   // single-team single-CTA, 124.5 two teams, 117 two teams + pairs)
   const bool pair = use_pair((J + kTcM - 1) / kTcM, true);
-  finish_params(p, kb_per_group, pair, f16);
+  finish_params(p, kb_per_group, pair, f16, gen_nmax());
   enforce_fold_window(p, TcCfg<kAPhase, false, true>::kTeams);
   p.scale = f16 ? 2.0f / (kF16PhaseScale * psi_scale) : 2.0f;
   p.maps = maps;
@@ -1863,7 +1877,7 @@ cudaError_t launch_interp_tc16_onthefly(const int32_t* sx_i, const float* sx_f, 
   // CTA pairs: each SM streams half of the tile's B rows (Xi is re-read from
   // L2 by every candidate tile; the weights are generated, not loaded)
   const bool pair = use_pair_otf((J + kTcM - 1) / kTcM);
-  finish_params(p, kb_per_group, pair, true);
+  finish_params(p, kb_per_group, pair, true, gen_nmax());
   enforce_fold_window(p, pair ? TcCfg<kASinc, true, true>::kTeams : TcCfg<kASinc, false, true>::kTeams);
   // candidate tiles fastest: the CTAs in flight share one frame tile's Xi
   // rows in L2 instead of streaming every frame tile's
