@@ -224,12 +224,12 @@ constexpr int kEpiStageBytes = kEpiChunk * 128;
 constexpr int kEpiStageTotal = kEpiWarps * 2 * kEpiStageBytes;
 // other kernels: per-quarter, per-frame tile argmax keys [4][kTcMaxN]
 constexpr int kTileKeysBytes = 4 * kTcMaxNGen * 8;
-// generator modes: running totals [2 halves x kTcMaxN / 2 columns][128 rows]
-constexpr int kTotSmemBytes = kTcMaxNGen * kTcM * 4;
+// generator modes: running totals [2 halves x N / 2 columns][128 rows]
+__host__ __device__ inline size_t tot_smem_bytes(int N) { return size_t(N) * kTcM * 4; }
 __host__ __device__ inline size_t tc_smem_bytes(int N, bool a_in_smem, bool pair, int stages,
                                                 bool epi_stage = false, bool tot_smem = false) {
   return 1024 /*align slack*/ + stages * tc_stage_bytes(N, a_in_smem, pair) +
-         (tot_smem ? kTotSmemBytes : 0) + (epi_stage ? kEpiStageTotal : kTileKeysBytes) +
+         (tot_smem ? tot_smem_bytes(N) : 0) + (epi_stage ? kEpiStageTotal : kTileKeysBytes) +
          (tot_smem ? sizeof(TcSmemT<32>) : sizeof(TcSmemT<8>));
 }
 // TMEM columns: accumulators [0, 2N); K2's A stages (hi 32 + lo 32 columns
@@ -929,7 +929,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
   // [stages][running totals (generator modes)][epilogue staging (K4 pairs) |
   // tile argmax keys][barriers]
   float* tot_smem = reinterpret_cast<float*>(smem + S * stage_bytes);
-  uint8_t* epi_stage = smem + S * stage_bytes + (Cfg::kTotSmem ? kTotSmemBytes : 0);
+  uint8_t* epi_stage = smem + S * stage_bytes + (Cfg::kTotSmem ? tot_smem_bytes(p.N) : 0);
   unsigned long long* tile_keys = reinterpret_cast<unsigned long long*>(epi_stage);
   using TcSmem = TcSmemT<Cfg::kItemRing>;
   constexpr int kItemRing = Cfg::kItemRing;
@@ -1330,9 +1330,9 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     // kb_per_group blocks of slack)
     int d_chunk = -1;  // chunk of group `drained` next to fold (-1: not started)
     // generator modes: this thread's slice of the shared running totals
-    float* tot_s = tot_smem + half * (kTcMaxNGen / 2) * kTcM + 32 * quarter + lane;
+    float* tot_s = tot_smem + half * (p.N / 2) * kTcM + 32 * quarter + lane;
     if constexpr (Cfg::kTotSmem) {
-      for (int c = c0; c < kTcMaxNGen / 32; c += kTeams)
+      for (int c = c0; c < p.N / 32; c += kTeams)
 #pragma unroll
         for (int i = 0; i < 16; ++i) tot_s[(16 * c + i) * kTcM] = 0.0f;
     }
