@@ -766,7 +766,10 @@ constexpr int kLtRW = kLtRows / kLtGenWarps;  // rows per generator warp (8)
 constexpr int kLtWarp0 = 2;  // first generator warp
 constexpr int kLtThreads = 32 * (kLtWarp0 + kLtGenWarps);
 constexpr int kLtStages = 4;
-constexpr int kLtMaxN = 64;
+constexpr int kLtMaxN = 64;     // lag slots per pass
+constexpr int kLtMaxPasses = 16;  // long lattices (C4: 2L + 1 = 603) run in passes of
+                                  // kLtMaxN slots (grid y), the psi rows regenerated per pass
+constexpr int kLtOS = kLtRows + 1;  // slot stride of the C staging (odd: conflict-free rows)
 constexpr float kLtScale = 16384.0f;  // 2^14 on both operands
 // TMEM accumulation drift: bin blocks go to fresh accumulators in groups of
 // 4 (48 MMA steps per chain, as K2 / K4), summed in order by the epilogue
@@ -802,16 +805,20 @@ __host__ __device__ inline size_t lt_y_bytes(int nF, int M) { return size_t(nF) 
 __host__ __device__ inline size_t lt_stage_bytes(int N, int nF, int M) {
   return (2 * 16384 + 2 * size_t(N) * 128 + lt_y_bytes(nF, M) + 1023) / 1024 * 1024;
 }
-__host__ __device__ inline size_t lt_smem_bytes(int N, int nF, int M, int S) {
-  return 1024 + S * lt_stage_bytes(N, nF, M) + 2 * size_t(kLtRows) * N * 4 /*own, partner C*/ +
+// multipass: this CTA's own C lives in the idle stage ring (no Xi staging)
+__host__ __device__ inline size_t lt_smem_bytes(int N, int nF, int M, int S, bool multipass = false) {
+  return 1024 + S * lt_stage_bytes(N, nF, M) +
+         (multipass ? 1 : 2) * size_t(kLtOS) * N * 4 /*partner (and own) C*/ +
          sizeof(LtSmem);
 }
 // frames a 128-row tile spans
 inline int lt_frames(int P) { return (kLtRows - 1 + P - 1) / P + 1; }
 // stages that fit in 227 KB (0: the tile does not fit)
-inline int lt_stages(int N, int nF, int M) {
+inline int lt_stages(int N, int nF, int M, bool multipass = false) {
   for (int S = kLtStages; S >= 2; --S)
-    if (lt_smem_bytes(N, nF, M, S) + 1024 <= 232448) return S;
+    if (lt_smem_bytes(N, nF, M, S, multipass) + 1024 <= 232448 &&
+        (!multipass || S * lt_stage_bytes(N, nF, M) >= size_t(kLtOS) * N * 4))
+      return S;
   return 0;
 }
 
@@ -848,9 +855,14 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
   const int N = a.N;
   const int S = a.S;
   const size_t stage_bytes = lt_stage_bytes(N, a.nF, a.M);
-  float* s_part = reinterpret_cast<float*>(smem + S * stage_bytes);  // [N][128] from CTA 1
-  float* s_own = s_part + kLtRows * N;                                // [N][128] this CTA
-  LtSmem* sm = reinterpret_cast<LtSmem*>(s_own + kLtRows * N);
+  // [N][129] partial C of CTA 1 and of this CTA (multipass: in the stage
+  // ring, idle once this CTA's MMAs are done -- nothing is staged there)
+  const bool multipass = gridDim.y > 1;
+  float* s_part = reinterpret_cast<float*>(smem + S * stage_bytes);
+  float* s_own = multipass ? reinterpret_cast<float*>(smem) : s_part + kLtOS * N;
+  LtSmem* sm = reinterpret_cast<LtSmem*>(s_part + (multipass ? 1 : 2) * kLtOS * N);
+  // pass (grid y): lag slots [cb, cb + N) of the 2L + 1
+  const int cb = static_cast<int>(blockIdx.y) * N;
   auto a_hi = [&](int s) { return smem + s * stage_bytes; };
   auto a_lo = [&](int s) { return smem + s * stage_bytes + 16384; };
   auto b_hi = [&](int s) { return smem + s * stage_bytes + 32768; };
@@ -924,8 +936,8 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
         mbar_expect_tx(&sm->yfull[s], static_cast<uint32_t>(lt_y_bytes(a.nF, a.M)));
         tma_load_3d(y_st(s), &tmY, &sm->yfull[s], (kb0 + i) * 64, 0, f_lo);
         mbar_expect_tx(&sm->full[s], static_cast<uint32_t>(2 * N * 128));
-        tma_load_2d(b_hi(s), &tmB_hi, &sm->full[s], (kb0 + i) * 64, 0);
-        tma_load_2d(b_lo(s), &tmB_lo, &sm->full[s], (kb0 + i) * 64, 0);
+        tma_load_2d(b_hi(s), &tmB_hi, &sm->full[s], (kb0 + i) * 64, cb);
+        tma_load_2d(b_lo(s), &tmB_lo, &sm->full[s], (kb0 + i) * 64, cb);
       }
       __syncwarp();
     }
@@ -1082,7 +1094,7 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
       }
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const uint32_t ad = dst + 4u * kLtRows * (c + e);
+        const uint32_t ad = dst + 4u * kLtOS * (c + e);
         if (rank == 1)
           st_shared_cluster_u32(ad, __float_as_uint(acc[e]));
         else
@@ -1108,12 +1120,53 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
   if (rank == 0) {
     for (int r = threadIdx.x; r < kLtRows; r += blockDim.x) {
       const long long R = R0 + r;
-      if (R < n_rows && a.spec_sum) {
+      if (R < n_rows && a.spec_sum && blockIdx.y == 0) {  // statistics: pass 0
         a.spec_sum[R] = sm->st_sum[0][r] + sm->st_sum[1][r];
         a.spec_min[R] = fminf(sm->st_min[0][r], sm->st_min[1][r]);
         a.spec_bad[R] = sm->st_bad[0][r] | sm->st_bad[1][r];
       }
     }
+    if (gridDim.y > 1) {
+      // multi-pass: a row's slots of this pass are one contiguous run of its
+      // Xi row; a warp per row, lanes over the slots (coalesced 2-byte
+      // stores; the [slot][129] staging keeps the reads conflict-free)
+      const float out_scale = 2.0f / (kLtScale * kLtScale);
+      if (!(a.dbg & 12)) {
+        for (int orow = warp; orow < kLtRows; orow += kLtThreads / 32) {
+          const long long R = R0 + orow;
+          if (R >= n_rows) break;
+          const int f = static_cast<int>(R / a.P), p = static_cast<int>(R - static_cast<long long>(f) * a.P);
+          const int Rp = __ldg(a.reach + p);
+          const int lo = max(cb, a.L - Rp), hi = min(cb + N - 1, a.L + Rp);
+          const size_t g0 = static_cast<size_t>(f) * a.T_pad + __ldg(a.off + p) + Rp - a.L;
+          for (int c = lo + lane; c <= hi; c += 32) {
+            const int cl = c - cb;
+            const float v = (s_own[cl * kLtOS + orow] + s_part[cl * kLtOS + orow]) * out_scale;
+            if (a.Xi) a.Xi[g0 + c] = v;
+            const float x = v * a.split_scale;
+            const __half hh = __float2half_rn(x);
+            a.Xi_hi[g0 + c] = hh;
+            a.Xi_lo[g0 + c] = __float2half_rn(x - __half2float(hh));
+          }
+        }
+        // pad columns past the last pair's lattice: pass 0 of the frame's
+        // last row writes them
+        if (blockIdx.y == 0) {
+          const int t_pad0 = __ldg(a.off + a.P);
+          const long long R_end = min(R0 + kLtRows, n_rows);
+          for (long long R = R0 + warp; R < R_end; R += kLtThreads / 32) {
+            const int f = static_cast<int>(R / a.P);
+            if (R - static_cast<long long>(f) * a.P != a.P - 1) continue;
+            const size_t g0 = static_cast<size_t>(f) * a.T_pad;
+            for (int c = t_pad0 + lane; c < a.T_pad; c += 32) {
+              if (a.Xi) a.Xi[g0 + c] = 0.0f;
+              a.Xi_hi[g0 + c] = __float2half_rn(0.0f);
+              a.Xi_lo[g0 + c] = __float2half_rn(0.0f);
+            }
+          }
+        }
+      }
+    } else {
     // Xi rows of the tile's frames are staged in shared memory (the stage
     // ring is idle now) and leave with coalesced stores: each tile row owns
     // 2 reach_p + 1 scattered columns, which as direct 2-byte global stores
@@ -1137,7 +1190,7 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
         for (int c = a.L - Rp + sub; c <= a.L + Rp; c += 4) {
           const int n = c - a.L;
           {
-            const float v = (own[c * kLtRows] + part[c * kLtRows]) * out_scale;
+            const float v = (own[c * kLtOS] + part[c * kLtOS]) * out_scale;
             const int idx = col0 + n;
             if (a.Xi) xs[idx] = v;
             const float x = v * a.split_scale;
@@ -1171,6 +1224,7 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
         }
       }
     }
+    }  // single pass
     if (a.frame_cnt) {
       // floor fix-up without a second kernel: the CTA that completes a frame
       // (its rows can span two tiles) checks the frame's statistics and, if
@@ -1180,7 +1234,7 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
       if (threadIdx.x == 0) {
         const long long R_end = min(R0 + kLtRows, n_rows);
         int nd = 0;
-        for (int fl = 0; fl < nF; ++fl) {
+        for (int fl = 0; fl < a.nF; ++fl) {
           const long long f = f_lo + fl;
           const long long r_lo = max(R0, f * a.P), r_hi = min(R_end, (f + 1) * a.P);
           if (r_lo >= r_hi) break;
@@ -1271,26 +1325,46 @@ cudaError_t launch_lattice_tc_twiddles(const double* omega, int Kb, double T, in
 }
 
 // whether the tensor-core lattice serves this shape
+// slots per pass and passes of the tensor-core lattice: one pass up to 64
+// slots; beyond, the widest pass whose stages fit next to the partner's C
+// (psi rows are regenerated per pass, so fewer passes is the saving)
+inline int lt_pass_n(int L, int P = 0, int M = 0) {
+  const int n = lattice_tc_n(L);
+  if (n <= kLtMaxN) return n;
+  if (P > 0)
+    for (int N = min(128, n); N > kLtMaxN; N -= 16)
+      if (lt_stages(N, lt_frames(P), M, (n + N - 1) / N > 1) >= 2) return N;
+  return kLtMaxN;
+}
+inline int lt_passes(int L, int P = 0, int M = 0) {
+  const int N = lt_pass_n(L, P, M);
+  return (lattice_tc_n(L) + N - 1) / N;
+}
+
 bool lattice_tc_ok(int Kb, int L, float split_scale, const void* Xi_hi) {
-  return Kb % 32 == 0 && Kb >= 64 && lattice_tc_n(L) <= kLtMaxN && split_scale != 0.0f &&
+  return Kb % 32 == 0 && Kb >= 64 && lt_passes(L) <= kLtMaxPasses && split_scale != 0.0f &&
          Xi_hi != nullptr && getenv("SRPB_LATTICE_SIMT") == nullptr;
 }
 
 // shapes the tensor-core lattice serves (besides PHAT + fp16 split output)
 bool lattice_tc_shape_ok(int M, int P, int Kb, int L, int T_pad) {
-  if (Kb % 32 != 0 || Kb < 64 || lattice_tc_n(L) > kLtMaxN || M > 256 || P < 1) return false;
+  if (Kb % 32 != 0 || Kb < 64 || lt_passes(L) > kLtMaxPasses || M > 256 || P < 1) return false;
   const int nF = lt_frames(P);
   if (nF > 256) return false;
-  const int S = lt_stages(lattice_tc_n(L), nF, M);
-  return S >= 2 &&  // the tile's spectra fit the stages, and its Xi rows the ring
-         static_cast<size_t>(nF) * T_pad * 8 <= S * lt_stage_bytes(lattice_tc_n(L), nF, M);
+  const int N = lt_pass_n(L, P, M);
+  const bool multi = lt_passes(L, P, M) > 1;
+  const int S = lt_stages(N, nF, M, multi);
+  // the tile's spectra fit the stages, and (single pass) its Xi rows the ring
+  return S >= 2 && (multi || static_cast<size_t>(nF) * T_pad * 8 <= S * lt_stage_bytes(N, nF, M));
 }
 
 static cudaError_t launch_lattice_tc(const LatticeArgs& la, int L, const void* bh, const void* bl,
                                      int* frame_cnt, cudaStream_t stream) {
-  const int N = lattice_tc_n(L);
+  const int N = lt_pass_n(L, la.P, la.M), passes = lt_passes(L, la.P, la.M);
+  if (passes > 1) frame_cnt = nullptr;  // the fix-up kernel follows (all passes done)
   CUtensorMap mh, ml;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * la.Kb), static_cast<cuuint64_t>(N)};
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(2 * la.Kb),
+                        static_cast<cuuint64_t>(lattice_tc_n(L))};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(2 * la.Kb) * 2};
   cuuint32_t box[2] = {64, static_cast<cuuint32_t>(N)};
   cudaError_t e = encode_tensor_map(&mh, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, bh, dims, strides, box,
@@ -1300,7 +1374,7 @@ static cudaError_t launch_lattice_tc(const LatticeArgs& la, int L, const void* b
                           CU_TENSOR_MAP_SWIZZLE_128B);
   if (e != cudaSuccess) return e;
   const int nF = lt_frames(la.P);
-  const int S = lt_stages(N, nF, la.M);
+  const int S = lt_stages(N, nF, la.M, passes > 1);
   // spectra as [F][M][2 Kb] floats; box = 32 bins x all mics x the tile's frames
   CUtensorMap my;
   {
@@ -1318,13 +1392,13 @@ static cudaError_t launch_lattice_tc(const LatticeArgs& la, int L, const void* b
            la.pm, la.pmp, la.off, la.reach, la.T_pad,
            la.Xi, static_cast<__half*>(la.Xi_hi), static_cast<__half*>(la.Xi_lo), la.split_scale,
            la.spec_sum, la.spec_min, la.spec_bad, frame_cnt, la};
-  const size_t smem = lt_smem_bytes(N, nF, la.M, S);
+  const size_t smem = lt_smem_bytes(N, nF, la.M, S, passes > 1);
   e = allow_dynamic_smem(lattice_tc_kernel, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const long long rows = static_cast<long long>(la.F) * la.P;
   const int tiles = static_cast<int>((rows + kLtRows - 1) / kLtRows);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * tiles);
+  cfg.gridDim = dim3(2 * tiles, passes);
   cfg.blockDim = dim3(kLtThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -1372,7 +1446,7 @@ cudaError_t launch_lattice_from_spectra(const float* Y, int F, int M, int Kb, co
       lattice_tc_shape_ok(M, P, Kb, L, T_pad))
   {
     e = launch_lattice_tc(a, L, tc_bh, tc_bl, frame_cnt, stream);
-    fixed_in_kernel = frame_cnt != nullptr;
+    fixed_in_kernel = frame_cnt != nullptr && lt_passes(L, P, M) == 1;
   } else {
     e = launch_lattice_args(a, true, max_Tp, stream);
   }

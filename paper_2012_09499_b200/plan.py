@@ -243,10 +243,10 @@ class SrpPlan:
                N.ptr(self.twiddles), s)
         # tensor-core lattice (PHAT, fp16 split): B = [cos; -sin] rows per lag
         # slot, 3xFP16 (srpb_lattice_tc_twiddles); shapes it serves: Kb a
-        # multiple of 32, 2L + 1 <= 64 lag slots
+        # multiple of 32, 2L + 1 <= 1024 lag slots (passes of 64 slots beyond 64)
         self.tc_twiddles = None
         n_tc = (2 * self.L + 1 + 15) // 16 * 16
-        if self.Kb % 32 == 0 and self.Kb >= 64 and n_tc <= 64:
+        if self.Kb % 32 == 0 and self.Kb >= 64 and n_tc <= 1024:
             self.tc_twiddles = tuple(torch.empty((n_tc, 2 * self.Kb), dtype=torch.float16,
                                                  device=dev) for _ in range(2))
             N.call("srpb_lattice_tc_twiddles", N.ptr(self.omega_dev), self.Kb, T, self.L,

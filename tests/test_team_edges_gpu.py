@@ -120,3 +120,47 @@ def test_conventional_few_frames_vs_oracle(F):
     m2, a2 = tc.run(torch.from_numpy(Y).cuda(), "conventional")
     assert rel_l2(maps.cpu().numpy(), m2.cpu().numpy()) <= 1e-5
     assert torch.equal(am.cpu(), a2.cpu())
+
+
+def _xi16(plan, Y):
+    hi, lo = plan.lattice_from_spectra(Y, split="f16")
+    return ((hi.double() + lo.double()) / plan.xi_scale16).cpu().numpy()
+
+
+@pytest.mark.parametrize("room,M", [((6.0, 5.0, 3.0), 12), ((0.9, 0.8, 0.5), 6)])
+def test_lattice_tensor_core_multipass(room, M):
+    """Tensor-core lattice with more than 64 lag slots (2L + 1 = 781 in a
+    6x5x3 m room: 13 passes of 64 slots; ~2 passes for the small room):
+    vs the SIMT lattice (3e-6) and the reference lattice (1e-5), pad columns
+    zero, bitwise repeatable, and speculative-floor edge frames redone by
+    the fix-up kernel after all passes."""
+    rng = np.random.default_rng(M)
+    mic = rng.uniform(0.0, 1.0, size=(M, 3)) * np.array(room)
+    pts = rng.uniform(0.0, 1.0, size=(64, 3)) * np.array(room)
+    pairs, pm, pmp, bounds, tdoa = _geometry(mic, pts)
+    omega = O.bin_frequencies(16000.0, 1024)
+    plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=2)
+    assert plan.lattice_tc and 2 * plan.L + 1 > 64
+    from paper_2012_09499_b200 import _native as NN
+    assert NN.query("srpb_lattice_tc_supported", M, plan.P, plan.Kb, plan.L, plan.T_pad)
+    Y = _spectra(rng, 21, M, omega.size)
+    Y[2, 1, 7] = 1e-13 + 0j     # floor edge cases (the fix-up redoes the frame)
+    Y[3, 0, 3] = 1e-20 + 1e-20j
+    Y[4] = 0
+    Yd = torch.from_numpy(Y).cuda()
+    tc = _xi16(plan, Yd)
+    assert np.array_equal(tc, _xi16(plan, Yd))
+    plan.lattice_tc = False
+    simt = _xi16(plan, Yd)
+    plan.lattice_tc = True
+    total = plan.total_samples
+    assert np.all(tc[:, total:] == 0.0)
+    for f in range(Y.shape[0]):
+        if f == 4:
+            assert np.all(tc[f] == 0.0)
+            continue
+        assert rel_l2(tc[f, :total], simt[f, :total]) <= 3e-6, f
+    for f in (0, 2, 3, 20):
+        psi = O.cross_spectrum(Y[f].astype(np.complex128), pm, pmp)[0]
+        ref = np.concatenate(O.gcc_lattice(psi, omega, bounds, T, 2)[1])
+        assert rel_l2(tc[f, :total], ref) <= REL_L2_TOL, f
