@@ -164,3 +164,50 @@ def test_lattice_tensor_core_multipass(room, M):
         psi = O.cross_spectrum(Y[f].astype(np.complex128), pm, pmp)[0]
         ref = np.concatenate(O.gcc_lattice(psi, omega, bounds, T, 2)[1])
         assert rel_l2(tc[f, :total], ref) <= REL_L2_TOL, f
+
+
+_SINGLE_CTA_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+sys.path.insert(0, sys.argv[1] + '/tests')
+from test_team_edges_gpu import _geometry, _spectra, T
+from oracle import srp_oracle as O
+from paper_2012_09499_b200.plan import SrpPlan
+rng = np.random.default_rng(5)
+mic = rng.uniform(0.0, 1.0, size=(10, 3)) * np.array([6.0, 5.0, 3.0])
+pts = rng.uniform(0.0, 1.0, size=(40_000, 3)) * np.array([6.0, 5.0, 3.0])
+pairs, pm, pmp, bounds, tdoa = _geometry(mic, pts)
+omega = O.bin_frequencies(16000.0, 1024)
+Y = torch.from_numpy(_spectra(rng, 40, 10, omega.size)).cuda()
+out = {}
+for w in ("onthefly", "stored"):
+    plan = SrpPlan(tdoa, pm, pmp, bounds, omega, sample_period=T, n_aux=2, weights=w)
+    m, a = plan.run(Y, "approx")
+    out[w] = (m.cpu().numpy(), a.cpu().numpy())
+m, a = plan.run(Y, "conventional")
+out["conv"] = (m.cpu().numpy(), a.cpu().numpy())
+np.savez(sys.argv[2], **{k + "_m": v[0] for k, v in out.items()}, **{k + "_a": v[1] for k, v in out.items()})
+"""
+
+
+def test_single_cta_and_paired_kernels_agree_bitwise(tmp_path):
+    """The CTA-pair (cta_group::2, default) and single-CTA variants of the
+    generator kernels (K2, on-the-fly K4) and of the stored-weight K4 give
+    bitwise identical maps and argmax (same per-element accumulation order);
+    the switches are read once per process, so each variant runs in its own."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for name, env in (("pair", {}), ("single", {"SRPB_OTF_PAIR": "0", "SRPB_TC_PAIR": "0"})):
+        path = tmp_path / f"{name}.npz"
+        e = dict(os.environ, **env)
+        subprocess.run([sys.executable, "-c", _SINGLE_CTA_SCRIPT, root, str(path)], env=e,
+                       check=True, timeout=600)
+        with np.load(path) as z:
+            res[name] = {k: z[k] for k in z.files}
+    for k in res["pair"]:
+        assert np.array_equal(res["pair"][k], res["single"][k]), k
+    assert np.array_equal(res["pair"]["onthefly_m"], res["pair"]["stored_m"])
