@@ -149,6 +149,9 @@ struct TcParams {
   int full_items;     // items run at full width; the tail wave's items are split
   int n_piece0;       // frames of a split item's pieces (the last: N - (k - 1) n_piece0)
   int n_pieces;       // pieces k per split item
+  int n_last;         // frames of the last frame tile (multiple of 32, <= N): the
+                      // tiles are N wide except the last, which covers only the
+                      // remaining frames (C4: 25 x 160 + 96, not 26 x 160)
   int total_items;    // full_items + k * (num_items - full_items)
   int num_kb;         // K blocks of 32 per tile
   int maps_tma;       // staged epilogue: maps stored by TMA (J % 4 == 0), else st.global
@@ -976,7 +979,7 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
     const int nt = p.m_fast ? b / p.m_units : b % p.n_tiles;
     r.m0 = (mt * kCta + rank) * kTcM;
     r.n0 = nt * p.N;
-    r.nc = p.N;
+    r.nc = nt == p.n_tiles - 1 ? p.n_last : p.N;
     if (piece >= 0) {
       r.n0 += piece * p.n_piece0;
       r.nc = piece < p.n_pieces - 1 ? p.n_piece0 : p.N - (p.n_pieces - 1) * p.n_piece0;
@@ -1701,7 +1704,10 @@ void finish_params(TcParams& p, int kb_per_group, bool pair, bool f16, int nmax 
   // 16-column chunks per column half)
   const int units = max(1, min(p.num_items, num_sms() / cta));
   p.n_piece0 = (p.N / 2 + 31) / 32 * 32;
-  const bool split = p.N >= 64 && p.n_piece0 < p.N && p.num_items > units &&
+  p.n_last = getenv("SRPB_TC_NOLAST") ? p.N
+                                      : min(p.N, (p.F - (p.n_tiles - 1) * p.N + 31) / 32 * 32);
+  // (a narrower last tile already shortens the tail wave: no piece split)
+  const bool split = p.N >= 64 && p.n_piece0 < p.N && p.n_last == p.N && p.num_items > units &&
                      p.num_items % units != 0 && getenv("SRPB_TC_NOSPLIT") == nullptr;
   p.full_items = split ? p.num_items / units * units : p.num_items;
   p.n_pieces = 2;
