@@ -74,7 +74,7 @@ constexpr int kEpiWarp0 = 4;
 constexpr int kEpiWarps = 8;
 constexpr int kABytes = kTcM * 128;  // one of A_hi / A_lo per stage
 
-enum : int { kAFromTma = 0, kAPhase = 1, kASinc = 2 };
+enum : int { kAFromTma = 0, kAPhase = 1, kASinc = 2, kALoad = 3 };
 
 #ifndef SRPB_K4_STAGES
 #define SRPB_K4_STAGES 4
@@ -193,6 +193,11 @@ struct TcParams {
   const int32_t* off;    // [P + 1] lattice column offsets
   const int32_t* reach;  // [P]
   int P;
+  // K4 with the stored fp16 W split loaded by the generator warps into TMEM
+  // (kALoad): rows of T_pad halves
+  const __half* w_hi;
+  const __half* w_lo;
+  int T_pad;
 };
 
 // Work-item ids in flight between the roles.  A generator warp releases an
@@ -901,6 +906,33 @@ struct SincGen {
   }
 };
 
+// Stored-weight "generator" (kALoad): the thread's 32 columns of its row of
+// the fp16 W split (64 contiguous bytes of hi and of lo) loaded with 16-byte
+// read-only loads and stored into the TMEM A stage -- the TS MMA then reads A
+// from tensor memory, taking A off the shared-memory path (the SS kernel moves
+// A through shared memory twice per stage: TMA write, two MMA reads).
+struct WLoadGen {
+  __device__ __forceinline__ void start_tile(const TcParams&) {}
+  __device__ __forceinline__ void block(const TcParams& prm, int j, int half, int kb,
+                                        uint32_t a_hi_tmem, uint32_t a_lo_tmem) {
+    uint32_t hi[16], lo[16];
+    const int t0 = 64 * kb + 32 * half;
+    const size_t row = static_cast<size_t>(j) * prm.T_pad;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 h = make_uint4(0u, 0u, 0u, 0u), l = h;
+      if (j < prm.J && t0 + 8 * q < prm.T_pad) {  // T_pad % 8 == 0: whole 16-byte chunks
+        h = __ldg(reinterpret_cast<const uint4*>(prm.w_hi + row + t0 + 8 * q));
+        l = __ldg(reinterpret_cast<const uint4*>(prm.w_lo + row + t0 + 8 * q));
+      }
+      hi[4 * q] = h.x; hi[4 * q + 1] = h.y; hi[4 * q + 2] = h.z; hi[4 * q + 3] = h.w;
+      lo[4 * q] = l.x; lo[4 * q + 1] = l.y; lo[4 * q + 2] = l.z; lo[4 * q + 3] = l.w;
+    }
+    tmem_st16(a_hi_tmem + 16 * half, hi);
+    tmem_st16(a_lo_tmem + 16 * half, lo);
+  }
+};
+
 template <int kAMode, bool kPair, bool kF16>
 __global__ void __launch_bounds__((TcCfg<kAMode, kPair, kF16>::kThreads), 1)
 srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
@@ -1442,7 +1474,9 @@ srp_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant_
       // [16*half, +16) of each 32-column A block
       const int r = 32 * quarter + lane;
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * quarter) << 16);
-      using Gen = typename std::conditional<kAMode == kASinc, SincGen, PhaseGen<kF16, kTeams>>::type;
+      using Gen = typename std::conditional<
+          kAMode == kASinc, SincGen,
+          typename std::conditional<kAMode == kALoad, WLoadGen, PhaseGen<kF16, kTeams>>::type>::type;
       Gen gen;
       // global K block kg (across items) and its stage ring position; a team
       // takes every kTeams-th block (S >= 2 >= kTeams)
@@ -1837,6 +1871,23 @@ static cudaError_t interp_tc(const void* w_hi, const void* w_lo, const void* xi_
   p.keys = keys;
   p.argmax_out = argmax_out;
   p.done = done;
+  static const bool ts = getenv("SRPB_K4_TS") != nullptr;
+  if (f16 && ts && T_pad % 8 == 0) {
+    // A (W split) loaded into TMEM by the generator warps: TS MMA
+    p.kb_per_group = max(p.kb_per_group, 2);
+    enforce_fold_window(p, TcCfg<kALoad, false, true>::kTeams);
+    p.full_items = p.num_items;  // no piece split (generator-mode schedule)
+    p.total_items = p.num_items;
+    p.w_hi = static_cast<const __half*>(w_hi);
+    p.w_lo = static_cast<const __half*>(w_lo);
+    p.T_pad = T_pad;
+    CUtensorMap bh, bl;
+    cudaError_t e = make_map(&bh, xi_hi, F, T_pad, p.b_box, true);
+    if (e == cudaSuccess) e = make_map(&bl, xi_lo, F, T_pad, p.b_box, true);
+    if (e != cudaSuccess) return e;
+    return pair ? launch_tc<kALoad, true, true>(bh, bl, bh, bl, p, stream)
+                : launch_tc<kALoad, false, true>(bh, bl, bh, bl, p, stream);
+  }
   CUtensorMap ah, al, bh, bl;
   cudaError_t e = make_map(&ah, w_hi, J, T_pad, kTcM, f16);
   if (e == cudaSuccess) e = make_map(&al, w_lo, J, T_pad, kTcM, f16);
