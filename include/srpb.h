@@ -213,8 +213,10 @@ int srpb_lattice_from_spectra(const float* Y, int F, int M, int Kb, const int32_
  * over lag slots c = n + L, psi generated by PHAT on the fly (3xFP16,
  * tcgen05).  Used for PHAT with the relative floor (speculative + fix-up) and
  * the fp16 split output when Kb % 32 == 0, Kb >= 64 and
- * srpb_lattice_tc_cols(L) <= 64; any other call behaves exactly like
- * srpb_lattice_from_spectra.  Arguments as there, plus
+ * srpb_lattice_tc_cols(L) <= 1024 (beyond 64 slots the lag slots run in passes
+ * of up to 128, each regenerating its rows' psi; frame_counters is then
+ * ignored and the fix-up kernel runs after the passes); any other call
+ * behaves exactly like srpb_lattice_from_spectra.  Arguments as there, plus
  *   tc_b_hi, tc_b_lo  [srpb_lattice_tc_cols(L), 2 Kb] fp16 from
  *                     srpb_lattice_tc_twiddles (both NULL: SIMT path).
  *   frame_counters    [F] int32, zero on entry and left zero (or NULL): the
