@@ -288,3 +288,20 @@ def test_harness_install_rebinds_and_restores():
     assert ns.approximation_error_db is B.approximation_error_db
     restore()
     assert ns.approximation_error_db is stub
+
+
+def test_tensor_core_lattice_shape_rules_without_gpu():
+    """Host-side shape rules of the tensor-core lattice (no launch): lag
+    slots rounded to 16; long lattices (C4: 2L + 1 = 603) are served in passes,
+    C2/C3 in one; beyond 1024 slots or with Kb % 32 != 0 the SIMT lattice
+    serves the call."""
+    _native.load()
+    q = _native.query
+    assert q("srpb_lattice_tc_cols", 301) == 608 and q("srpb_lattice_tc_cols", 9) == 32
+    # C4: 32 mics, 496 pairs, Kb 512, L = 301 (N_aux 2 included), T_pad 143712
+    assert q("srpb_lattice_tc_supported", 32, 496, 512, 301, 143712) == 1
+    # C2: 8 mics, 28 pairs, L = 13; C3: 16 mics, 120 pairs, Kb 1024, L = 23
+    assert q("srpb_lattice_tc_supported", 8, 28, 512, 13, 640) == 1
+    assert q("srpb_lattice_tc_supported", 16, 120, 1024, 23, 3392) == 1
+    assert q("srpb_lattice_tc_supported", 32, 496, 512, 600, 600000) == 0  # > 1024 slots
+    assert q("srpb_lattice_tc_supported", 8, 28, 520, 13, 640) == 0       # Kb % 32 != 0
