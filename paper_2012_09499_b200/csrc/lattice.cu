@@ -16,6 +16,7 @@
 #include "umma.cuh"
 
 #include <cuda_fp16.h>
+#include <type_traits>
 
 namespace srpb {
 
@@ -990,10 +991,17 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
 #pragma unroll
     for (int q = 0; q < 8; ++q)
       xo[q] = (static_cast<uint32_t>((lane >> 2) ^ q) << 4) + static_cast<uint32_t>(lane & 3) * 4u;
-    const int2* ro = sm->rows + kLtRW * g;  // byte offsets of the two spectra rows in the Y tile
+    // byte offsets of the two spectra rows in the Y tile, kept in registers
+    int2 ro[kLtRW];
+#pragma unroll
+    for (int q = 0; q < kLtRW; ++q) ro[q] = sm->rows[kLtRW * g + q];
 #ifdef SRPB_TC_PROFILE
     long long w_y = 0;
 #endif
+    // the floor statistics are written by pass 0 only (the fix-up after the
+    // last pass redoes flagged frames in full): later passes skip them
+    auto gen_loop = [&](auto stats_tag) {
+    constexpr bool kStats = decltype(stats_tag)::value;
     int s = 0, ph = 0;  // stage ring position (no divisions in the loop)
     for (int i = 0; i < my_kb; ++i, s = s + 1 == S ? 0 : s + 1, ph ^= (s == 0)) {
       // the producer loads a stage only after its previous A was consumed
@@ -1018,10 +1026,12 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
         const float pa = fmaf(ya[q].x, ya[q].x, ya[q].y * ya[q].y);
         const float pb = fmaf(yb[q].x, yb[q].x, yb[q].y * yb[q].y);
         const float qq = pa * pb;
-        const bool nz = fminf(pa, pb) != 0.0f;  // pa pb may underflow: test the factors
-        ssum[q] += qq;
-        smin[q] = fminf(smin[q], nz ? qq : 3.0e38f);
-        smax[q] = fmaxf(smax[q], qq);
+        if (kStats) {
+          const bool nz = fminf(pa, pb) != 0.0f;  // pa pb may underflow: test the factors
+          ssum[q] += qq;
+          smin[q] = fminf(smin[q], nz ? qq : 3.0e38f);
+          smax[q] = fmaxf(smax[q], qq);
+        }
         // 1/|raw| = rsqrt(pa pb): exact to fp32 rounding in the range above;
         // frames outside it are redone by the fix-up pass
         const float sc = rsqrt_approx_ftz(fmaxf(qq, 1e-37f)) * kLtScale;
@@ -1037,6 +1047,11 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm->full[s]);
     }
+    };
+    if (blockIdx.y == 0)
+      gen_loop(std::true_type{});
+    else
+      gen_loop(std::false_type{});
     uint32_t sbad = 0;
 #pragma unroll
     for (int q = 0; q < kLtRW; ++q)

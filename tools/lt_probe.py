@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Phase breakdown of the tensor-core lattice kernel (instrumentation build:
-make prof && python tools/lt_probe.py).  Cycles summed over CTAs / warps."""
+make prof && python tools/lt_probe.py [--c4 F]).  Cycles summed over CTAs / warps."""
 import ctypes
 import os
 import sys
@@ -22,12 +22,35 @@ NAMES = {0: "setup", 2: "mma_done(epi view)", 3: "generator loop (per gen warp)"
          6: "cluster_sync wait", 7: "rank0 output + end", 8: "lifetime"}
 
 
+def c4_setup(F):
+    """C4 shapes (32 mics, 496 pairs, 512 bins, N_aux 2): random spectra."""
+    import numpy as np
+    from paper_2012_09499_b200 import scenes
+    from paper_2012_09499_b200.plan import SrpPlan
+
+    rng = np.random.default_rng(np.random.SeedSequence([4, 0, 0]))
+    box = np.array([6.0, 5.0, 3.0])
+    mic = rng.uniform(0.0, 1.0, size=(32, 3)) * box
+    grid = scenes.box_grid(120, 100, 50, box)[:4096]
+    omega = 2.0 * np.pi * np.arange(512) * 16000.0 / 1024
+    plan = SrpPlan.from_geometry(mic, grid, omega, speed_of_sound=343.0,
+                                 sample_period=1 / 16000.0, n_aux=2, weights="onthefly",
+                                 conventional=False)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    Y = torch.complex(torch.randn((F, 32, 512), device="cuda", generator=g),
+                      torch.randn((F, 32, 512), device="cuda", generator=g)).to(torch.complex64)
+    return plan, Y
+
+
 def main():
     from paper_2012_09499_b200 import scenes
 
-    scene = scenes.make_c2()
-    plan = bench.build_plan(scene, 4, torch.device("cuda", 0), weights="stored")
-    Y = torch.from_numpy(scene.Y).cuda()
+    if len(sys.argv) > 1 and sys.argv[1] == "--c4":
+        plan, Y = c4_setup(int(sys.argv[2]) if len(sys.argv) > 2 else 320)
+    else:
+        scene = scenes.make_c2()
+        plan = bench.build_plan(scene, 4, torch.device("cuda", 0), weights="stored")
+        Y = torch.from_numpy(scene.Y).cuda()
     for _ in range(2):
         plan.lattice_from_spectra(Y, split="f16")
     torch.cuda.synchronize()
@@ -44,6 +67,13 @@ def main():
           f"{(c[12] - (M - c[10])) / 1e3:.1f} us")
     for i, name in NAMES.items():
         print(f"  {name:34s} {c[i] / per[i]:10.0f} cycles")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(5):
+        plan.lattice_from_spectra(Y, split="f16")
+    ev[1].record()
+    ev[1].synchronize()
+    print(f"  event time per launch (instrumented build): {ev[0].elapsed_time(ev[1]) / 5 * 1e3:.1f} us")
 
 
 if __name__ == "__main__":
