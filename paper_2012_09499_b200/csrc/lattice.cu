@@ -1022,7 +1022,9 @@ lattice_tc_kernel(const __grid_constant__ CUtensorMap tmB_hi,
       uint8_t* als = a_lo(s) + kLtRW * 128 * g;
 #pragma unroll
       for (int q = 0; q < kLtRW; ++q) {
-        if (a.dbg & 1) continue;
+#ifdef SRPB_TC_PROFILE
+        if (a.dbg & 1) continue;  // (a branch per row: instrumentation build only)
+#endif
         const float pa = fmaf(ya[q].x, ya[q].x, ya[q].y * ya[q].y);
         const float pb = fmaf(yb[q].x, yb[q].x, yb[q].y * yb[q].y);
         const float qq = pa * pb;

@@ -16,36 +16,18 @@ lib = _native.load(os.path.join(ROOT, "paper_2012_09499_b200", "libsrpb_prof.so"
 lib.srpb_lt_profile_read.argtypes = [ctypes.c_void_p]
 
 import bench  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 NAMES = {0: "setup", 2: "mma_done(epi view)", 3: "generator loop (per gen warp)",
          4: "gen wait Y (per gen warp)", 5: "epi wait acc (per epi warp)",
          6: "cluster_sync wait", 7: "rank0 output + end", 8: "lifetime"}
 
 
-def c4_setup(F):
-    """C4 shapes (32 mics, 496 pairs, 512 bins, N_aux 2): random spectra."""
-    import numpy as np
-    from paper_2012_09499_b200 import scenes
-    from paper_2012_09499_b200.plan import SrpPlan
-
-    rng = np.random.default_rng(np.random.SeedSequence([4, 0, 0]))
-    box = np.array([6.0, 5.0, 3.0])
-    mic = rng.uniform(0.0, 1.0, size=(32, 3)) * box
-    grid = scenes.box_grid(120, 100, 50, box)[:4096]
-    omega = 2.0 * np.pi * np.arange(512) * 16000.0 / 1024
-    plan = SrpPlan.from_geometry(mic, grid, omega, speed_of_sound=343.0,
-                                 sample_period=1 / 16000.0, n_aux=2, weights="onthefly",
-                                 conventional=False)
-    g = torch.Generator(device="cuda").manual_seed(0)
-    Y = torch.complex(torch.randn((F, 32, 512), device="cuda", generator=g),
-                      torch.randn((F, 32, 512), device="cuda", generator=g)).to(torch.complex64)
-    return plan, Y
-
-
 def main():
     from paper_2012_09499_b200 import scenes
 
     if len(sys.argv) > 1 and sys.argv[1] == "--c4":
+        from lattice_time import c4_setup
         plan, Y = c4_setup(int(sys.argv[2]) if len(sys.argv) > 2 else 320)
     else:
         scene = scenes.make_c2()
