@@ -133,7 +133,8 @@ def test_lattice_tensor_core_multipass(room, M):
     6x5x3 m room: 13 passes of 64 slots; ~2 passes for the small room):
     vs the SIMT lattice (3e-6) and the reference lattice (1e-5), pad columns
     zero, bitwise repeatable, and speculative-floor edge frames redone by
-    the fix-up kernel after all passes."""
+    the fix-up kernel after all passes (including a tiny channel power the
+    in-place per-channel normalisation of later passes cannot take)."""
     rng = np.random.default_rng(M)
     mic = rng.uniform(0.0, 1.0, size=(M, 3)) * np.array(room)
     pts = rng.uniform(0.0, 1.0, size=(64, 3)) * np.array(room)
@@ -147,6 +148,10 @@ def test_lattice_tensor_core_multipass(room, M):
     Y[2, 1, 7] = 1e-13 + 0j     # floor edge cases (the fix-up redoes the frame)
     Y[3, 0, 3] = 1e-20 + 1e-20j
     Y[4] = 0
+    # a channel power below 1e-30 whose pair products stay above it: later
+    # passes normalise channels in place, so pass 0 must flag the frame
+    Y[5, :, 9] *= 1e3
+    Y[5, 2, 9] = 1e-16 + 0j
     Yd = torch.from_numpy(Y).cuda()
     tc = _xi16(plan, Yd)
     assert np.array_equal(tc, _xi16(plan, Yd))
@@ -160,7 +165,7 @@ def test_lattice_tensor_core_multipass(room, M):
             assert np.all(tc[f] == 0.0)
             continue
         assert rel_l2(tc[f, :total], simt[f, :total]) <= 3e-6, f
-    for f in (0, 2, 3, 20):
+    for f in (0, 2, 3, 5, 20):
         psi = O.cross_spectrum(Y[f].astype(np.complex128), pm, pmp)[0]
         ref = np.concatenate(O.gcc_lattice(psi, omega, bounds, T, 2)[1])
         assert rel_l2(tc[f, :total], ref) <= REL_L2_TOL, f
