@@ -23,10 +23,12 @@ Timing: W untimed warm-ups, then K timed steps bracketed by CUDA events on
 the launching stream; a 256 MiB buffer write flushes L2 before every timed
 step (outside the events; the C4 inputs are larger than L2 anyway).
 Multi-GPU (``--gpus N``; spawned through torch.distributed.run when
-WORLD_SIZE is unset): strong scaling -- the 4096 frames are split into
-contiguous ranges (one per rank, geometry replicated), and every timed step
-ends with the NCCL all-gather of the per-frame maps and argmaxes; barrier +
-synchronize around the timed region, max over ranks.  ``--impl reference``
+WORLD_SIZE is unset): strong scaling -- ``distributed.ShardedRunner`` cuts the
+4096 frames into rounds of whole frame tiles, each rank runs its block of a
+round (geometry replicated) and the round's NCCL all-gather of maps and
+argmaxes runs under the next round's compute; every timed step ends with all
+frames' maps and argmaxes on every rank; barrier + synchronize around the
+timed region, max over ranks.  ``--impl reference``
 times the reference's CPU algorithm (the oracle port in ``oracle/``) on the
 host cores, on bounded samples of the same workload.
 """
@@ -65,6 +67,8 @@ def parse():
     ap.add_argument("--frames", type=int, default=4096, help="C4 frames (BASELINE: 4096)")
     ap.add_argument("--conv-steps", type=int, default=3,
                     help="timed steps of the C4 conventional line (~6 s each)")
+    ap.add_argument("--rounds", type=int, default=4,
+                    help="multi-GPU: rounds per step (gathers overlap the next round)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-sweeps", action="store_true")
@@ -134,8 +138,10 @@ def c4_config(F, plan, world):
         "value_path": "approx (GCC-PHAT fused into the lattice IDFT -> tcgen05 sinc "
                       "interpolation, weights generated in TMEM -> maps + fused argmax)",
         "l2": "flushed before every timed step (256 MiB write); inputs also exceed L2",
-        "parallelism": (f"frame-sharded over {world} GPUs (contiguous frame ranges, geometry "
-                        "replicated, NCCL all-gather of maps + argmax in every step)"
+        "parallelism": (f"frame-sharded over {world} GPUs (ShardedRunner: rounds of whole "
+                        "frame tiles, geometry replicated, each round's NCCL all-gather of "
+                        "maps + argmax overlapped with the next round's compute; every step "
+                        "ends with all frames' results on every rank)"
                         if world > 1 else "1 GPU"),
     }
 
@@ -705,7 +711,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2012_09499_b200 import _native
-    from paper_2012_09499_b200.distributed import frame_ranges, gather_results
+    from paper_2012_09499_b200.distributed import ShardedRunner, frame_ranges
     from paper_2012_09499_b200.pipeline import ChunkedRunner
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -715,7 +721,12 @@ def run_ours(args):
         raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but {torch.cuda.device_count()} GPUs")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # N > 1: frames split over the ranks by ShardedRunner (rounds whose NCCL
+    # all-gathers overlap the next round's compute).  SRPB_BENCH_SHARDED=1
+    # forces that path at any world size (1-GPU check of the NCCL plumbing).
+    sharded = world > 1 or os.environ.get("SRPB_BENCH_SHARDED") == "1"
+    use_pg = world > 1 or (sharded and "WORLD_SIZE" in os.environ)
+    if use_pg:
         dist.init_process_group("nccl", device_id=dev)
     clocks = ClockSampler(local)
     clocks.start()
@@ -741,16 +752,21 @@ def run_ours(args):
         graphs[path] = g
     torch.cuda.synchronize()
 
+    runners = {}
+    if sharded:  # every timed step ends with all frames' maps + argmax on every rank
+        Y_all = torch.from_numpy(scene.Y).pin_memory()
+        for path in ("approx", "conventional"):
+            runners[path] = ShardedRunner(plan, F, M, path, maps=True, rounds=args.rounds)
+            runners[path].load(Y_all)
+        del Y_all
+        torch.cuda.synchronize()
+
     def step(path):
-        def run():
-            maps, am = graphs[path].replay()
-            if world > 1:  # results of all ranks on every rank (NVLink all-gather)
-                gather_results(maps, am, F)
-        return run
+        return runners[path].run if sharded else graphs[path].replay
 
     n0 = _native.launch_count()
     ms_a, _ = timer(step("approx"), args.steps, args.warmup)
-    launches_a = graphs["approx"].launches
+    launches_a = runners["approx"].launches if sharded else graphs["approx"].launches
     ms_c, _ = timer(step("conventional"), args.conv_steps, 1)
     # per-kernel device times (un-captured eager step, events per launch)
     # (one untimed warm-up each: the eager step's first call allocates its
@@ -812,15 +828,18 @@ def run_ours(args):
         "peaks_used": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained")},
     }
     if rank == 0 and not args.no_parity:
-        frames = [0, 1, Fl // 2, Fl - 1]
+        # sharded: the gathered [F, J] maps (global frame order, so a frame
+        # misplaced by the gather fails parity); else this rank's step outputs
+        res = runners if sharded else graphs
+        frames = [0, 1, F // 2, F - 1] if sharded else [0, 1, Fl // 2, Fl - 1]
         out["parity"] = {
-            "approx": parity_block(graphs["approx"].maps, graphs["approx"].argmax, scene, plan,
+            "approx": parity_block(res["approx"].maps, res["approx"].argmax, scene, plan,
                                    frames, 2048, "approx", 2),
-            "conventional": parity_block(graphs["conventional"].maps,
-                                         graphs["conventional"].argmax, scene, plan, frames,
+            "conventional": parity_block(res["conventional"].maps,
+                                         res["conventional"].argmax, scene, plan, frames,
                                          2048, "conventional", 2),
         }
-    del graphs
+    del graphs, runners
     torch.cuda.empty_cache()
     if world == 1 and not args.no_sweeps:
         out["sweeps"] = sweep_lines(timer, dev, args)
@@ -840,7 +859,7 @@ def run_ours(args):
         }
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if use_pg:
         dist.destroy_process_group()
 
 

@@ -158,3 +158,127 @@ def gather_results(maps_local, argmax_local, num_frames, group=None):
     am_all = gather_frames(argmax_local.to(torch.int64), num_frames, group).to(torch.int32)
     m_all = gather_frames(maps_local, num_frames, group) if maps_local is not None else None
     return m_all, am_all
+
+
+def round_widths(per_rank: int, rounds: int = 4, tile: int = 160):
+    """Per-rank frame widths of the rounds of :class:`ShardedRunner`: whole
+    tensor-core frame tiles (``tile`` frames) per round where the frames
+    allow, the leftover frames in the first round and the extra tiles in the
+    earliest rounds -- the last round's gather is the only one no compute
+    hides, so it is the smallest."""
+    per_rank, rounds = int(per_rank), max(1, int(rounds))
+    if per_rank <= 0:
+        return []
+    tiles, rem = divmod(per_rank, tile)
+    if tiles == 0:
+        return [per_rank]
+    rounds = min(rounds, tiles)
+    base, extra = divmod(tiles, rounds)
+    widths = [(base + (1 if c < extra else 0)) * tile for c in range(rounds)]
+    widths[0] += rem
+    return widths
+
+
+class ShardedRunner:
+    """Strong-scaling frame split whose result gathers hide under compute.
+
+    The F frames are cut into rounds; round c covers the global frames
+    ``[W*s_c, W*(s_c + w_c))`` (W ranks, per-rank width ``w_c``, ``s_c`` the
+    widths before it) and rank r runs the r-th ``w_c``-frame block of it as
+    one graph-captured step (``SrpPlan.capture``).  An all-gather of a
+    round's per-rank blocks therefore lands in frame order in the static
+    ``[F, J]`` / ``[F]`` outputs with no padding, concatenation or copy, and
+    it is issued asynchronously (the collective's own stream, NCCL over
+    NVLink) right after the round's replay, so it runs while the next round
+    computes; only the last -- smallest -- round's gather is exposed.
+    ``F % W`` leftover frames run as a one-frame tail on the first ranks and
+    travel through the padded :func:`gather_frames`.
+
+    The reference's only parallelism is a process pool over scenes
+    (``experiment.py:631-641``); this is its replacement for one long batch.
+    """
+
+    def __init__(self, plan, F, M=None, path="approx", maps=True, rounds=4, tile=160,
+                 group=None):
+        self.plan, self.F, self.path, self.want_maps, self.group = plan, int(F), path, maps, group
+        on = self._dist = dist.is_initialized()
+        self.world = dist.get_world_size(group) if on else 1
+        self.rank = dist.get_rank(group) if on else 0
+        W, r = self.world, self.rank
+        base = self.F // W
+        self.tail = self.F - base * W          # < W leftover frames
+        #: (global first frame of the round, per-rank width)
+        self.rounds, s = [], 0
+        for w in round_widths(base, rounds, tile):
+            self.rounds.append((W * s, w))
+            s += w
+        #: this rank's global [lo, hi) frame range per round
+        self.mine = [(g0 + r * w, g0 + (r + 1) * w) for g0, w in self.rounds]
+        self.tail_frame = base * W + r if r < self.tail else None
+        kw = {} if M is None else {"M": M}
+        self.steps = [plan.capture(w, path=path, maps=maps, **kw) for _, w in self.rounds]
+        self.tail_step = plan.capture(1, path=path, maps=maps, **kw) if self.tail else None
+        ref = self.steps[0] if self.steps else self.tail_step
+        dev = ref.argmax.device
+        #: kernels launched by one ``run`` on this rank
+        self.launches = sum(getattr(st, "launches", 0) for st in self.steps) + \
+            (getattr(self.tail_step, "launches", 0) if self.tail_frame is not None else 0)
+        self.argmax = torch.empty((self.F,), dtype=ref.argmax.dtype, device=dev)
+        self.maps = (torch.empty((self.F, ref.maps.shape[1]), dtype=ref.maps.dtype, device=dev)
+                     if maps else None)
+
+    @property
+    def local_frames(self):
+        """Global frame indices this rank computes, in its processing order."""
+        idx = [torch.arange(lo, hi) for lo, hi in self.mine]
+        if self.tail_frame is not None:
+            idx.append(torch.tensor([self.tail_frame]))
+        return torch.cat(idx) if idx else torch.empty(0, dtype=torch.int64)
+
+    def load(self, Y_all):
+        """Copy this rank's frames of ``Y_all`` [F, M, Kb] (host, pinned for an
+        asynchronous copy, or device) into the rounds' static inputs."""
+        for st, (lo, hi) in zip(self.steps, self.mine):
+            st.Y.copy_(Y_all[lo:hi], non_blocking=True)
+        if self.tail_frame is not None:
+            self.tail_step.Y.copy_(Y_all[self.tail_frame:self.tail_frame + 1], non_blocking=True)
+
+    def run(self):
+        """One step over the loaded frames -> (maps [F, J] | None, argmax
+        [F]) of ALL frames on every rank, valid on the current stream."""
+        W, works = self.world, []
+        for st, (g0, w) in zip(self.steps, self.rounds):
+            m, am = st.replay()
+            if not self._dist:   # one process, no group: plain copies
+                self.argmax[g0:g0 + w].copy_(am)
+                if self.want_maps:
+                    self.maps[g0:g0 + w].copy_(m)
+                continue
+            works.append(dist.all_gather_into_tensor(self.argmax[g0:g0 + W * w], am,
+                                                     group=self.group, async_op=True))
+            if self.want_maps:
+                works.append(dist.all_gather_into_tensor(self.maps[g0:g0 + W * w], m,
+                                                         group=self.group, async_op=True))
+        for wk in works:      # the current stream waits for the gathers
+            wk.wait()
+        if self.tail:
+            t0 = self.F - self.tail
+            if self.tail_frame is not None:
+                m, am = self.tail_step.replay()
+            else:             # nothing to run: contributes padding only
+                m = self.maps[:0] if self.want_maps else None
+                am = self.argmax[:0]
+            self.argmax[t0:].copy_(_gather_tail(am, self.tail, W, self.group))
+            if self.want_maps:
+                self.maps[t0:].copy_(_gather_tail(m, self.tail, W, self.group))
+        return self.maps, self.argmax
+
+
+def _gather_tail(local, tail, world, group=None):
+    """Ranks ``< tail`` hold one row each, the others none: all-gather the
+    padded rows and keep the first ``tail``."""
+    pad = torch.zeros((1,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    out = torch.empty((world,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    return out[:tail]

@@ -145,3 +145,89 @@ def test_run_frame_sharded_two_ranks_end_to_end(F):
     ret = mgr.dict()
     mp.spawn(_sharded_worker, args=(2, _free_port(), Y, ret), nprocs=2, join=True)
     assert dict(ret) == {0: True, 1: True}
+
+
+class _StubStep:
+    """CPU stand-in for CapturedStep: static input ``Y``, ``replay()``."""
+
+    def __init__(self, plan, F, M, path, maps):
+        self.plan, self.path, self.want = plan, path, maps
+        self.Y = torch.zeros((F, M, 8), dtype=torch.complex64)
+        self.maps, self.argmax = plan.run(self.Y, path, maps)
+
+    def replay(self):
+        m, a = self.plan.run(self.Y, self.path, self.want)
+        if self.want:
+            self.maps.copy_(m)
+        self.argmax.copy_(a)
+        return self.maps, self.argmax
+
+
+class _StubCapturePlan(_StubPlan):
+    M = 4
+
+    def capture(self, F, M=None, path="approx", maps=True):
+        return _StubStep(self, F, M if M is not None else self.M, path, maps)
+
+
+def test_round_widths():
+    assert D.round_widths(512, 4) == [192, 160, 160]
+    assert D.round_widths(2048, 4) == [608, 480, 480, 480]
+    assert D.round_widths(1024, 4) == [384, 320, 160, 160]
+    assert D.round_widths(4096, 1) == [4096]
+    assert D.round_widths(100, 4) == [100]
+    assert D.round_widths(0, 4) == []
+    for n in (1, 159, 160, 161, 777, 4096):
+        for r in (1, 2, 3, 8):
+            w = D.round_widths(n, r)
+            assert sum(w) == n and all(x > 0 for x in w) and w == sorted(w, reverse=True)
+
+
+def _runner_worker(rank, world, port, Y, rounds, tile, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        plan = _StubCapturePlan()
+        ok = []
+        for path, maps in (("approx", True), ("conventional", True), ("approx", False)):
+            ref_m, ref_a = plan.run(Y, path)
+            rn = D.ShardedRunner(plan, Y.shape[0], path=path, maps=maps, rounds=rounds, tile=tile)
+            rn.load(Y)
+            for _ in range(2):   # static outputs are reusable
+                m, a = rn.run()
+                ok.append(torch.equal(a, ref_a))
+                ok.append(torch.equal(m, ref_m) if maps else m is None)
+            mine = rn.local_frames
+            ok.append(len(mine) in (Y.shape[0] // world, Y.shape[0] // world + 1))
+        # every frame is computed by exactly one rank
+        got = [None] * world
+        dist.all_gather_object(got, mine.tolist())
+        ok.append(sorted(sum(got, [])) == list(range(Y.shape[0])))
+        ret[rank] = all(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("F,rounds,tile", [(64, 4, 8), (37, 3, 4), (5, 4, 160), (1, 2, 160)])
+def test_sharded_runner_two_ranks(F, rounds, tile):
+    """ShardedRunner on 2 gloo ranks (rounds of whole tiles, each round's
+    blocks all-gathered asynchronously into frame order, odd tail frame):
+    maps and argmax of every frame on every rank, identical to one process."""
+    g = torch.Generator().manual_seed(F)
+    Y = torch.complex(torch.randn((F, 4, 8), generator=g), torch.randn((F, 4, 8), generator=g))
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_runner_worker, args=(2, _free_port(), Y, rounds, tile, ret), nprocs=2, join=True)
+    assert dict(ret) == {0: True, 1: True}
+
+
+def test_sharded_runner_single_process():
+    g = torch.Generator().manual_seed(3)
+    Y = torch.complex(torch.randn((50, 4, 8), generator=g), torch.randn((50, 4, 8), generator=g))
+    plan = _StubCapturePlan()
+    rn = D.ShardedRunner(plan, 50, rounds=3, tile=8)
+    rn.load(Y)
+    m, a = rn.run()
+    ref_m, ref_a = plan.run(Y)
+    assert torch.equal(m, ref_m) and torch.equal(a, ref_a)
+    assert [w for _, w in rn.rounds] == [18, 16, 16]
