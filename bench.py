@@ -727,6 +727,9 @@ def run_ours(args):
     sharded = world > 1 or os.environ.get("SRPB_BENCH_SHARDED") == "1"
     use_pg = world > 1 or (sharded and "WORLD_SIZE" in os.environ)
     if use_pg:
+        # stdout carries the one JSON line: NCCL's own log lines (the version
+        # banner when NCCL_DEBUG is set in the environment) go to stderr
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     clocks = ClockSampler(local)
     clocks.start()
