@@ -29,7 +29,8 @@ round (geometry replicated) and the round's NCCL all-gather of maps and
 argmaxes runs under the next round's compute; every timed step ends with all
 frames' maps and argmaxes on every rank; barrier + synchronize around the
 timed region, max over ranks.  ``--impl reference``
-times the reference's CPU algorithm (the oracle port in ``oracle/``) on the
+times the reference's CPU implementation (the unmodified package from
+baseline/_ref through its public API; the oracle port if it is absent) on the
 host cores, on bounded samples of the same workload.
 """
 
@@ -249,9 +250,59 @@ def _cpu_worker(job):
     return t_lat, t_int, t_conv
 
 
+CPU_WHAT = {"reference": "the unmodified reference package (baseline/_ref/srpfast, fp64 numpy) "
+                         "through its public API",
+            "port": "oracle port of the reference (fp64 numpy)"}
+REF_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+
+
+def reference_installed():
+    """The unmodified reference package (pure Python, installed by
+    ``__graft_entry__.build()`` into the git-ignored baseline/_ref)."""
+    return os.path.isfile(os.path.join(REF_DIR, "srpfast", "srp.py"))
+
+
+def cpu_kind():
+    return "reference" if reference_installed() else "port"
+
+
+def _cpu_worker_ref(job):
+    """The same sample as :func:`_cpu_worker`, through the UNMODIFIED
+    reference package's public API (baseline/_ref/srpfast): cross_spectrum ->
+    build_gcc_lattice -> srp_approx -> argmax_candidate per frame
+    (experiment.py:460-484), srp_conventional_frames for the exact maps;
+    the sinc table is precomputed and untimed, as the reference does."""
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from srpfast import geometry as G, spectral as S, srp as R
+
+    Y, mic_pos, pts_sub, pts_conv, omega, n_aux = job
+    arr = G.MicArray(mic_pos, C_SOUND)
+    g_sub = G.build_tdoa_table(arr, G.CandidateGrid("near_field", pts_sub))
+    g_conv = G.build_tdoa_table(arr, G.CandidateGrid("near_field", pts_conv))
+    table = R.precompute_sinc_table(g_sub, arr.pairs, T, n_aux)
+    t_lat = t_int = 0.0
+    crosses = []
+    for f in range(Y.shape[0]):
+        t0 = time.perf_counter()
+        cross = S.cross_spectrum(S.SpectralFrame(Y[f], omega, f), arr.pairs)
+        lat = R.build_gcc_lattice(cross, T, n_aux)
+        t1 = time.perf_counter()
+        R.argmax_candidate(R.srp_approx(lat, table))
+        t2 = time.perf_counter()
+        t_lat += t1 - t0
+        t_int += t2 - t1
+        crosses.append(cross)
+    t0 = time.perf_counter()
+    [R.argmax_candidate(m) for m in R.srp_conventional_frames(crosses, g_conv)]
+    return t_lat, t_int, time.perf_counter() - t0
+
+
 def cpu_sample(scene, n_frames, n_cands, n_aux, procs=1, pool=None, conv_cands=4096):
-    """The reference algorithm (oracle port) on the host cores, on a bounded
-    sample of the workload, extrapolated to the full J x F.
+    """The reference algorithm on the host cores -- the unmodified reference
+    package when baseline/_ref holds it (``kind`` "reference"), else the
+    oracle port -- on a bounded sample of the workload, extrapolated to the
+    full J x F.
 
     approx: cross_spectrum + build_gcc_lattice per frame (J-independent) and
     srp_approx + argmax over ``n_cands`` candidates (sinc table precomputed
@@ -275,16 +326,22 @@ def cpu_sample(scene, n_frames, n_cands, n_aux, procs=1, pool=None, conv_cands=4
     csub = np.sort(np.random.default_rng(8).choice(J, size=min(conv_cands, J), replace=False))
     tdoa_conv = O.tdoa_table_nearfield(scene.mic_pos, scene.grid[csub], pairs, C_SOUND)
     omega = omega_of(scene.frame_length)
-    jobs = [(Y[i * n_frames:(i + 1) * n_frames], pm, pmp, bounds, omega, tdoa_sub, tdoa_conv,
-             n_aux) for i in range(procs)]
+    if reference_installed():
+        worker = _cpu_worker_ref
+        jobs = [(Y[i * n_frames:(i + 1) * n_frames], scene.mic_pos, scene.grid[sub],
+                 scene.grid[csub], omega, n_aux) for i in range(procs)]
+    else:
+        worker = _cpu_worker
+        jobs = [(Y[i * n_frames:(i + 1) * n_frames], pm, pmp, bounds, omega, tdoa_sub,
+                 tdoa_conv, n_aux) for i in range(procs)]
     t0 = time.perf_counter()
     if procs == 1:
-        res = [_cpu_worker(jobs[0])]
+        res = [worker(jobs[0])]
     elif pool is not None:
-        res = pool.map(_cpu_worker, jobs)
+        res = pool.map(worker, jobs)
     else:
         with single_thread_pool(procs) as pl:
-            res = pl.map(_cpu_worker, jobs)
+            res = pl.map(worker, jobs)
     wall = time.perf_counter() - t0
     t_lat = float(np.mean([r[0] for r in res])) / n_frames     # s per frame per process
     t_int = float(np.mean([r[1] for r in res])) / (n_frames * len(sub))  # s per f.c
@@ -292,6 +349,7 @@ def cpu_sample(scene, n_frames, n_cands, n_aux, procs=1, pool=None, conv_cands=4
     approx = procs / (t_lat / J + t_int)                        # f.c/s, all processes
     conv = procs / t_conv
     return {"approx": approx, "conventional": conv, "wall_s": wall, "procs": procs,
+            "kind": cpu_kind(),
             "s_per_frame_lattice": t_lat, "s_per_fc_interp": t_int, "s_per_fc_conv": t_conv,
             "frames": n_frames * procs, "cands": int(len(sub)), "conv_cands": int(len(csub))}
 
@@ -357,7 +415,7 @@ def run_reference(args):
             walls.append(r["wall_s"])
     value = float(np.median(vals))
     J = scene.grid.shape[0]
-    sample = (f"per step: {procs} C4 frames (one per process, 1 BLAS thread each, "
+    sample = (f"{CPU_WHAT[cpu_kind()]}; per step: {procs} C4 frames (one per process, 1 BLAS thread each, "
               f"experiment.py:631-641 sharding) x lattice of all 496 pairs + interpolation "
               f"over {args.cpu_cands} and conventional over {args.cpu_conv_cands} of the {J} "
               "candidates; full-J cost "
@@ -369,7 +427,7 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C4 (BASELINE configs[3]), as the GPU arm", "frames": 4096,
                    "candidates": J, "n_aux": n_aux},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": cpu_kind(),
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "conventional": {"value": float(np.median(convs)), "unit": UNIT},
@@ -851,8 +909,8 @@ def run_ours(args):
         best, one, shard, cores = cpu_baseline(scene, args, 2)
         out["cpu_baseline"] = {
             "value": best["approx"], "unit": UNIT,
-            "cores": cores if best is shard else os.cpu_count(), "kind": "port",
-            "sample": (f"C4, oracle port of the reference (fp64 numpy): {best['frames']} frames "
+            "cores": cores if best is shard else os.cpu_count(), "kind": cpu_kind(),
+            "sample": (f"C4, {CPU_WHAT[cpu_kind()]}: {best['frames']} frames "
                        f"x lattice of all pairs + interpolation over {best['cands']} candidates, "
                        f"extrapolated to J={J} (cost linear in J); setting "
                        f"{'(ii) frames sharded over %d processes, 1 BLAS thread each' % best['procs'] if best is shard else '(i) one process, all BLAS threads'}"
