@@ -492,7 +492,8 @@ def roofline_entry(kms, plan, F, path, peaks, traffic_file="r2_traffic.json"):
         key = f"{name}@{path}"
         if key in tr or name in tr:
             entry["traffic"] = tr.get(key, tr.get(name))
-            entry["traffic_unit"] = f"DRAM bytes/launch (profiles/{traffic_file}, ncu --set full)"
+            entry["traffic_unit"] = (f"DRAM bytes/launch (profiles/{traffic_file}: ncu "
+                                     "dram__bytes_read.sum + dram__bytes_write.sum)")
     except (OSError, ValueError):
         pass
     return entry
