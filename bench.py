@@ -501,6 +501,33 @@ def roofline_entry(kms, plan, F, path, peaks, traffic_file="r2_traffic.json"):
     return entry
 
 
+def step_roofline(ms, plan, F, path, peaks, maps=True):
+    """Whole-step roofline of a sweep line (all the step's kernels in `ms`):
+    the step's algorithmic flops against the 3xFP16 tensor peak (bf16 / 3;
+    sustained figure for steps >= 100 ms) and its compulsory HBM bytes (the
+    stored fp16 hi/lo weight table or the TDOA split read once, spectra in,
+    maps out) against the measured HBM peak; `bound` names the larger floor."""
+    bf16 = (peaks.get("bf16_tflops_sustained") if ms >= 100.0 else None) or \
+        peaks.get("bf16_tflops") or 1590.0
+    hbm = peaks.get("hbm_gbs") or 6500.0
+    J = plan.J
+    if path == "approx":
+        flops = 2.0 * plan.total_samples * F * J
+        table = 4.0 * J * plan.T_pad if plan.weight_mode == "stored" else 8.0 * J * plan.P
+    else:
+        flops = 4.0 * plan.P * plan.Kb * F * J
+        table = 8.0 * J * plan.P
+    nbytes = table + 8.0 * F * plan.M * plan.Kb + (4.0 * F * J if maps else 0.0)
+    t_tensor = flops / (bf16 / 3.0 * 1e12)
+    t_hbm = nbytes / (hbm * 1e9)
+    sec = ms * 1e-3
+    return {"roofline": {"bound": "tensor" if t_tensor >= t_hbm else "hbm",
+                         "tensor_tflops": flops / sec / 1e12, "tensor_frac": t_tensor / sec,
+                         "hbm_gbs": nbytes / sec / 1e9, "hbm_frac": t_hbm / sec,
+                         "frac": max(t_tensor, t_hbm) / sec,
+                         "peaks": {"tflops_3xfp16": bf16 / 3.0, "hbm_gbs": hbm}}}
+
+
 # ------------------------------------------------------------------ parity
 def parity_block(maps_dev, am_dev, scene, plan, frames, n_cands, path, n_aux, seed=11):
     """GPU maps vs the oracle (fp64 reference algorithm) on ``frames`` x a
@@ -696,7 +723,7 @@ def dropin_line(dev, n_frames=64):
     return res
 
 
-def sweep_lines(timer, dev, args):
+def sweep_lines(timer, dev, args, peaks):
     """Driver-visible lines for the other BASELINE configs (graph replay,
     inputs resident, 2 warm-ups + a few timed steps each)."""
     import torch
@@ -728,12 +755,14 @@ def sweep_lines(timer, dev, args):
         ms, _ = timer(cap.replay, 10, 2)
         c2[f"approx_naux{n_aux}"] = {"value": Y.shape[0] * plan.J / (ms * 1e-3), "ms": ms,
                                      "lattice_samples": plan.total_samples, "steps": 10,
+                                     **step_roofline(ms, plan, Y.shape[0], "approx", peaks),
                                      **par(cap, sc, plan, "approx", n_aux)}
         if n_aux == 4:
             capc = plan.capture(Y.shape[0], Y.shape[1], "conventional")
             capc.Y.copy_(Y)
             ms, _ = timer(capc.replay, 5, 2)
             c2["conventional"] = {"value": Y.shape[0] * plan.J / (ms * 1e-3), "ms": ms, "steps": 5,
+                                  **step_roofline(ms, plan, Y.shape[0], "conventional", peaks),
                                   **par(capc, sc, plan, "conventional", n_aux)}
             del capc
         del cap, plan
@@ -751,12 +780,14 @@ def sweep_lines(timer, dev, args):
         ms, _ = timer(cap.replay, 5, 2)
         c3[f"approx_naux{n_aux}"] = {"value": Y.shape[0] * plan.J / (ms * 1e-3), "ms": ms,
                                      "lattice_samples": plan.total_samples, "steps": 5,
+                                     **step_roofline(ms, plan, Y.shape[0], "approx", peaks),
                                      **par(cap, sc, plan, "approx", n_aux)}
         if n_aux == 0:
             capc = plan.capture(Y.shape[0], Y.shape[1], "conventional")
             capc.Y.copy_(Y)
             ms, _ = timer(capc.replay, 3, 1)
             c3["conventional"] = {"value": Y.shape[0] * plan.J / (ms * 1e-3), "ms": ms, "steps": 3,
+                                  **step_roofline(ms, plan, Y.shape[0], "conventional", peaks),
                                   **par(capc, sc, plan, "conventional", n_aux)}
             del capc
         del cap, plan
@@ -779,7 +810,7 @@ def sweep_lines(timer, dev, args):
             steps = 10 if B <= 256 else 3
             ms, _ = timer(cap.replay, steps, 2 if B <= 4096 else 1)
             row[path] = {"ms": ms, "value": B * plan.J / (ms * 1e-3), "steps": steps,
-                         "maps": not big}
+                         "maps": not big, **step_roofline(ms, plan, B, path, peaks, not big)}
             if not big:
                 row[path].update(par(cap, sc, plan, path, 4))
                 if B == 4096:
@@ -948,7 +979,7 @@ def run_ours(args):
     del graphs, runners
     torch.cuda.empty_cache()
     if world == 1 and not args.no_sweeps:
-        out["sweeps"] = sweep_lines(timer, dev, args)
+        out["sweeps"] = sweep_lines(timer, dev, args, peaks)
     out["clocks"] = clocks.stop()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         best, one, shard, cores = cpu_baseline(scene, args, 2)
