@@ -305,3 +305,37 @@ def test_tensor_core_lattice_shape_rules_without_gpu():
     assert q("srpb_lattice_tc_supported", 16, 120, 1024, 23, 3392) == 1
     assert q("srpb_lattice_tc_supported", 32, 496, 512, 600, 600000) == 0  # > 1024 slots
     assert q("srpb_lattice_tc_supported", 8, 28, 520, 13, 640) == 0       # Kb % 32 != 0
+
+
+# ------------------------------------------------------- bench.py host logic
+def test_bench_step_roofline_bounds_and_fractions():
+    """Per-sweep-line roofline of bench.py: tensor floor = algorithmic flops /
+    (bf16 peak / 3), HBM floor = weight table + spectra + maps / HBM peak."""
+    import types
+
+    import bench
+
+    peaks = {"hbm_gbs": 6500.0, "bf16_tflops": 1600.0, "bf16_tflops_sustained": 1400.0}
+    c5 = types.SimpleNamespace(J=200000, total_samples=596, T_pad=608, weight_mode="stored",
+                               P=28, Kb=512, M=8)
+    r = bench.step_roofline(0.115, c5, 1, "approx", peaks)["roofline"]
+    assert r["bound"] == "hbm"          # batch 1 streams the weight table once
+    nbytes = 4 * 200000 * 608 + 8 * 8 * 512 + 4 * 200000
+    assert math.isclose(r["hbm_gbs"], nbytes / 0.115e-3 / 1e9, rel_tol=1e-12)
+    assert math.isclose(r["frac"], r["hbm_frac"]) and 0 < r["frac"] < 1
+    r = bench.step_roofline(2.6, c5, 4096, "approx", peaks)["roofline"]
+    assert r["bound"] == "tensor"
+    assert math.isclose(r["tensor_tflops"], 2 * 596 * 4096 * 200000 / 2.6e-3 / 1e12, rel_tol=1e-12)
+    assert math.isclose(r["peaks"]["tflops_3xfp16"], 1600.0 / 3)   # short step: burst peak
+    r = bench.step_roofline(1750.0, c5, 65536, "conventional", peaks, maps=False)["roofline"]
+    assert math.isclose(r["peaks"]["tflops_3xfp16"], 1400.0 / 3)   # long step: sustained peak
+    assert math.isclose(r["tensor_tflops"], 4 * 28 * 512 * 65536 * 200000 / 1.75 / 1e12,
+                        rel_tol=1e-12)
+
+
+def test_bench_reference_arm_uses_installed_reference_when_present():
+    import bench
+
+    assert bench.cpu_kind() in ("reference", "port")
+    assert (bench.cpu_kind() == "reference") == os.path.isfile(
+        os.path.join(bench.REF_DIR, "srpfast", "srp.py"))
