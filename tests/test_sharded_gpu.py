@@ -63,3 +63,22 @@ def test_sharded_runner_nccl_one_rank(nccl_one_rank, path, key, amkey):
     m2, a2 = rn2.run()
     torch.cuda.synchronize()
     assert m2 is None and torch.equal(a2, ref_a)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_plan_on_a_non_current_device():
+    """A plan built with ``device='cuda:1'`` launches on that GPU (the C-ABI
+    calls run under ``torch.cuda.device``), whatever the current device is."""
+    with np.load(GOLDEN) as z:
+        g = {k: z[k] for k in z.files}
+    torch.cuda.set_device(0)
+    plan = SrpPlan(g["tdoa"], g["pair_m"], g["pair_mp"], g["bounds"], g["omega"],
+                   sample_period=1.0 / 16000.0, n_aux=2, device="cuda:1")
+    Y = torch.as_tensor(g["Y"]).to("cuda:1")
+    for path, key, amkey in (("approx", "approx_2", "argmax_approx_2"),
+                             ("conventional", "conv", "argmax_conv")):
+        maps, am = plan.run(Y, path)
+        torch.cuda.synchronize("cuda:1")
+        assert maps.device == torch.device("cuda", 1) and torch.cuda.current_device() == 0
+        assert_maps_match(maps.cpu().numpy(), g[key], am.cpu().numpy(), what=f"cuda:1 {path}")
+        assert list(am.cpu().numpy()) == list(g[amkey])
