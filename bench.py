@@ -72,6 +72,11 @@ def parse():
                     help="multi-GPU: rounds per step (gathers overlap the next round)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--parity-frames", type=int, default=4,
+                    help="headline parity block: frames compared with the oracle (evenly "
+                         "spread, first and last included)")
+    ap.add_argument("--parity-cands", type=int, default=2048,
+                    help="headline parity block: seeded candidate subset size")
     ap.add_argument("--no-sweeps", action="store_true")
     ap.add_argument("--cpu-frames", type=int, default=2,
                     help="C4 frames in the CPU sample (per process)")
@@ -968,13 +973,17 @@ def run_ours(args):
         # sharded: the gathered [F, J] maps (global frame order, so a frame
         # misplaced by the gather fails parity); else this rank's step outputs
         res = runners if sharded else graphs
-        frames = [0, 1, F // 2, F - 1] if sharded else [0, 1, Fl // 2, Fl - 1]
+        Fp = F if sharded else Fl
+        if args.parity_frames <= 4:
+            frames = [0, 1, Fp // 2, Fp - 1]
+        else:
+            frames = sorted({int(x) for x in np.linspace(0, Fp - 1, args.parity_frames)})
         out["parity"] = {
             "approx": parity_block(res["approx"].maps, res["approx"].argmax, scene, plan,
-                                   frames, 2048, "approx", 2),
+                                   frames, args.parity_cands, "approx", 2),
             "conventional": parity_block(res["conventional"].maps,
                                          res["conventional"].argmax, scene, plan, frames,
-                                         2048, "conventional", 2),
+                                         args.parity_cands, "conventional", 2),
         }
     del graphs, runners
     torch.cuda.empty_cache()
