@@ -21,6 +21,7 @@ from .geometry import (
     tdoa_farfield,
     tdoa_nearfield,
 )
+from .distributed import ShardedRunner, run_candidate_sharded, run_frame_sharded
 from .metrics import APPROX_ERROR_FLOOR_DB, approximation_error_db, map_error_energy
 from .pipeline import ChunkedRunner, chunk_bounds
 from .plan import CapturedStep, SrpPlan, lattice_layout, standalone_argmax
@@ -60,6 +61,7 @@ __version__ = "0.1.0"
 __all__ = [
     "CapturedStep",
     "ChunkedRunner",
+    "ShardedRunner", "run_frame_sharded", "run_candidate_sharded",
     "chunk_bounds",
     "CandidateGrid", "MicArray", "MicPair", "build_tdoa_table", "circular_array",
     "enumerate_pairs", "tdoa_farfield", "tdoa_nearfield",
