@@ -400,10 +400,21 @@ def cpu_baseline(scene, args, n_aux):
     return best, one, shard, cores
 
 
+def claim_stdout():
+    """stdout carries exactly ONE JSON line: file descriptor 1 is pointed at
+    stderr for the rest of the process (NCCL's version banner, any library
+    print), and the returned stream -- the original stdout -- gets the line."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    return os.fdopen(saved, "w")
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return  # the reference arm runs on rank 0 only
+    real_stdout = claim_stdout()
     scene = c4_scene(max(args.cpu_frames, 16))
     n_aux = 2
     cores = os.cpu_count() or 1
@@ -437,7 +448,7 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "conventional": {"value": float(np.median(convs)), "unit": UNIT},
     }
-    print(json.dumps(out), flush=True)
+    print(json.dumps(out), file=real_stdout, flush=True)
 
 
 # ------------------------------------------------------------------ roofline
@@ -851,6 +862,7 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    real_stdout = claim_stdout()
     if torch.cuda.device_count() <= local:
         raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but {torch.cuda.device_count()} GPUs")
     torch.cuda.set_device(local)
@@ -861,9 +873,6 @@ def run_ours(args):
     sharded = world > 1 or os.environ.get("SRPB_BENCH_SHARDED") == "1"
     use_pg = world > 1 or (sharded and "WORLD_SIZE" in os.environ)
     if use_pg:
-        # stdout carries the one JSON line: NCCL's own log lines (the version
-        # banner when NCCL_DEBUG is set in the environment) go to stderr
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=dev)
     clocks = ClockSampler(local)
     clocks.start()
@@ -1004,7 +1013,7 @@ def run_ours(args):
             "settings": {"i_one_process": one, "ii_sharded": shard},
         }
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out), file=real_stdout, flush=True)
     if use_pg:
         dist.destroy_process_group()
 
