@@ -6,6 +6,7 @@ group.  The reference arm prints its line with ``impl: reference``."""
 
 import json
 import os
+import socket
 import subprocess
 import sys
 
@@ -52,9 +53,12 @@ def test_bench_line_contract_small():
 
 def test_bench_sharded_path_one_rank_nccl():
     env = dict(os.environ, SRPB_BENCH_SHARDED="1")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
     out = subprocess.run(
         [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
-         "--master-addr", "127.0.0.1", "--master-port", "29617",
+         "--master-addr", "127.0.0.1", "--master-port", str(port),
          os.path.join(ROOT, "bench.py"), "--gpus", "1", *SMALL],
         capture_output=True, text=True, cwd=ROOT, env=env, timeout=900)
     assert out.returncode == 0, out.stderr[-3000:]
