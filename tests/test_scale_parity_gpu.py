@@ -148,3 +148,27 @@ def test_c5_batches_full_grid_vs_oracle(batch):
     refc = oracle_conventional(scene, fr, cand)
     assert_maps_match(mc[fr].cpu().numpy(), refc, ac[fr].cpu().numpy(),
                       what=f"C5 conv batch {batch}")
+
+
+def test_c5_large_batch_argmax_only_vs_oracle():
+    """The mode of C5's 65536 batch (maps never materialised, only the fused
+    in-kernel argmax leaves the kernels) at 2,048 frames on the full 200k
+    grid: the argmax of sampled frames equals the oracle's over all
+    candidates, and the whole batch equals the maps path's argmax."""
+    batch = 2048
+    scene = scenes.make_c5(batch)
+    plan = device_plan(scene, 4, weights="stored")
+    Y = torch.from_numpy(scene.Y).cuda()
+    cand = np.arange(plan.J)
+    frames = [0, 1023, 1024, 2047]
+    for path in ("approx", "conventional"):
+        none, am = plan.run(Y, path, maps=False)
+        assert none is None and am.shape == (batch,)
+        maps, am_maps = plan.run(Y, path)
+        assert torch.equal(am, am_maps) and torch.equal(am.long(), torch.argmax(maps, dim=1))
+        fr = frames if path == "approx" else frames[:1]
+        ref = (oracle_approx(scene, fr, cand, 4, chunk=50000) if path == "approx"
+               else oracle_conventional(scene, fr, cand))
+        assert_maps_match(maps[fr].cpu().numpy(), ref, am[fr].cpu().numpy(),
+                          what=f"C5 {path} argmax-only batch {batch}")
+        del maps
