@@ -148,11 +148,12 @@ def _device_psi(crosses, device=None):
         if idx == list(range(t.shape[0])):
             return t
         return t[torch.as_tensor(idx, device=dev)].contiguous()
-    return torch.stack([
+    vals = [
         c.device_values(dev) if isinstance(c, CrossSpectra)
         else torch.as_tensor(np.ascontiguousarray(c.values, dtype=np.complex64), device=dev)
         for c in crosses
-    ]).contiguous()
+    ]
+    return (vals[0][None] if len(vals) == 1 else torch.stack(vals)).contiguous()
 
 
 def gcc_at_lag(cross, pair_index: int, lag: float) -> float:
@@ -258,11 +259,31 @@ class GccLattice:
 _LATTICE_PLANS: dict = {}
 
 
-def _lattice_plan(pairs, omega, sample_period, n_aux, device):
+#: pair-derived parts of the key, built once per immutable pairs tuple (a
+#: per-frame harness passes the same tuple every frame); keyed on identity
+_PAIR_KEYS: dict = {}
+
+
+def _pair_key(pairs):
+    """(bounds fp64, pair_m int32, pair_mp int32, key bytes) of ``pairs``."""
+    if isinstance(pairs, tuple):
+        e = _PAIR_KEYS.get(id(pairs))
+        if e is not None and e[0] is pairs:
+            return e[1]
     bounds = np.array([p.tdoa_bound for p in pairs], dtype=np.float64)
     pm = np.array([p.index_m for p in pairs], dtype=np.int32)
     pmp = np.array([p.index_m_prime for p in pairs], dtype=np.int32)
-    key = (bounds.tobytes(), pm.tobytes(), pmp.tobytes(), np.asarray(omega).tobytes(),
+    val = (bounds, pm, pmp, bounds.tobytes() + pm.tobytes() + pmp.tobytes())
+    if isinstance(pairs, tuple):
+        if len(_PAIR_KEYS) >= 16:
+            _PAIR_KEYS.clear()
+        _PAIR_KEYS[id(pairs)] = (pairs, val)   # holds `pairs`: the id cannot be reused
+    return val
+
+
+def _lattice_plan(pairs, omega, sample_period, n_aux, device):
+    bounds, pm, pmp, pkey = _pair_key(pairs)
+    key = (pkey, np.asarray(omega).tobytes(),
            float(sample_period), int(n_aux), str(device))
     plan = _LATTICE_PLANS.get(key)
     if plan is None:
@@ -283,7 +304,10 @@ def build_gcc_lattice_frames(crosses, sample_period, n_aux, counter=None, device
     if not crosses:
         return []
     pairs = crosses[0].pairs
-    halves = lattice_half_counts(pairs, sample_period)
+    if not (sample_period > 0 and math.isfinite(sample_period)):
+        raise ValueError(f"sample_period must be positive, got {sample_period}")
+    # floor(bound / T) per pair (srp.py:123-134) from the cached bounds row
+    halves = tuple(np.floor(_pair_key(pairs)[0] / sample_period).astype(np.int64).tolist())
     dev = N.require_cuda(device)
     plan = _lattice_plan(pairs, crosses[0].bin_frequencies, sample_period, int(n_aux), dev)
     psi = _device_psi(crosses, dev)
@@ -406,6 +430,8 @@ def srp_approx_frames(lattices, table, counter=None, maps=True):
         xi = rows[0].tensor
         if idx != list(range(xi.shape[0])):
             xi = xi[torch.as_tensor(idx, device=dev)].contiguous()
+    elif len(lattices) == 1:
+        xi = lattices[0].device_row(plan.T_pad, dev)[None].contiguous()
     else:
         xi = torch.stack([l.device_row(plan.T_pad, dev) for l in lattices]).contiguous()
     kbs = {getattr(l, "_bounded", 0) for l in lattices}
