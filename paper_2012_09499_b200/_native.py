@@ -141,7 +141,22 @@ def ptr(t):
     return t.data_ptr()
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle(device=None):
+    """``cudaStream_t`` of torch's current stream on ``device`` (an int).
+    The raw getter skips the Stream object the public call builds (several
+    lookups per frame on the per-frame drop-in path)."""
+    if _raw_stream is not None:
+        idx = getattr(device, "index", None) if device is not None else None
+        if isinstance(device, int):
+            idx = device
+        if idx is None:
+            if device is not None and not isinstance(device, torch.device):
+                return torch.cuda.current_stream(device).cuda_stream
+            idx = torch.cuda.current_device()
+        return _raw_stream(idx)
     return torch.cuda.current_stream(device).cuda_stream
 
 
